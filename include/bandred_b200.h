@@ -1,0 +1,118 @@
+/*
+ * bandred_b200 — C ABI of the B200-native (sm_100a) first-stage band
+ * reduction: dense symmetric -> symmetric band (SEVP) and dense general ->
+ * upper triangular-band (SVD), arXiv 1709.00302, with static look-ahead.
+ *
+ * Every entry point replaces one function of the reference package
+ * `bandred` (paths relative to the reference's pkg/src/bandred/); the
+ * reference-side binding a maintainer would add is in INTEGRATION.md.
+ *
+ * Conventions (all functions):
+ *   - fp64, column-major, leading dimensions in elements, sizes int64_t;
+ *   - device pointers unless the name ends in _host;
+ *   - work is enqueued on the handle's streams; kernel-level calls run on
+ *     the handle's main stream and are asynchronous (call br_sync), the
+ *     reductions return after the device work completed;
+ *   - return 0 on success, -i when argument i is invalid (LAPACK style,
+ *     Python raises ValueError), >0 on a CUDA/NCCL failure (RuntimeError);
+ *     br_last_error() gives the message. No exception crosses the ABI.
+ *   - Reflector conventions follow the reference exactly: beta =
+ *     -sign(x0)*||x|| with x0 == 0 counted positive, tau = 2 for a zero
+ *     tail, tau = beta = 0 for a zero vector; Q = I + W*Y^T with W = Y*T
+ *     (T = -T_larft).
+ */
+#ifndef BANDRED_B200_H
+#define BANDRED_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct br_handle_s* br_handle_t;
+
+/* Statistics filled by the reductions (nullable). */
+typedef struct br_stats {
+  int64_t iterations;   /* panels factored (ref SevpResult/SvdResult.iterations) */
+  double device_ms;     /* device time of the reduction proper (CUDA events) */
+  double nominal_flops; /* 4n^3/3 (SEVP) or 4(mn^2 - n^3/3) (SVD) */
+  int64_t launches;     /* kernels launched by the reduction */
+} br_stats;
+
+/* ---- context ---------------------------------------------------------- */
+int br_version(void);
+const char* br_last_error(void);
+/* Create a context on `device` with its own main/panel streams (the panel
+ * stream has the higher priority: look-ahead factorizations win SMs). */
+int br_create(int device, br_handle_t* out);
+int br_destroy(br_handle_t h);
+/* Use caller-owned streams (cudaStream_t passed as void*); NULL keeps the
+ * handle's own. */
+int br_set_streams(br_handle_t h, void* main_stream, void* panel_stream);
+int br_sync(br_handle_t h);
+/* Per-kernel-class CUDA-event timing of subsequent reductions (bench). */
+int br_set_timing(br_handle_t h, int enable);
+/* Class: 0 = panel, 1 = symm, 2 = syr2k, 3 = gemm (other updates).
+ * Accumulated since br_set_timing(h, 1). */
+int br_get_timing(br_handle_t h, int cls, double* ms, double* flops, int64_t* launches);
+
+/* ---- kernel level (ref kernels.py) ------------------------------------ */
+/* house_gen (kernels.py:86-110): v (L) and tau_beta = {tau, beta}. */
+int br_house_gen(br_handle_t h, int64_t L, const double* x, double* v, double* tau_beta);
+/* qr_panel (kernels.py:165-208): in-place QR of the j x b panel P; R into
+ * P's top triangle; Y (j x b), T (b x b), W (j x b, nullable), tau (b). */
+int br_qr_panel(br_handle_t h, int64_t j, int64_t b, double* P, int64_t ldp, double* Y,
+                int64_t ldy, double* T, int64_t ldt, double* W, int64_t ldw, double* tau);
+/* lq_panel (kernels.py:211-255): in-place LQ of the b x j panel P; L into
+ * P's left triangle; Y (j x b), T, W, tau as for QR. */
+int br_lq_panel(br_handle_t h, int64_t b, int64_t j, double* P, int64_t ldp, double* Y,
+                int64_t ldy, double* T, int64_t ldt, double* W, int64_t ldw, double* tau);
+/* build_w (kernels.py:139-149): W = Y T. */
+int br_build_w(br_handle_t h, int64_t j, int64_t b, const double* Y, int64_t ldy,
+               const double* T, int64_t ldt, double* W, int64_t ldw);
+/* apply_wy_left (kernels.py:258-284): A (rows x cols) += Y (W^T A). */
+int br_apply_wy_left(br_handle_t h, int64_t rows, int64_t cols, double* A, int64_t lda,
+                     const double* Y, int64_t ldy, const double* W, int64_t ldw, int64_t b);
+/* apply_wy_right (kernels.py:287-309): A (rows x cols) += (A W) Y^T. */
+int br_apply_wy_right(br_handle_t h, int64_t rows, int64_t cols, double* A, int64_t lda,
+                      const double* Y, int64_t ldy, const double* W, int64_t ldw, int64_t b);
+/* symm_lower (kernels.py:312-341): X1 = sym(A2) W, A2 lower-only. */
+int br_symm_lower(br_handle_t h, int64_t j, int64_t b, const double* A2, int64_t lda,
+                  const double* W, int64_t ldw, double* X1, int64_t ldx);
+/* syr2k_lower (kernels.py:344-378): A2[:, c0:c1] += X3 Y^T + Y X3^T, lower. */
+int br_syr2k_lower(br_handle_t h, int64_t j, int64_t b, double* A2, int64_t lda,
+                   const double* X3, int64_t ldx, const double* Y, int64_t ldy, int64_t c0,
+                   int64_t c1);
+/* sym_two_sided_update (kernels.py:381-401): A2 := Q^T A2 Q, lower only. */
+int br_sym_two_sided_update(br_handle_t h, int64_t j, int64_t b, double* A2, int64_t lda,
+                            const double* Y, int64_t ldy, const double* W, int64_t ldw);
+
+/* ---- reductions --------------------------------------------------------- */
+/* reduce_sym_band (sevp.py:287-324) on a device matrix, in place. Reads
+ * only the lower triangle; on return A holds the finalized band (mirrored,
+ * off-band exactly zero). lookahead: 0 = reference schedule, 1 = next panel
+ * factored on the panel stream while the trailing update finishes (V1/V2).
+ * Q (nullable, n x n) receives the accumulated orthogonal factor
+ * (accumulate_q, sevp.py:138-144). If n <= w+1 nothing is done. */
+int br_reduce_sym_band(br_handle_t h, int64_t n, int64_t w, int64_t b, int lookahead, double* A,
+                       int64_t lda, double* Q, int64_t ldq, br_stats* stats);
+/* reduce_tri_band (svd.py:179-247) on a device m x n matrix, m >= n, in
+ * place: upper triangular-band with bandwidth w, everything else exactly 0.
+ * lookahead 1 overlaps the LQ / next QR panels with the rank-b updates
+ * (extension: the reference schedule is sequential, results identical). */
+int br_reduce_tri_band(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b, int lookahead,
+                       double* A, int64_t lda, br_stats* stats);
+/* Host-buffer variants: copy A (host, lda) to the device, reduce, copy the
+ * band back to `band` (host, ldb). Host buffers may be pageable or pinned. */
+int br_reduce_sym_band_host(br_handle_t h, int64_t n, int64_t w, int64_t b, int lookahead,
+                            const double* A, int64_t lda, double* band, int64_t ldb, double* Q,
+                            int64_t ldq, br_stats* stats);
+int br_reduce_tri_band_host(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b,
+                            int lookahead, const double* A, int64_t lda, double* band,
+                            int64_t ldb, br_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BANDRED_B200_H */

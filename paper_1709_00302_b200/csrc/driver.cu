@@ -1,0 +1,582 @@
+// Context, workspace, elementwise kernels and the C ABI (include/bandred_b200.h).
+#include <algorithm>
+#include <cstdarg>
+#include <cstring>
+#include <atomic>
+#include <new>
+
+#include "../../include/bandred_b200.h"
+#include "driver.cuh"
+#include "gemm.cuh"
+
+namespace br {
+
+static thread_local char g_err[1024] = "";
+static std::atomic<int64_t> g_launches{0};
+int64_t launch_count() { return g_launches.load(); }
+void count_launch(int64_t n) { g_launches += n; }
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int devbuf_reserve(DevBuf& b, int64_t n) {
+  if (n <= b.cap) return 0;
+  if (b.p) {
+    BR_CUDA(cudaDeviceSynchronize());
+    BR_CUDA(cudaFree(b.p));
+    b.p = nullptr;
+    b.cap = 0;
+  }
+  BR_CUDA(cudaMalloc(&b.p, (size_t)n * sizeof(double)));
+  b.cap = n;
+  return 0;
+}
+void devbuf_free(DevBuf& b) {
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+}
+
+cudaEvent_t ws_event(Workspace& ws) {
+  if (ws.event_next == ws.events.size()) {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    ws.events.push_back(e);
+  }
+  return ws.events[ws.event_next++];
+}
+void ws_events_reset(Workspace& ws) { ws.event_next = 0; }
+
+static cudaEvent_t ws_tevent(Workspace& ws) {
+  if (ws.tevent_next == ws.tevents.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    ws.tevents.push_back(e);
+  }
+  return ws.tevents[ws.tevent_next++];
+}
+
+TimeScope::TimeScope(Workspace& w, cudaStream_t s, int c, double f) : ws(w), st(s), cls(c), flops(f) {
+  if (ws.timing) {
+    a = ws_tevent(ws);
+    cudaEventRecord(a, st);
+  }
+}
+TimeScope::~TimeScope() {
+  if (ws.timing) {
+    cudaEvent_t b = ws_tevent(ws);
+    cudaEventRecord(b, st);
+    ws.timed.push_back({cls, a, b, flops});
+  }
+}
+
+int ws_collect_timing(Workspace& ws) {
+  for (auto& t : ws.timed) {
+    float ms = 0.f;
+    BR_CUDA(cudaEventElapsedTime(&ms, t.a, t.b));
+    ws.t_ms[t.cls] += ms;
+    ws.t_flops[t.cls] += t.flops;
+    ws.t_launches[t.cls] += 1;
+  }
+  ws.timed.clear();
+  ws.tevent_next = 0;
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// elementwise kernels
+// ---------------------------------------------------------------------------
+
+// In-place finalize of the SEVP band (ref sevp.py:276-284): lower in-band
+// entries kept, upper in-band entries mirrored from the lower triangle,
+// everything with |i-j| > w set to exactly 0. Upper entries are only
+// written, never read, so the input's upper triangle is never observed.
+__global__ void finalize_sym_kernel(double* A, int64_t lda, int64_t n, int64_t w) {
+  const int64_t total = n * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx % n, c = idx / n;
+    const int64_t d = r - c;
+    if (d > w || -d > w) A[r + c * lda] = 0.0;
+    else if (d < 0) A[r + c * lda] = A[c + r * lda];
+  }
+}
+
+// Exact off-band zeroing (ref svd.py:237-239 / oracles.py band pattern).
+__global__ void mask_band_kernel(double* A, int64_t lda, int64_t m, int64_t n, int64_t lo,
+                                 int64_t up) {
+  const int64_t total = m * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx % m, c = idx / m;
+    if (r - c > lo || c - r > up) A[r + c * lda] = 0.0;
+  }
+}
+
+__global__ void identity_kernel(double* Q, int64_t ldq, int64_t n) {
+  const int64_t total = n * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx % n, c = idx / n;
+    Q[r + c * ldq] = (r == c) ? 1.0 : 0.0;
+  }
+}
+
+static int grid_for(int64_t total) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 148 * 16));
+}
+
+int finalize_sym(cudaStream_t st, double* A, int64_t lda, int64_t n, int64_t w) {
+  if (n <= 0) return 0;
+  count_launch();
+  finalize_sym_kernel<<<grid_for(n * n), 256, 0, st>>>(A, lda, n, w);
+  BR_CUDA(cudaGetLastError());
+  return 0;
+}
+int mask_tri(cudaStream_t st, double* A, int64_t lda, int64_t m, int64_t n, int64_t lo,
+             int64_t up) {
+  if (m <= 0 || n <= 0) return 0;
+  count_launch();
+  mask_band_kernel<<<grid_for(m * n), 256, 0, st>>>(A, lda, m, n, lo, up);
+  BR_CUDA(cudaGetLastError());
+  return 0;
+}
+int set_identity(cudaStream_t st, double* Q, int64_t ldq, int64_t n) {
+  if (n <= 0) return 0;
+  count_launch();
+  identity_kernel<<<grid_for(n * n), 256, 0, st>>>(Q, ldq, n);
+  BR_CUDA(cudaGetLastError());
+  return 0;
+}
+int zero_fill(cudaStream_t st, MatView V) {
+  if (V.rows <= 0 || V.cols <= 0) return 0;
+  const int64_t r = V.trans ? V.cols : V.rows, c = V.trans ? V.rows : V.cols;
+  BR_CUDA(cudaMemset2DAsync(V.p, V.ld * sizeof(double), 0, r * sizeof(double), c, st));
+  return 0;
+}
+
+}  // namespace br
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+using namespace br;
+
+struct br_handle_s {
+  Workspace ws;
+};
+
+#define ARG(cond, i)                                   \
+  do {                                                 \
+    if (!(cond)) {                                     \
+      set_error("invalid argument %d (%s)", i, #cond); \
+      return -(i);                                     \
+    }                                                  \
+  } while (0)
+
+#define DEV(h)                                  \
+  do {                                          \
+    BR_CUDA(cudaSetDevice((h)->ws.device));     \
+  } while (0)
+
+static int ensure_scratch(Workspace& ws, int64_t main_doubles, int64_t panel_doubles,
+                          int64_t pscr) {
+  BR_CHECK(devbuf_reserve(ws.skbuf_main, main_doubles));
+  BR_CHECK(devbuf_reserve(ws.skbuf_panel, panel_doubles));
+  BR_CHECK(devbuf_reserve(ws.pscratch, pscr));
+  ws.sk_main.p = ws.skbuf_main.p;
+  ws.sk_main.cap = ws.skbuf_main.cap;
+  ws.sk_panel.p = ws.skbuf_panel.p;
+  ws.sk_panel.cap = ws.skbuf_panel.cap;
+  ws.sk_main.num_sms = ws.sk_panel.num_sms = ws.num_sms;
+  return 0;
+}
+
+extern "C" {
+
+int br_version(void) { return 100; }
+const char* br_last_error(void) { return g_err; }
+
+int br_create(int device, br_handle_t* out) {
+  ARG(out != nullptr, 2);
+  int ndev = 0;
+  BR_CUDA(cudaGetDeviceCount(&ndev));
+  ARG(device >= 0 && device < ndev, 1);
+  BR_CUDA(cudaSetDevice(device));
+  auto* h = new (std::nothrow) br_handle_s();
+  if (!h) {
+    set_error("out of host memory");
+    return 1;
+  }
+  h->ws.device = device;
+  BR_CUDA(cudaDeviceGetAttribute(&h->ws.num_sms, cudaDevAttrMultiProcessorCount, device));
+  int lo = 0, hi = 0;
+  BR_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  BR_CUDA(cudaStreamCreateWithPriority(&h->ws.own_main, cudaStreamNonBlocking, lo));
+  BR_CUDA(cudaStreamCreateWithPriority(&h->ws.own_panel, cudaStreamNonBlocking, hi));
+  h->ws.main = h->ws.own_main;
+  h->ws.panel = h->ws.own_panel;
+  *out = h;
+  return 0;
+}
+
+int br_destroy(br_handle_t h) {
+  if (!h) return 0;
+  cudaSetDevice(h->ws.device);
+  cudaDeviceSynchronize();
+  Workspace& ws = h->ws;
+  devbuf_free(ws.skbuf_main);
+  devbuf_free(ws.skbuf_panel);
+  devbuf_free(ws.pscratch);
+  devbuf_free(ws.factors);
+  devbuf_free(ws.tmp);
+  devbuf_free(ws.stageA);
+  devbuf_free(ws.stageQ);
+  for (auto e : ws.events) cudaEventDestroy(e);
+  for (auto e : ws.tevents) cudaEventDestroy(e);
+  if (ws.own_main) cudaStreamDestroy(ws.own_main);
+  if (ws.own_panel) cudaStreamDestroy(ws.own_panel);
+  delete h;
+  return 0;
+}
+
+int br_set_streams(br_handle_t h, void* main_stream, void* panel_stream) {
+  ARG(h != nullptr, 1);
+  h->ws.main = main_stream ? (cudaStream_t)main_stream : h->ws.own_main;
+  h->ws.panel = panel_stream ? (cudaStream_t)panel_stream : h->ws.own_panel;
+  return 0;
+}
+
+int br_sync(br_handle_t h) {
+  ARG(h != nullptr, 1);
+  DEV(h);
+  BR_CUDA(cudaStreamSynchronize(h->ws.main));
+  BR_CUDA(cudaStreamSynchronize(h->ws.panel));
+  return 0;
+}
+
+int br_set_timing(br_handle_t h, int enable) {
+  ARG(h != nullptr, 1);
+  h->ws.timing = enable != 0;
+  for (int c = 0; c < TC_COUNT; ++c) {
+    h->ws.t_ms[c] = 0;
+    h->ws.t_flops[c] = 0;
+    h->ws.t_launches[c] = 0;
+  }
+  h->ws.timed.clear();
+  h->ws.tevent_next = 0;
+  return 0;
+}
+
+int br_get_timing(br_handle_t h, int cls, double* ms, double* flops, int64_t* launches) {
+  ARG(h != nullptr, 1);
+  ARG(cls >= 0 && cls < TC_COUNT, 2);
+  if (ms) *ms = h->ws.t_ms[cls];
+  if (flops) *flops = h->ws.t_flops[cls];
+  if (launches) *launches = h->ws.t_launches[cls];
+  return 0;
+}
+
+int br_house_gen(br_handle_t h, int64_t L, const double* x, double* v, double* tau_beta) {
+  ARG(h != nullptr, 1);
+  ARG(L >= 1, 2);
+  ARG(x && v && tau_beta, 3);
+  DEV(h);
+  return house_gen_dev(h->ws.main, L, x, v, tau_beta);
+}
+
+static int qr_common(br_handle_t h, MatView P, double* Y, int64_t ldy, double* T, int64_t ldt,
+                     double* W, int64_t ldw, double* tau) {
+  Workspace& ws = h->ws;
+  const int64_t j = P.rows, b = P.cols;
+  BR_CHECK(ensure_scratch(ws, 4 * std::max<int64_t>(j, 1) * b + (1 << 20), (1 << 20) + 4 * j * b,
+                          panel_scratch_doubles(b)));
+  MatView Yv(Y, ldy, j, b), Tv(T, ldt, b, b), Wv(W, ldw, j, b);
+  return panel_qr(ws.main, ws.sk_main, ws.pscratch, P, Yv, tau, Tv, W ? &Wv : nullptr);
+}
+
+int br_qr_panel(br_handle_t h, int64_t j, int64_t b, double* P, int64_t ldp, double* Y,
+                int64_t ldy, double* T, int64_t ldt, double* W, int64_t ldw, double* tau) {
+  ARG(h != nullptr, 1);
+  ARG(b >= 1 && j >= b, 2);
+  ARG(P != nullptr && ldp >= j, 4);
+  ARG(Y != nullptr && ldy >= j, 6);
+  ARG(T != nullptr && ldt >= b, 8);
+  ARG(W == nullptr || ldw >= j, 11);
+  ARG(tau != nullptr, 12);
+  DEV(h);
+  return qr_common(h, MatView(P, ldp, j, b), Y, ldy, T, ldt, W, ldw, tau);
+}
+
+int br_lq_panel(br_handle_t h, int64_t b, int64_t j, double* P, int64_t ldp, double* Y,
+                int64_t ldy, double* T, int64_t ldt, double* W, int64_t ldw, double* tau) {
+  ARG(h != nullptr, 1);
+  ARG(b >= 1 && j >= b, 3);
+  ARG(P != nullptr && ldp >= b, 4);
+  ARG(Y != nullptr && ldy >= j, 6);
+  ARG(T != nullptr && ldt >= b, 8);
+  ARG(W == nullptr || ldw >= j, 11);
+  ARG(tau != nullptr, 12);
+  DEV(h);
+  // LQ of the b x j rows == QR of the transposed (j x b) view
+  return qr_common(h, MatView(P, ldp, j, b, true), Y, ldy, T, ldt, W, ldw, tau);
+}
+
+int br_build_w(br_handle_t h, int64_t j, int64_t b, const double* Y, int64_t ldy,
+               const double* T, int64_t ldt, double* W, int64_t ldw) {
+  ARG(h != nullptr, 1);
+  ARG(j >= 0 && b >= 0, 2);
+  ARG(Y && ldy >= std::max<int64_t>(j, 1), 4);
+  ARG(T && ldt >= std::max<int64_t>(b, 1), 6);
+  ARG(W && ldw >= std::max<int64_t>(j, 1), 8);
+  DEV(h);
+  Workspace& ws = h->ws;
+  BR_CHECK(ensure_scratch(ws, 4 * std::max<int64_t>(j, 1) * std::max<int64_t>(b, 1) + (1 << 20),
+                          1 << 20, panel_scratch_doubles(1)));
+  return gemm(ws.main, ws.sk_main, MatView(W, ldw, j, b), MatView((double*)Y, ldy, j, b),
+              MatView((double*)T, ldt, b, b), 1.0, 0.0);
+}
+
+int br_apply_wy_left(br_handle_t h, int64_t rows, int64_t cols, double* A, int64_t lda,
+                     const double* Y, int64_t ldy, const double* W, int64_t ldw, int64_t b) {
+  ARG(h != nullptr, 1);
+  ARG(rows >= 0, 2);
+  ARG(cols >= 0, 3);
+  ARG(A && lda >= std::max<int64_t>(rows, 1), 4);
+  ARG(Y && ldy >= std::max<int64_t>(rows, 1), 6);
+  ARG(W && ldw >= std::max<int64_t>(rows, 1), 8);
+  ARG(b >= 0, 10);
+  DEV(h);
+  if (rows == 0 || cols == 0 || b == 0) return 0;
+  Workspace& ws = h->ws;
+  BR_CHECK(ensure_scratch(ws, 4 * std::max(rows, cols) * b + (1 << 20), 1 << 20,
+                          panel_scratch_doubles(1)));
+  BR_CHECK(devbuf_reserve(ws.tmp, b * cols));
+  MatView Z(ws.tmp.p, b, b, cols), Av(A, lda, rows, cols);
+  BR_CHECK(gemm(ws.main, ws.sk_main, Z, MatView((double*)W, ldw, rows, b).T(), Av, 1.0, 0.0));
+  return gemm(ws.main, ws.sk_main, Av, MatView((double*)Y, ldy, rows, b), Z, 1.0, 1.0);
+}
+
+int br_apply_wy_right(br_handle_t h, int64_t rows, int64_t cols, double* A, int64_t lda,
+                      const double* Y, int64_t ldy, const double* W, int64_t ldw, int64_t b) {
+  ARG(h != nullptr, 1);
+  ARG(rows >= 0, 2);
+  ARG(cols >= 0, 3);
+  ARG(A && lda >= std::max<int64_t>(rows, 1), 4);
+  ARG(Y && ldy >= std::max<int64_t>(cols, 1), 6);
+  ARG(W && ldw >= std::max<int64_t>(cols, 1), 8);
+  ARG(b >= 0, 10);
+  DEV(h);
+  if (rows == 0 || cols == 0 || b == 0) return 0;
+  Workspace& ws = h->ws;
+  BR_CHECK(ensure_scratch(ws, 4 * std::max(rows, cols) * b + (1 << 20), 1 << 20,
+                          panel_scratch_doubles(1)));
+  BR_CHECK(devbuf_reserve(ws.tmp, rows * b));
+  MatView Z(ws.tmp.p, rows, rows, b), Av(A, lda, rows, cols);
+  BR_CHECK(gemm(ws.main, ws.sk_main, Z, Av, MatView((double*)W, ldw, cols, b), 1.0, 0.0));
+  return gemm(ws.main, ws.sk_main, Av, Z, MatView((double*)Y, ldy, cols, b).T(), 1.0, 1.0);
+}
+
+int br_symm_lower(br_handle_t h, int64_t j, int64_t b, const double* A2, int64_t lda,
+                  const double* W, int64_t ldw, double* X1, int64_t ldx) {
+  ARG(h != nullptr, 1);
+  ARG(j >= 0, 2);
+  ARG(b >= 0, 3);
+  ARG(A2 && lda >= std::max<int64_t>(j, 1), 4);
+  ARG(W && ldw >= std::max<int64_t>(j, 1), 6);
+  ARG(X1 && ldx >= std::max<int64_t>(j, 1), 8);
+  DEV(h);
+  if (j == 0 || b == 0) return 0;
+  Workspace& ws = h->ws;
+  BR_CHECK(ensure_scratch(ws, 4 * j * b + (1 << 20), 1 << 20, panel_scratch_doubles(1)));
+  return symm_lower(ws.main, ws.sk_main, MatView(X1, ldx, j, b), MatView((double*)A2, lda, j, j),
+                    MatView((double*)W, ldw, j, b));
+}
+
+int br_syr2k_lower(br_handle_t h, int64_t j, int64_t b, double* A2, int64_t lda,
+                   const double* X3, int64_t ldx, const double* Y, int64_t ldy, int64_t c0,
+                   int64_t c1) {
+  ARG(h != nullptr, 1);
+  ARG(j >= 0, 2);
+  ARG(b >= 0, 3);
+  ARG(A2 && lda >= std::max<int64_t>(j, 1), 4);
+  ARG(X3 && ldx >= std::max<int64_t>(j, 1), 6);
+  ARG(Y && ldy >= std::max<int64_t>(j, 1), 8);
+  ARG(0 <= c0 && c0 <= c1 && c1 <= j, 10);
+  DEV(h);
+  if (j == 0 || b == 0 || c0 == c1) return 0;
+  return syr2k_lower(h->ws.main, MatView(A2, lda, j, j), MatView((double*)X3, ldx, j, b),
+                     MatView((double*)Y, ldy, j, b), c0, c1);
+}
+
+int br_sym_two_sided_update(br_handle_t h, int64_t j, int64_t b, double* A2, int64_t lda,
+                            const double* Y, int64_t ldy, const double* W, int64_t ldw) {
+  ARG(h != nullptr, 1);
+  ARG(j >= 0, 2);
+  ARG(b >= 0, 3);
+  ARG(A2 && lda >= std::max<int64_t>(j, 1), 4);
+  ARG(Y && ldy >= std::max<int64_t>(j, 1), 6);
+  ARG(W && ldw >= std::max<int64_t>(j, 1), 8);
+  DEV(h);
+  if (j == 0 || b == 0) return 0;
+  Workspace& ws = h->ws;
+  BR_CHECK(ensure_scratch(ws, 4 * j * b + (1 << 20), 1 << 20, panel_scratch_doubles(1)));
+  BR_CHECK(devbuf_reserve(ws.tmp, 2 * j * b + b * b));
+  MatView X1(ws.tmp.p, j, j, b), X3(ws.tmp.p + j * b, j, j, b), X2(ws.tmp.p + 2 * j * b, b, b, b);
+  MatView A2v(A2, lda, j, j), Yv((double*)Y, ldy, j, b), Wv((double*)W, ldw, j, b);
+  BR_CHECK(symm_lower(ws.main, ws.sk_main, X1, A2v, Wv));
+  BR_CHECK(gemm(ws.main, ws.sk_main, X2, X1.T(), Wv, 0.5, 0.0));
+  BR_CHECK(gemm(ws.main, ws.sk_main, X3, Yv, X2, 1.0, 1.0, &X1));
+  return syr2k_lower(ws.main, A2v, X3, Yv, 0, j);
+}
+
+static double sevp_nominal(int64_t n) { return 4.0 * (double)n * n * n / 3.0; }
+static double svd_nominal(int64_t m, int64_t n) {
+  return 4.0 * ((double)m * n * n - (double)n * n * n / 3.0);
+}
+
+int br_reduce_sym_band(br_handle_t h, int64_t n, int64_t w, int64_t b, int lookahead, double* A,
+                       int64_t lda, double* Q, int64_t ldq, br_stats* stats) {
+  ARG(h != nullptr, 1);
+  ARG(n >= 1, 2);
+  ARG(w >= 1, 3);
+  ARG(b >= 1 && b <= w, 4);
+  ARG(lookahead == 0 || lookahead == 1, 5);
+  ARG(A != nullptr && lda >= n, 6);
+  ARG(Q == nullptr || ldq >= n, 9);
+  DEV(h);
+  Workspace& ws = h->ws;
+  cudaEvent_t e0, e1;
+  BR_CUDA(cudaEventCreate(&e0));
+  BR_CUDA(cudaEventCreate(&e1));
+  const int64_t l0 = launch_count();
+  BR_CUDA(cudaEventRecord(e0, ws.main));
+  int64_t iters = 0;
+  int rc = sevp_reduce(ws, n, w, b, lookahead, A, lda, Q, ldq, &iters);
+  if (rc) {
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return rc;
+  }
+  BR_CUDA(cudaEventRecord(e1, ws.main));
+  BR_CUDA(cudaEventSynchronize(e1));
+  BR_CUDA(cudaStreamSynchronize(ws.panel));
+  BR_CUDA(cudaGetLastError());
+  float ms = 0;
+  BR_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (ws.timing) BR_CHECK(ws_collect_timing(ws));
+  if (stats) {
+    stats->iterations = iters;
+    stats->device_ms = ms;
+    stats->nominal_flops = sevp_nominal(n);
+    stats->launches = launch_count() - l0;
+  }
+  return 0;
+}
+
+int br_reduce_tri_band(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b, int lookahead,
+                       double* A, int64_t lda, br_stats* stats) {
+  ARG(h != nullptr, 1);
+  ARG(m >= 1 && m >= n, 2);
+  ARG(n >= 1, 3);
+  ARG(w >= 1, 4);
+  ARG(b >= 1 && b <= w, 5);
+  ARG(lookahead == 0 || lookahead == 1, 6);
+  ARG(A != nullptr && lda >= m, 7);
+  DEV(h);
+  Workspace& ws = h->ws;
+  cudaEvent_t e0, e1;
+  BR_CUDA(cudaEventCreate(&e0));
+  BR_CUDA(cudaEventCreate(&e1));
+  const int64_t l0 = launch_count();
+  BR_CUDA(cudaEventRecord(e0, ws.main));
+  int64_t iters = 0;
+  int rc = tri_reduce(ws, m, n, w, b, lookahead, A, lda, &iters);
+  if (rc) {
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return rc;
+  }
+  BR_CUDA(cudaEventRecord(e1, ws.main));
+  BR_CUDA(cudaEventSynchronize(e1));
+  BR_CUDA(cudaStreamSynchronize(ws.panel));
+  BR_CUDA(cudaGetLastError());
+  float ms = 0;
+  BR_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (ws.timing) BR_CHECK(ws_collect_timing(ws));
+  if (stats) {
+    stats->iterations = iters;
+    stats->device_ms = ms;
+    stats->nominal_flops = svd_nominal(m, n);
+    stats->launches = launch_count() - l0;
+  }
+  return 0;
+}
+
+static int host_stage_in(Workspace& ws, int64_t m, int64_t n, const double* A, int64_t lda,
+                         DevBuf& dev, int64_t& ldd) {
+  ldd = (m + 31) / 32 * 32;
+  BR_CHECK(devbuf_reserve(dev, ldd * n));
+  BR_CUDA(cudaMemcpy2DAsync(dev.p, ldd * sizeof(double), A, lda * sizeof(double),
+                            m * sizeof(double), n, cudaMemcpyHostToDevice, ws.main));
+  return 0;
+}
+
+int br_reduce_sym_band_host(br_handle_t h, int64_t n, int64_t w, int64_t b, int lookahead,
+                            const double* A, int64_t lda, double* band, int64_t ldb, double* Q,
+                            int64_t ldq, br_stats* stats) {
+  ARG(h != nullptr, 1);
+  ARG(n >= 1, 2);
+  ARG(A != nullptr && lda >= n, 6);
+  ARG(band != nullptr && ldb >= n, 8);
+  ARG(Q == nullptr || ldq >= n, 11);
+  DEV(h);
+  Workspace& ws = h->ws;
+  DevBuf& dA = ws.stageA;
+  DevBuf& dQ = ws.stageQ;
+  int64_t ldd = 0;
+  BR_CHECK(host_stage_in(ws, n, n, A, lda, dA, ldd));
+  double* qd = nullptr;
+  if (Q) {
+    BR_CHECK(devbuf_reserve(dQ, ldd * n));
+    qd = dQ.p;
+  }
+  BR_CHECK(br_reduce_sym_band(h, n, w, b, lookahead, dA.p, ldd, qd, ldd, stats));
+  BR_CUDA(cudaMemcpy2DAsync(band, ldb * sizeof(double), dA.p, ldd * sizeof(double),
+                            n * sizeof(double), n, cudaMemcpyDeviceToHost, ws.main));
+  if (Q)
+    BR_CUDA(cudaMemcpy2DAsync(Q, ldq * sizeof(double), dQ.p, ldd * sizeof(double),
+                              n * sizeof(double), n, cudaMemcpyDeviceToHost, ws.main));
+  BR_CUDA(cudaStreamSynchronize(ws.main));
+  return 0;
+}
+
+int br_reduce_tri_band_host(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b,
+                            int lookahead, const double* A, int64_t lda, double* band,
+                            int64_t ldb, br_stats* stats) {
+  ARG(h != nullptr, 1);
+  ARG(m >= 1 && m >= n, 2);
+  ARG(n >= 1, 3);
+  ARG(A != nullptr && lda >= m, 7);
+  ARG(band != nullptr && ldb >= m, 9);
+  DEV(h);
+  Workspace& ws = h->ws;
+  DevBuf& dA = ws.stageA;
+  int64_t ldd = 0;
+  BR_CHECK(host_stage_in(ws, m, n, A, lda, dA, ldd));
+  BR_CHECK(br_reduce_tri_band(h, m, n, w, b, lookahead, dA.p, ldd, stats));
+  BR_CUDA(cudaMemcpy2DAsync(band, ldb * sizeof(double), dA.p, ldd * sizeof(double),
+                            m * sizeof(double), n, cudaMemcpyDeviceToHost, ws.main));
+  BR_CUDA(cudaStreamSynchronize(ws.main));
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,99 @@
+// Host-side handle, workspace and driver entry points (internal header).
+#pragma once
+#include <vector>
+
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace br {
+
+// Growable device buffer (cudaMalloc'd; grows only between synchronized calls).
+struct DevBuf {
+  double* p = nullptr;
+  int64_t cap = 0;  // doubles
+};
+int devbuf_reserve(DevBuf& b, int64_t n);
+void devbuf_free(DevBuf& b);
+
+enum TimeClass { TC_PANEL = 0, TC_SYMM = 1, TC_SYR2K = 2, TC_GEMM = 3, TC_COUNT = 4 };
+
+// Per-device execution context: the two streams of the look-ahead (main =
+// trailing update, panel = next panel's factorization; the T_P / T_S groups
+// of the reference runtime, ref runtime.py:142-180), events, and reusable
+// device workspace.
+struct Workspace {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t main = nullptr, panel = nullptr;
+  cudaStream_t own_main = nullptr, own_panel = nullptr;
+  Scratch sk_main, sk_panel;  // split-K partials, one per stream
+  DevBuf skbuf_main, skbuf_panel;
+  DevBuf pscratch;  // panel_qr internal scratch (panel stream)
+  DevBuf factors;   // reduction buffers
+  DevBuf tmp;       // kernel-level API temporaries
+  DevBuf stageA, stageQ;  // host-buffer entry points
+  // events
+  std::vector<cudaEvent_t> events;
+  size_t event_next = 0;
+  // optional per-class timing
+  bool timing = false;
+  struct Timed {
+    int cls;
+    cudaEvent_t a, b;
+    double flops;
+  };
+  std::vector<Timed> timed;
+  std::vector<cudaEvent_t> tevents;
+  size_t tevent_next = 0;
+  double t_ms[TC_COUNT] = {0, 0, 0, 0};
+  double t_flops[TC_COUNT] = {0, 0, 0, 0};
+  int64_t t_launches[TC_COUNT] = {0, 0, 0, 0};
+  int64_t launches = 0;
+};
+
+// Kernels launched by this library in this process (stats / bench evidence).
+int64_t launch_count();
+void count_launch(int64_t n = 1);
+
+cudaEvent_t ws_event(Workspace& ws);  // recycled sync-only event
+void ws_events_reset(Workspace& ws);
+// Timing scope: records CUDA events around the enclosed launches on `st`
+// (only when ws.timing), attributing `flops` algorithmic flops to `cls`.
+struct TimeScope {
+  Workspace& ws;
+  cudaStream_t st;
+  int cls;
+  double flops;
+  cudaEvent_t a = nullptr;
+  TimeScope(Workspace& w, cudaStream_t s, int c, double f);
+  ~TimeScope();
+};
+int ws_collect_timing(Workspace& ws);  // after a sync: fold events into t_ms
+
+// Panel factorization (panel.cu). P is the j x b panel view (a transposed
+// view gives the LQ of the underlying b x j rows). Outputs: Y (j x b, unit
+// lower trapezoidal with explicit zeros/ones), tau (b), T (b x b, T =
+// -T_larft), W = Y*T (j x b, optional). R (or L) is written into P's top
+// b x b triangle; the strictly-lower part of P is left unspecified (the
+// reductions zero it in their final band mask).
+int panel_qr(cudaStream_t st, Scratch& sk, DevBuf& pscratch, MatView P, MatView Y, double* tau,
+             MatView T, MatView* W);
+int64_t panel_scratch_doubles(int64_t b);
+int t_from_gram(cudaStream_t st, const double* G, int64_t ldg, const double* tau, int64_t b,
+                double* T, int64_t ldt);
+int house_gen_dev(cudaStream_t st, int64_t L, const double* x, double* v, double* tau_beta);
+
+// Elementwise helpers (driver.cu)
+int finalize_sym(cudaStream_t st, double* A, int64_t lda, int64_t n, int64_t w);
+int mask_tri(cudaStream_t st, double* A, int64_t lda, int64_t m, int64_t n, int64_t lower_bw,
+             int64_t upper_bw);
+int zero_fill(cudaStream_t st, MatView V);
+int set_identity(cudaStream_t st, double* Q, int64_t ldq, int64_t n);
+
+// Reductions (reduce.cu)
+int sevp_reduce(Workspace& ws, int64_t n, int64_t w, int64_t b, int lookahead, double* A,
+                int64_t lda, double* Q, int64_t ldq, int64_t* iterations);
+int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lookahead,
+               double* A, int64_t lda, int64_t* iterations);
+
+}  // namespace br

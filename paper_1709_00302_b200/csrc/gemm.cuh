@@ -1,0 +1,66 @@
+// FP64 tensor-core (DMMA, mma.sync m8n8k4) GEMM engine for sm_100a.
+//
+// One templated CTA-tile kernel serves every dense contraction of the
+// band reduction:
+//   * general C = alpha*op(A)*op(B) + beta*Cin  (apply_wy_left/right pairs,
+//     X2, X3, W = Y*T, Gram Y^T*Y, block-reflector steps inside panels);
+//   * SYMM   X1 = sym(A2)*W reading only A2's lower triangle
+//     (ref kernels.py:312-341);
+//   * SYR2K  A2[:, c0:c1] += X3*Y^T + Y*X3^T on lower tiles only
+//     (ref kernels.py:344-378).
+// Operands are staged global->shared with cp.async (16 B when aligned, else
+// 8 B, zero-filled at the edges) in a STAGES-deep pipeline; fragments are read
+// with conflict-free padded layouts and fed to DMMA.8x8x4. There are no
+// floating-point atomics: split-K partials go to a workspace and are summed
+// in a fixed order, so every result is run-to-run deterministic and
+// independent of how the output is split into launches (the look-ahead
+// relies on that to stay bitwise equal to the non-look-ahead schedule).
+#pragma once
+#include "common.cuh"
+
+namespace br {
+
+// Device scratch owned by one stream (split-K partials).
+struct Scratch {
+  double* p = nullptr;
+  int64_t cap = 0;  // doubles
+  int num_sms = 148;
+};
+
+enum AMode { A_N = 0, A_T = 1, A_SYM = 2 };
+enum BMode { B_N = 0, B_T = 1 };
+enum EpiMode { EPI_GEN = 0, EPI_SPLIT = 1, EPI_LOWER = 2 };
+
+struct GemmArgs {
+  int64_t M, N, K;
+  const double* A;
+  int64_t lda;
+  const double* A2;  // optional second K-source for A_N (k >= ksplitA)
+  int64_t lda2, ksplitA;
+  const double* B;
+  int64_t ldb;
+  const double* B2;  // optional second K-source for B_T (k >= ksplitB)
+  int64_t ldb2, ksplitB;
+  double* C;
+  int64_t ldc;
+  const double* Cin;  // beta term source (may alias C); unused when beta == 0
+  int64_t ldcin;
+  double alpha, beta;
+  int64_t k_per_split;  // EPI_SPLIT: K range per blockIdx.z
+  double* ws;           // EPI_SPLIT: partials [z][N][M]
+  int64_t c0, c1;       // EPI_LOWER: rows [c0, M) x cols [c0, c1)
+  int vecA, vecB;       // 16-byte cp.async allowed for A / B
+};
+
+// Host-side launch helpers (gemm.cu). All return 0 or a positive CUDA error.
+// C = alpha*op(A)*op(B) + beta*Cin (Cin defaults to C). Views carry the
+// transposition; a transposed C is handled by transposing the product.
+int gemm(cudaStream_t st, Scratch& ws, MatView C, MatView A, MatView B, double alpha,
+         double beta, const MatView* Cin = nullptr, int max_ctas = 0);
+// X1 = sym(A2) * W, A2 lower-stored j x j (non-transposed view).
+int symm_lower(cudaStream_t st, Scratch& ws, MatView X1, MatView A2, MatView W);
+// A2[:, c0:c1] += X3*Y^T + Y*X3^T, lower triangle only.
+int syr2k_lower(cudaStream_t st, MatView A2, MatView X3, MatView Y, int64_t c0, int64_t c1,
+                int max_ctas = 0);
+
+}  // namespace br

@@ -1,0 +1,348 @@
+// The two first-stage reductions with static look-ahead, as stream programs.
+//
+// SEVP  (ref sevp.py:110-324): dense symmetric -> symmetric band.
+// Triband SVD (ref svd.py:179-247): dense general (m >= n) -> upper
+//   triangular-band.
+//
+// Look-ahead (ref sevp.py:209-273, PAPER.md T1/T2): the reference's two
+// worker groups T_S / T_P become two CUDA streams of one context: `panel`
+// (high priority, the T_S role) factors the next panel while `main` (the
+// T_P role) finishes the rest of the current trailing update. The updates
+// that touch the next panel's columns are issued first on `main`, then an
+// event hands the panel to the panel stream. Every update kernel is
+// split-invariant (fixed K order, no atomics), so look-ahead depth 1 is
+// bitwise identical to depth 0 on the same GPU.
+#include <algorithm>
+#include <vector>
+
+#include "driver.cuh"
+#include "gemm.cuh"
+
+namespace br {
+
+static double gemm_flops(double m, double n, double k) { return 2.0 * m * n * k; }
+// Lower-triangle SYR2K columns [c0, c1) of a j x j matrix, rank 2*bp.
+static double syr2k_flops(int64_t j, int64_t bp, int64_t c0, int64_t c1) {
+  double s = 0.0;  // sum_{c=c0}^{c1-1} (j - c)
+  s = (double)(c1 - c0) * (double)j - 0.5 * ((double)c1 * (c1 - 1) - (double)c0 * (c0 - 1));
+  return 4.0 * (double)bp * s;
+}
+static double panel_flops(int64_t j, int64_t b) {
+  return 2.0 * j * b * b - 2.0 * b * b * b / 3.0 + (double)j * b * b;  // QR + T/W
+}
+
+// ---------------------------------------------------------------------------
+// SEVP
+// ---------------------------------------------------------------------------
+int sevp_reduce(Workspace& ws, int64_t n, int64_t w, int64_t b, int lookahead, double* A,
+                int64_t lda, double* Q, int64_t ldq, int64_t* iterations) {
+  std::vector<int64_t> ks;
+  for (int64_t k = 0; n - k - w >= 2; k += std::min(b, n - k - w)) ks.push_back(k);
+  *iterations = (int64_t)ks.size();
+  if (ks.empty()) return 0;  // n <= w + 1: input returned unchanged (sevp.py:302-305)
+
+  const int64_t jmax = n - w;
+  // factor buffers: Y[2], W[2] (jmax x b), T[2] (b x b), tau[2] (b), X1, X3
+  // (jmax x b), X2 (b x b), Zm (b x w) mid-block temp, ZQ (n x b)
+  const int64_t nY = jmax * b, nT = b * b;
+  const int64_t total = 4 * nY + 2 * nT + 2 * b + 2 * nY + nT + b * w + n * b;
+  BR_CHECK(devbuf_reserve(ws.factors, total));
+  BR_CHECK(devbuf_reserve(ws.skbuf_main, 4 * n * b + (1 << 20)));
+  BR_CHECK(devbuf_reserve(ws.skbuf_panel, 4 * jmax * b + (1 << 20)));
+  BR_CHECK(devbuf_reserve(ws.pscratch, panel_scratch_doubles(b)));
+  ws.sk_main = Scratch{ws.skbuf_main.p, ws.skbuf_main.cap, ws.num_sms};
+  ws.sk_panel = Scratch{ws.skbuf_panel.p, ws.skbuf_panel.cap, ws.num_sms};
+  double* f = ws.factors.p;
+  double *Yb[2], *Wb[2], *Tb[2], *taub[2];
+  for (int p = 0; p < 2; ++p) {
+    Yb[p] = f; f += nY;
+    Wb[p] = f; f += nY;
+  }
+  for (int p = 0; p < 2; ++p) {
+    Tb[p] = f; f += nT;
+  }
+  for (int p = 0; p < 2; ++p) {
+    taub[p] = f; f += b;
+  }
+  double* X1b = f; f += nY;
+  double* X3b = f; f += nY;
+  double* X2b = f; f += nT;
+  double* Zm = f; f += b * w;
+  double* ZQ = f; f += n * b;
+
+  if (Q) BR_CHECK(set_identity(ws.main, Q, ldq, n));
+  auto Aat = [&](int64_t r, int64_t c) { return A + r + c * lda; };
+
+  auto do_panel = [&](cudaStream_t st, Scratch& sk, int64_t k, int par) -> int {
+    const int64_t bp = std::min(b, n - k - w), j = n - k - w;
+    MatView P(Aat(k + w, k), lda, j, bp);
+    MatView Y(Yb[par], jmax, j, bp), T(Tb[par], b, bp, bp), W(Wb[par], jmax, j, bp);
+    TimeScope ts(ws, st, TC_PANEL, panel_flops(j, bp));
+    return panel_qr(st, sk, ws.pscratch, P, Y, taub[par], T, &W);
+  };
+
+  cudaEvent_t ev_panel = nullptr;
+  BR_CHECK(do_panel(ws.main, ws.sk_main, ks[0], 0));
+  for (size_t idx = 0; idx < ks.size(); ++idx) {
+    const int64_t k = ks[idx];
+    const int64_t bp = std::min(b, n - k - w), j = n - k - w;
+    const int par = (int)(idx & 1);
+    if (ev_panel) {
+      BR_CUDA(cudaStreamWaitEvent(ws.main, ev_panel, 0));
+      ev_panel = nullptr;
+    }
+    MatView Y(Yb[par], jmax, j, bp), W(Wb[par], jmax, j, bp);
+    MatView A2(Aat(k + w, k + w), lda, j, j);
+    const bool has_next = idx + 1 < ks.size();
+    const int64_t kn = has_next ? ks[idx + 1] : 0;
+    const int64_t bpn = has_next ? std::min(b, n - kn - w) : 0;
+    const int64_t split = has_next ? std::max<int64_t>(0, bp + bpn - w) : 0;
+    const bool la = lookahead && has_next;
+
+    // mid block A[k+w:n, k+bp:k+w] := Q^T mid (ref sevp.py:147-153)
+    auto mid = [&](int64_t c0, int64_t c1) -> int {
+      if (c0 >= c1) return 0;
+      MatView M(Aat(k + w, c0), lda, j, c1 - c0);
+      MatView Z(Zm, b, bp, c1 - c0);
+      TimeScope ts(ws, ws.main, TC_GEMM, 2 * gemm_flops(bp, c1 - c0, j));
+      BR_CHECK(gemm(ws.main, ws.sk_main, Z, W.T(), M, 1.0, 0.0));
+      return gemm(ws.main, ws.sk_main, M, Y, Z, 1.0, 1.0);
+    };
+    // X1 = sym(A2) W; X2 = 1/2 X1^T W; X3 = X1 + Y X2 (ref sevp.py:156-176)
+    auto xprods = [&]() -> int {
+      MatView X1(X1b, jmax, j, bp), X3(X3b, jmax, j, bp), X2(X2b, b, bp, bp);
+      {
+        TimeScope ts(ws, ws.main, TC_SYMM, gemm_flops(j, bp, j));
+        BR_CHECK(symm_lower(ws.main, ws.sk_main, X1, A2, W));
+      }
+      TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(bp, bp, j) + gemm_flops(j, bp, bp));
+      BR_CHECK(gemm(ws.main, ws.sk_main, X2, X1.T(), W, 0.5, 0.0));
+      return gemm(ws.main, ws.sk_main, X3, Y, X2, 1.0, 1.0, &X1);
+    };
+    auto trail = [&](int64_t c0, int64_t c1) -> int {
+      if (c0 >= c1) return 0;
+      MatView X3(X3b, jmax, j, bp);
+      TimeScope ts(ws, ws.main, TC_SYR2K, syr2k_flops(j, bp, c0, c1));
+      return syr2k_lower(ws.main, A2, X3, Y, c0, c1);
+    };
+    // Q[:, k+w:n] := Q[:, k+w:n] (I + W Y^T) (ref sevp.py:138-144)
+    auto accq = [&]() -> int {
+      if (!Q) return 0;
+      MatView Qs(Q + (k + w) * ldq, ldq, n, j);
+      MatView Z(ZQ, n, n, bp);
+      TimeScope ts(ws, ws.main, TC_GEMM, 2 * gemm_flops(n, bp, j));
+      BR_CHECK(gemm(ws.main, ws.sk_main, Z, Qs, W, 1.0, 0.0));
+      return gemm(ws.main, ws.sk_main, Qs, Z, Y.T(), 1.0, 1.0);
+    };
+    auto launch_next_panel = [&]() -> int {
+      cudaEvent_t ev = ws_event(ws);
+      BR_CUDA(cudaEventRecord(ev, ws.main));
+      BR_CUDA(cudaStreamWaitEvent(ws.panel, ev, 0));
+      BR_CHECK(do_panel(ws.panel, ws.sk_panel, kn, par ^ 1));
+      ev_panel = ws_event(ws);
+      BR_CUDA(cudaEventRecord(ev_panel, ws.panel));
+      return 0;
+    };
+
+    if (la && split == 0) {
+      // V1 regime (2b <= w): next panel lies inside the mid block
+      const int64_t h1 = std::min(k + bp + bpn, k + w);
+      BR_CHECK(mid(k + bp, h1));
+      BR_CHECK(launch_next_panel());
+      BR_CHECK(mid(h1, k + w));
+      BR_CHECK(xprods());
+      BR_CHECK(trail(0, j));
+      BR_CHECK(accq());
+    } else if (la) {
+      // V2 regime (2b > w): next panel spills `split` columns into A2
+      BR_CHECK(mid(k + bp, k + w));
+      BR_CHECK(xprods());
+      BR_CHECK(trail(0, split));
+      BR_CHECK(launch_next_panel());
+      BR_CHECK(trail(split, j));
+      BR_CHECK(accq());
+    } else {
+      BR_CHECK(mid(k + bp, k + w));
+      BR_CHECK(xprods());
+      BR_CHECK(trail(0, j));
+      BR_CHECK(accq());
+      if (has_next) BR_CHECK(do_panel(ws.main, ws.sk_main, kn, par ^ 1));
+    }
+  }
+  ws_events_reset(ws);
+  return finalize_sym(ws.main, A, lda, n, w);
+}
+
+// ---------------------------------------------------------------------------
+// Triangular-band SVD
+// ---------------------------------------------------------------------------
+int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lookahead,
+               double* A, int64_t lda, int64_t* iterations) {
+  struct It {
+    int64_t k, bp;
+  };
+  std::vector<It> its;
+  for (int64_t k = 0; m - k >= 2 && k < n;) {
+    const int64_t bp = std::min({b, n - k, m - k});
+    its.push_back({k, bp});
+    k += bp;
+  }
+  *iterations = (int64_t)its.size();
+  if (its.empty()) return mask_tri(ws.main, A, lda, m, n, 0, w);
+
+  const int64_t nYu = m * b, nYv = n * b, nT = b * b;
+  const int64_t total = 4 * nYu + 2 * nT + 2 * b + 2 * nYv + nT + b + b * n + m * b;
+  BR_CHECK(devbuf_reserve(ws.factors, total));
+  BR_CHECK(devbuf_reserve(ws.skbuf_main, 4 * std::max(m, n) * b + (1 << 20)));
+  BR_CHECK(devbuf_reserve(ws.skbuf_panel, 4 * std::max(m, n) * b + (1 << 20)));
+  BR_CHECK(devbuf_reserve(ws.pscratch, panel_scratch_doubles(b)));
+  ws.sk_main = Scratch{ws.skbuf_main.p, ws.skbuf_main.cap, ws.num_sms};
+  ws.sk_panel = Scratch{ws.skbuf_panel.p, ws.skbuf_panel.cap, ws.num_sms};
+  double* f = ws.factors.p;
+  double *Yu[2], *Wu[2], *Tu[2], *tauu[2];
+  for (int p = 0; p < 2; ++p) {
+    Yu[p] = f; f += nYu;
+    Wu[p] = f; f += nYu;
+  }
+  for (int p = 0; p < 2; ++p) {
+    Tu[p] = f; f += nT;
+  }
+  for (int p = 0; p < 2; ++p) {
+    tauu[p] = f; f += b;
+  }
+  double* Yv = f; f += nYv;
+  double* Wv = f; f += nYv;
+  double* Tv = f; f += nT;
+  double* tauv = f; f += b;
+  double* ZL = f; f += b * n;
+  double* ZR = f; f += m * b;
+
+  auto Aat = [&](int64_t r, int64_t c) { return A + r + c * lda; };
+  auto qr = [&](cudaStream_t st, Scratch& sk, int64_t k, int64_t bp, int par) -> int {
+    const int64_t i = m - k;
+    MatView P(Aat(k, k), lda, i, bp);
+    MatView Y(Yu[par], m, i, bp), T(Tu[par], b, bp, bp), W(Wu[par], m, i, bp);
+    TimeScope ts(ws, st, TC_PANEL, panel_flops(i, bp));
+    return panel_qr(st, sk, ws.pscratch, P, Y, tauu[par], T, &W);
+  };
+  auto lq = [&](cudaStream_t st, Scratch& sk, int64_t k, int64_t bq) -> int {
+    const int64_t jr = n - k - w;
+    MatView P(Aat(k, k + w), lda, jr, bq, true);  // transposed view of the bq x jr rows
+    MatView Y(Yv, n, jr, bq), T(Tv, b, bq, bq), W(Wv, n, jr, bq);
+    TimeScope ts(ws, st, TC_PANEL, panel_flops(jr, bq));
+    return panel_qr(st, sk, ws.pscratch, P, Y, tauv, T, &W);
+  };
+  auto handoff = [&]() -> int {  // main -> panel ordering point
+    cudaEvent_t ev = ws_event(ws);
+    BR_CUDA(cudaEventRecord(ev, ws.main));
+    BR_CUDA(cudaStreamWaitEvent(ws.panel, ev, 0));
+    return 0;
+  };
+  auto mark_panel = [&]() -> cudaEvent_t {  // completion point of the last panel launch
+    cudaEvent_t ev = ws_event(ws);
+    cudaEventRecord(ev, ws.panel);
+    return ev;
+  };
+  auto join = [&](cudaEvent_t ev) -> int {  // panel -> main
+    BR_CUDA(cudaStreamWaitEvent(ws.main, ev, 0));
+    return 0;
+  };
+
+  BR_CHECK(qr(ws.main, ws.sk_main, its[0].k, its[0].bp, 0));
+  cudaEvent_t ev_qr = nullptr;
+  for (size_t idx = 0; idx < its.size(); ++idx) {
+    const int64_t k = its[idx].k, bp = its[idx].bp, i = m - k;
+    const int par = (int)(idx & 1);
+    if (ev_qr) {
+      BR_CHECK(join(ev_qr));
+      ev_qr = nullptr;
+    }
+    const bool has_next = idx + 1 < its.size();
+    const int64_t kn = has_next ? its[idx + 1].k : 0, bpn = has_next ? its[idx + 1].bp : 0;
+    const bool la = lookahead && has_next;
+    MatView Yuv(Yu[par], m, i, bp), Wuv(Wu[par], m, i, bp);
+    const int64_t ncE = n - k - bp;
+    const int64_t jr = n - k - w;
+    const int64_t bq = jr >= 1 ? std::min(bp, jr) : 0;
+    bool next_issued = false;
+
+    auto next_qr_on_panel = [&]() -> int {
+      BR_CHECK(handoff());
+      BR_CHECK(qr(ws.panel, ws.sk_panel, kn, bpn, par ^ 1));
+      ev_qr = mark_panel();
+      next_issued = true;
+      return 0;
+    };
+
+    if (ncE > 0) {
+      // left update E := Q_U^T E = E + Y_U (W_U^T E)  (ref svd.py:191)
+      MatView E(Aat(k, k + bp), lda, i, ncE);
+      MatView Z(ZL, b, bp, ncE);
+      {
+        TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(bp, ncE, i));
+        BR_CHECK(gemm(ws.main, ws.sk_main, Z, Wuv.T(), E, 1.0, 0.0));
+      }
+      if (bq > 0) {
+        {  // rows of the LQ panel first
+          TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(bq, ncE, bp));
+          BR_CHECK(gemm(ws.main, ws.sk_main, E.sub(0, 0, bq, ncE), Yuv.sub(0, 0, bq, bp), Z, 1.0,
+                        1.0));
+        }
+        cudaEvent_t ev_lq = nullptr;
+        if (lookahead) {
+          BR_CHECK(handoff());
+          BR_CHECK(lq(ws.panel, ws.sk_panel, k, bq));
+          ev_lq = mark_panel();
+        }
+        {
+          TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, ncE, bp));
+          BR_CHECK(gemm(ws.main, ws.sk_main, E.sub(bq, 0, i - bq, ncE), Yuv.sub(bq, 0, i - bq, bp),
+                        Z, 1.0, 1.0));
+        }
+        const int64_t splitc = has_next ? std::max<int64_t>(0, bp + bpn - w) : 0;
+        if (la && splitc == 0) BR_CHECK(next_qr_on_panel());  // next panel is left-only
+        if (lookahead) BR_CHECK(join(ev_lq));
+        else BR_CHECK(lq(ws.main, ws.sk_main, k, bq));
+        // right update D := D Q_V = D + (D W_V) Y_V^T (ref svd.py:199)
+        MatView D(Aat(k + bq, k + w), lda, i - bq, jr);
+        MatView Yvv(Yv, n, jr, bq), Wvv(Wv, n, jr, bq);
+        MatView Zr(ZR, m, i - bq, bq);
+        if (i - bq > 0) {
+          {
+            TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, bq, jr));
+            BR_CHECK(gemm(ws.main, ws.sk_main, Zr, D, Wvv, 1.0, 0.0));
+          }
+          if (la && !next_issued && splitc > 0) {
+            const int64_t sc = std::min(splitc, jr);
+            {
+              TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, sc, bq));
+              BR_CHECK(gemm(ws.main, ws.sk_main, D.sub(0, 0, i - bq, sc), Zr,
+                            Yvv.sub(0, 0, sc, bq).T(), 1.0, 1.0));
+            }
+            BR_CHECK(next_qr_on_panel());
+            if (sc < jr) {
+              TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, jr - sc, bq));
+              BR_CHECK(gemm(ws.main, ws.sk_main, D.sub(0, sc, i - bq, jr - sc), Zr,
+                            Yvv.sub(sc, 0, jr - sc, bq).T(), 1.0, 1.0));
+            }
+          } else {
+            TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, jr, bq));
+            BR_CHECK(gemm(ws.main, ws.sk_main, D, Zr, Yvv.T(), 1.0, 1.0));
+          }
+        }
+      } else {
+        TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i, ncE, bp));
+        BR_CHECK(gemm(ws.main, ws.sk_main, E, Yuv, Z, 1.0, 1.0));
+      }
+    }
+    if (has_next && !next_issued) {
+      if (la) BR_CHECK(next_qr_on_panel());
+      else BR_CHECK(qr(ws.main, ws.sk_main, kn, bpn, par ^ 1));
+    }
+  }
+  if (ev_qr) BR_CHECK(join(ev_qr));
+  ws_events_reset(ws);
+  return mask_tri(ws.main, A, lda, m, n, 0, w);
+}
+
+}  // namespace br

@@ -1,0 +1,123 @@
+"""Dense symmetric -> symmetric band on the B200 (drop-in for ref sevp.py).
+
+`reduce_sym_band(A, cfg, groups=None)` keeps the reference's signature,
+validation, result type and edge semantics (ref sevp.py:287-324):
+  * only A's lower triangle is read; A itself is never mutated;
+  * the band is returned in full storage, mirrored, off-band exactly 0;
+  * n <= w + 1 returns the copied input unchanged (not symmetrized),
+    q=None, flops {"total": 0}, iterations 0.
+Schedules: REFERENCE -> look-ahead depth 0; V1 / V2 -> depth 1 (the next
+panel is factored on the panel stream while the trailing update finishes).
+Both are bitwise identical on the GPU. Extensions (keyword-only):
+`lookahead` overrides the depth, `device` selects the GPU.
+"""
+from __future__ import annotations
+
+import warnings
+from dataclasses import dataclass
+from enum import Enum
+
+import numpy as np
+
+from . import _dev, _lib
+from .flops import FLOPS, sevp_counted_flops, sevp_nominal_flops  # noqa: F401
+
+
+class SevpVariant(Enum):
+    REFERENCE = "reference"
+    V1 = "v1"
+    V2 = "v2"
+
+
+class V2Mapping(Enum):
+    ON_TS = "on_ts"
+    ON_ALL = "on_all"
+
+
+@dataclass
+class SevpConfig:
+    n: int
+    w: int
+    b: int
+    variant: SevpVariant = SevpVariant.REFERENCE
+    v2_mapping: V2Mapping = V2Mapping.ON_TS
+    accumulate_q: bool = False
+    inner_b: int = 16
+
+    def validate(self):
+        """Same rules and messages as ref sevp.py:66-81."""
+        if self.n < 1:
+            raise ValueError("n >= 1")
+        if self.w < 1:
+            raise ValueError("w >= 1")
+        if not (1 <= self.b <= self.w):
+            raise ValueError("need 1 <= b <= w")
+        if self.variant == SevpVariant.V1 and 2 * self.b > self.w:
+            raise ValueError(f"V1 requires 2b <= w, got b={self.b}, w={self.w}")
+        if self.variant == SevpVariant.V2 and 2 * self.b <= self.w:
+            warnings.warn(
+                f"V2 with 2b <= w (b={self.b}, w={self.w}) is valid but outside "
+                "its intended regime; V1 covers this case",
+                RuntimeWarning,
+                stacklevel=3,
+            )
+
+
+@dataclass
+class SevpResult:
+    band: np.ndarray
+    q: np.ndarray | None
+    flops: dict
+    iterations: int
+
+
+def _schedule(n, w, b):
+    """Leading columns of all iterations (ref sevp.py:110-118)."""
+    ks = []
+    k = 0
+    while n - k - w >= 2:
+        ks.append(k)
+        k += min(b, n - k - w)
+    return ks
+
+
+def _depth(cfg, groups, lookahead):
+    if lookahead is not None:
+        if lookahead not in (0, 1):
+            raise ValueError("lookahead must be 0 or 1 (depth > 1 is a reference non-goal)")
+        return int(lookahead)
+    if groups is not None and getattr(groups, "ts_count", 1) == 0:
+        return 0
+    return 0 if cfg.variant == SevpVariant.REFERENCE else 1
+
+
+def reduce_sym_band(A, cfg, groups=None, *, lookahead=None, device=None, stats=None):
+    """Reduce symmetric A to a symmetric band matrix of bandwidth cfg.w."""
+    cfg.validate()
+    A = np.array(A, dtype=np.float64, order="F")
+    if A.ndim != 2 or A.shape[0] != A.shape[1]:
+        raise ValueError("reduce_sym_band needs a square matrix")
+    if A.shape[0] != cfg.n:
+        raise ValueError(f"cfg.n={cfg.n} does not match matrix order {A.shape[0]}")
+    depth = _depth(cfg, groups, lookahead)
+    lib = _lib.load()
+    h, _ = _dev.ctx(device)
+    ks = _schedule(cfg.n, cfg.w, cfg.b)
+    if not ks:
+        return SevpResult(band=A, q=None, flops={"total": 0}, iterations=0)
+    n = cfg.n
+    band = np.empty((n, n), order="F")
+    Q = np.empty((n, n), order="F") if cfg.accumulate_q else None
+    st = _lib.BrStats()
+    rc = lib.br_reduce_sym_band_host(
+        h, n, cfg.w, cfg.b, depth, A.ctypes.data, n, band.ctypes.data, n,
+        Q.ctypes.data if Q is not None else None, n, st)
+    _lib.check(rc, "reduce_sym_band")
+    variant = {SevpVariant.REFERENCE: "reference", SevpVariant.V1: "v1", SevpVariant.V2: "v2"}[cfg.variant]
+    flops, iters = sevp_counted_flops(n, cfg.w, cfg.b, variant, cfg.accumulate_q, cfg.inner_b)
+    for key, val in flops.items():
+        if key != "total":
+            FLOPS.add(key, val)
+    if stats is not None:
+        stats.update(device_ms=st.device_ms, launches=st.launches, iterations=st.iterations)
+    return SevpResult(band=band, q=Q, flops=flops, iterations=int(st.iterations))

@@ -1,0 +1,144 @@
+"""Dense general -> upper triangular-band on the B200 (drop-in for ref svd.py).
+
+`reduce_tri_band(A, w, b, groups=None, range_log=None, inner_b=16)` keeps
+the reference signature and semantics (ref svd.py:205-247): m < n reduces
+A^T and transposes back (lower_bw = w, upper_bw = 0); off-band entries are
+exactly 0. The reference schedule is strictly sequential; the GPU adds
+look-ahead (keyword `lookahead`, default 1): the LQ panel and the next QR
+panel are factored on the panel stream while the rank-b halves of the
+left/right updates run. The split updates are bitwise identical to the
+sequential order on the same GPU.
+
+`reduce_band_svd(A, cfg)` dispatches cfg.form == TRIANGULAR_BAND to
+reduce_tri_band exactly like ref svd.py:552-553; the equal-bandwidth BAND
+form (ref svd.py:250-589) is ranked "next" in SURVEY.md 8(f) and not built
+yet, so it raises NotImplementedError rather than computing on the CPU.
+"""
+from __future__ import annotations
+
+import warnings
+from dataclasses import dataclass
+from enum import Enum
+
+import numpy as np
+
+from . import _dev, _lib
+from .flops import FLOPS, svd_nominal_flops, tri_counted_flops  # noqa: F401
+from .sevp import V2Mapping
+
+
+class SvdForm(Enum):
+    TRIANGULAR_BAND = "triband"
+    BAND = "band"
+
+
+class SvdVariant(Enum):
+    REFERENCE = "reference"
+    SIMULTANEOUS = "simultaneous"
+    V1 = "v1"
+    V2 = "v2"
+
+
+@dataclass
+class SvdConfig:
+    m: int
+    n: int
+    w: int
+    b: int
+    form: SvdForm = SvdForm.BAND
+    variant: SvdVariant = SvdVariant.REFERENCE
+    v2_mapping: V2Mapping = V2Mapping.ON_TS
+    inner_b: int = 16
+
+    def validate(self):
+        """Same rules and messages as ref svd.py:81-101."""
+        if self.m < 1 or self.n < 1:
+            raise ValueError("m, n >= 1")
+        if self.w < 1:
+            raise ValueError("w >= 1")
+        if not (1 <= self.b <= self.w):
+            raise ValueError("need 1 <= b <= w")
+        if self.form == SvdForm.TRIANGULAR_BAND:
+            if self.variant != SvdVariant.REFERENCE:
+                raise ValueError("triangular-band form supports only the reference schedule")
+        elif self.variant == SvdVariant.V1 and 2 * self.b > self.w:
+            raise ValueError(f"V1 requires 2b <= w, got b={self.b}, w={self.w}")
+        elif self.variant == SvdVariant.V2 and 2 * self.b <= self.w:
+            warnings.warn(
+                f"V2 with 2b <= w (b={self.b}, w={self.w}) is valid but outside "
+                "its intended regime; V1 covers this case",
+                RuntimeWarning,
+                stacklevel=3,
+            )
+
+
+@dataclass
+class SvdResult:
+    band: np.ndarray
+    flops: dict
+    form: SvdForm
+    lower_bw: int
+    upper_bw: int
+    iterations: int
+
+
+def _depth(groups, lookahead):
+    if lookahead is not None:
+        if lookahead not in (0, 1):
+            raise ValueError("lookahead must be 0 or 1")
+        return int(lookahead)
+    if groups is not None and getattr(groups, "ts_count", 1) == 0:
+        return 0
+    return 1
+
+
+def reduce_tri_band(A, w, b, groups=None, range_log=None, inner_b=16, *, lookahead=None,
+                    device=None, stats=None):
+    """Reduce A to upper triangular-band form (band[i,j] = 0 for i > j or j > i + w)."""
+    if w < 1:
+        raise ValueError("w >= 1")
+    if not (1 <= b <= w):
+        raise ValueError("need 1 <= b <= w")
+    A = np.array(A, dtype=np.float64, order="F")
+    if A.ndim != 2:
+        raise ValueError("reduce_tri_band needs a 2-D matrix")
+    if range_log is not None:
+        raise ValueError("range_log instrumentation is a CPU-reference analysis feature; "
+                         "not supported on the GPU path")
+    depth = _depth(groups, lookahead)
+    lib = _lib.load()
+    h, _ = _dev.ctx(device)
+    m, n = A.shape
+    if m < n:
+        inner = reduce_tri_band(np.asfortranarray(A.T), w, b, groups, None, inner_b,
+                                lookahead=lookahead, device=device, stats=stats)
+        return SvdResult(band=np.asfortranarray(inner.band.T), flops=inner.flops,
+                         form=SvdForm.TRIANGULAR_BAND, lower_bw=w, upper_bw=0,
+                         iterations=inner.iterations)
+    band = np.empty((m, n), order="F")
+    st = _lib.BrStats()
+    rc = lib.br_reduce_tri_band_host(h, m, n, w, b, depth, A.ctypes.data, m, band.ctypes.data, m, st)
+    _lib.check(rc, "reduce_tri_band")
+    flops, _ = tri_counted_flops(m, n, w, b, inner_b)
+    for key, val in flops.items():
+        if key != "total":
+            FLOPS.add(key, val)
+    if stats is not None:
+        stats.update(device_ms=st.device_ms, launches=st.launches, iterations=st.iterations)
+    return SvdResult(band=band, flops=flops, form=SvdForm.TRIANGULAR_BAND, lower_bw=0, upper_bw=w,
+                     iterations=int(st.iterations))
+
+
+def reduce_band_svd(A, cfg, groups=None, range_log=None, *, lookahead=None, device=None):
+    """Dispatch on cfg.form (ref svd.py:515-589)."""
+    cfg.validate()
+    A = np.array(A, dtype=np.float64, order="F")
+    if A.ndim != 2:
+        raise ValueError("reduce_band_svd needs a 2-D matrix")
+    if A.shape != (cfg.m, cfg.n):
+        raise ValueError(f"cfg says {cfg.m} x {cfg.n} but the matrix is {A.shape[0]} x {A.shape[1]}")
+    if cfg.form == SvdForm.TRIANGULAR_BAND:
+        return reduce_tri_band(A, cfg.w, cfg.b, groups, range_log, cfg.inner_b,
+                               lookahead=lookahead, device=device)
+    raise NotImplementedError(
+        "equal-bandwidth BAND form is not built on the B200 path yet (SURVEY.md 8(f) next #1)")
