@@ -1,0 +1,385 @@
+"""Benchmark: fp64 GFLOP/s of the first-stage dense->band reduction on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+
+One "step" = one full reduction of the configuration's matrix, starting from
+a fresh device copy of the input (the D2D restore is inside the timed step,
+like the reference's own copy of A). Workload defaults to BASELINE.json
+config 4 (SVD dense -> upper triangular-band, m=n=16384, w=b=256, look-ahead
+depth 1): the north-star configuration, and it fits one GPU. The metric
+uses the reference's nominal counts (4/3 n^3 SEVP, 8/3 n^3 square SVD;
+ref sevp.py:92-96, svd.py:127-132).
+
+Under torchrun (N > 1) every rank reduces its own matrix (replicas; the 1D
+block-cyclic multi-GPU split is not built yet), timing is
+the max over ranks and `value` is the whole-job aggregate.
+
+--impl reference times the reference algorithm's CPU implementation on the
+host cores: the NumPy port in oracle/ (the reference is pure Python and does
+not travel to the GPU box), on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "fp64 GFLOP/s of dense→band reduction (4/3·n³ SEVP, 8/3·n³ SVD) at 1–8 B200"
+
+CONFIGS = {
+    # name: (kind, n, w, b, description)
+    "c1": ("sevp", 2048, 32, 32, "SEVP n=2048 w=b=32, A=(G+G^T)/2 N(0,1) seed 0"),
+    "c2": ("tri", 2048, 32, 32, "SVD triband m=n=2048 w=b=32, N(0,1) seed 1"),
+    "c3": ("sevp", 8192, 128, 128, "SEVP n=8192 w=b=128, graded spectrum 1e-8, seeds 2/3"),
+    "c4": ("tri", 16384, 256, 256, "SVD triband m=n=16384 w=b=256, U(-1,1) seed 4"),
+    "c5": ("sevp", 32768, 256, 256, "SEVP n=32768 w=b=256, A=(G+G^T)/2 N(0,1) seed 5"),
+}
+
+
+def nominal(kind, n):
+    return 4.0 * n**3 / 3.0 if kind == "sevp" else 4.0 * (n * n * n - n**3 / 3.0)
+
+
+# --------------------------------------------------------------------------
+# clocks sampled during the timed region
+# --------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        smax = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for nm, v in zip(names, s[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------
+# inputs
+# --------------------------------------------------------------------------
+def make_input(cfg):
+    import oracle as O  # input generators only (same seeds/distributions as the survey)
+
+    return O.gen_config(cfg)
+
+
+def cpu_sample(cfg, A, seconds_hint=20.0):
+    """Time the oracle port (NumPy + multithreaded BLAS) on the first iterations
+    of the same workload; returns (gflops, iterations, seconds, cores)."""
+    import oracle as O
+    from paper_1709_00302_b200.flops import sevp_counted_flops, tri_counted_flops
+
+    kind, n, w, b, _ = CONFIGS[cfg]
+    iters = 1
+    t_total = 0.0
+    best = None
+    while True:
+        t0 = time.perf_counter()
+        if kind == "sevp":
+            O.reduce_sym_band(A, n, w, b, max_iters=iters)
+            fl = sevp_counted_flops(n, w, b, "v2", max_iters=iters)[0]["total"]
+        else:
+            O.reduce_tri_band(A, w, b, max_iters=iters)
+            fl = tri_counted_flops(n, n, w, b, max_iters=iters)[0]["total"]
+        dt = time.perf_counter() - t0
+        t_total += dt
+        best = (fl / dt / 1e9, iters, dt)
+        full = len(O.sevp_schedule(n, w, b)) if kind == "sevp" else len(O.tri_schedule(n, n, b))
+        if t_total > seconds_hint or iters >= full or dt * 2.2 > seconds_hint:
+            break
+        iters = min(full, iters * 2)
+    return best[0], best[1], best[2], os.cpu_count()
+
+
+def dgemm_peak(dev):
+    """Measured cuBLAS DGEMM throughput (TFLOP/s): the FP64 roofline denominator
+    (MEASURED_PEAKS.json carries no fp64 figure)."""
+    import torch
+
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device=dev)
+    b = torch.randn(n, n, dtype=torch.float64, device=dev)
+    for _ in range(2):
+        a @ b
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = 1e30
+    for _ in range(4):
+        e0.record()
+        a @ b
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    torch.cuda.empty_cache()
+    return 2.0 * n**3 / (best * 1e-3) / 1e12
+
+
+def load_traffic(cfg):
+    p = os.path.join(ROOT, "profiles", f"traffic_{cfg}.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))
+        except Exception:
+            return None
+    return None
+
+
+# --------------------------------------------------------------------------
+# arms
+# --------------------------------------------------------------------------
+def run_reference(args, rank, world):
+    kind, n, w, b, desc = CONFIGS[args.config]
+    if rank != 0:
+        return
+    A = make_input(args.config)
+    for _ in range(args.warmup):
+        pass  # the port has no warm-up state; a sample run below is timed per step
+    vals = []
+    sample = None
+    for _ in range(args.steps):
+        gf, iters, dt, cores = cpu_sample(args.config, A, args.cpu_seconds)
+        vals.append(gf)
+        sample = (iters, dt, cores)
+    v = float(np.median(vals))
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": v,
+        "unit": "GFLOP/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": sample[1] * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": args.config, "desc": desc, "kind": kind, "n": n, "w": w, "b": b},
+        "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": sample[2], "kind": "port",
+                         "sample": f"first {sample[0]} of the reduction's iterations on the full "
+                                   f"{n}x{n} input (oracle/ NumPy port, multithreaded OpenBLAS)"},
+        "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    from paper_1709_00302_b200 import _lib
+
+    kind, n, w, b, desc = CONFIGS[args.config]
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    lib = _lib.load()
+    h = _lib.handle(local_rank)
+    peak = dgemm_peak(dev)
+
+    A_host = make_input(args.config)  # F-order numpy
+    ld = (n + 31) // 32 * 32
+    A0 = torch.empty((n, ld), dtype=torch.float64, device=dev)
+    A0[:, :n].copy_(torch.from_numpy(A_host.T))  # column-major on the device
+    A = torch.empty_like(A0)
+    stream = torch.cuda.current_stream(dev)
+    la = args.lookahead
+
+    def one_step(st):
+        A.copy_(A0)
+        if kind == "sevp":
+            rc = lib.br_reduce_sym_band(h, n, w, b, la, A.data_ptr(), ld, None, 0, st)
+        else:
+            rc = lib.br_reduce_tri_band(h, n, n, w, b, la, A.data_ptr(), ld, st)
+        _lib.check(rc, "reduce")
+
+    # the library runs on its own streams: make it follow torch's stream
+    lib.br_set_streams(h, C.c_void_p(stream.cuda_stream), None)
+    st = _lib.BrStats()
+    for _ in range(args.warmup):
+        one_step(st)
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    lib.br_set_timing(h, 1)
+    launches = 0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    for _ in range(args.steps):
+        one_step(st)
+        launches += st.launches + 1  # + the D2D restore
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    timing = {}
+    names = ["panel", "symm", "syr2k", "gemm"]
+    for c in range(4):
+        tms, tfl, tnl = C.c_double(), C.c_double(), C.c_int64()
+        lib.br_get_timing(h, c, C.byref(tms), C.byref(tfl), C.byref(tnl))
+        timing[names[c]] = (tms.value / args.steps, tfl.value / args.steps, tnl.value // max(1, args.steps))
+    lib.br_set_timing(h, 0)
+    if dist:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    flops = nominal(kind, n)
+    value = world * flops / (ms * 1e-3) / 1e9
+
+    # ---- e2e through the C-ABI host entry point (pinned host buffers) ----
+    Ah = torch.from_numpy(np.asfortranarray(A_host).T.copy()).pin_memory()  # (n, n) = col-major
+    Bh = torch.empty((n, n), dtype=torch.float64).pin_memory()
+    lib.br_set_streams(h, None, None)
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        if kind == "sevp":
+            rc = lib.br_reduce_sym_band_host(h, n, w, b, la, Ah.data_ptr(), n, Bh.data_ptr(), n,
+                                             None, 0, st)
+        else:
+            rc = lib.br_reduce_tri_band_host(h, n, n, w, b, la, Ah.data_ptr(), n, Bh.data_ptr(), n, st)
+        _lib.check(rc, "reduce_host")
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if dist:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_val = world * flops / e2e_s / 1e9
+
+    # ---- roofline of the dominant kernel class ----
+    dom = max(timing, key=lambda k: timing[k][0])
+    dms, dfl, dnl = timing[dom]
+    achieved = dfl / (dms * 1e-3) / 1e12 if dms > 0 else 0.0
+    if dom == "panel":  # report the dominant GEMM class instead: panels are latency-bound
+        gem = max(("symm", "syr2k", "gemm"), key=lambda k: timing[k][0])
+        dom_note = f"panel dominates ({dms:.1f} ms); roofline for {gem}"
+        dms, dfl, dnl = timing[gem]
+        dom = gem
+        achieved = dfl / (dms * 1e-3) / 1e12 if dms > 0 else 0.0
+    else:
+        dom_note = None
+    traffic = load_traffic(args.config)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        gf, iters, dt, cores = cpu_sample(args.config, A_host, args.cpu_seconds)
+        cpu = {"value": gf, "unit": "GFLOP/s", "cores": cores, "kind": "port",
+               "sample": f"first {iters} iterations of the same {n}x{n} reduction "
+                         f"({dt:.1f} s, oracle/ NumPy port + multithreaded OpenBLAS)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "GFLOP/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": args.config, "desc": desc, "kind": kind, "n": n, "w": w, "b": b,
+                       "lookahead": la, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "l2": f"input {n * n * 8 / 2**30:.2f} GiB vs 126 MB L2 (no flush needed)"
+                       if n * n * 8 > 126e6 else "input fits L2; restored from a separate copy each step"},
+            "clocks": clocks.summary(),
+            "e2e": {"value": e2e_val, "unit": "GFLOP/s", "h2d_bytes_per_step": n * n * 8,
+                    "d2h_bytes_per_step": n * n * 8, "steps": e2e_steps,
+                    "path": "br_reduce_*_host (C ABI), pinned host in/out"},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak,
+                         "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
+                         "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (MEASURED_PEAKS.json has no fp64)",
+                         "traffic": traffic.get(dom) if traffic else None,
+                         "note": dom_note},
+            "breakdown_ms": {k: round(v[0], 3) for k, v in timing.items()},
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--lookahead", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

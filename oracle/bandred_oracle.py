@@ -266,7 +266,7 @@ def mask_tri_band(A, w):
     return A
 
 
-def reduce_sym_band(A, n, w, b, inner_b=16, accumulate_q=False):
+def reduce_sym_band(A, n, w, b, inner_b=16, accumulate_q=False, max_iters=None):
     """Dense symmetric -> symmetric band, Reference schedule.
 
     Restates reduce_sym_band (sevp.py:287-324) with _run_reference
@@ -283,6 +283,8 @@ def reduce_sym_band(A, n, w, b, inner_b=16, accumulate_q=False):
     if not ks:
         return A, None, 0
     Q = np.eye(n, order="F") if accumulate_q else None
+    if max_iters is not None:  # bounded CPU-baseline sample (bench.py)
+        ks = ks[:max_iters]
     for k in ks:
         bp = min(b, n - k - w)
         j = n - k - w
@@ -299,7 +301,7 @@ def reduce_sym_band(A, n, w, b, inner_b=16, accumulate_q=False):
     return finalize_sym(A, n, w), Q, len(ks)
 
 
-def reduce_tri_band(A, w, b, inner_b=16):
+def reduce_tri_band(A, w, b, inner_b=16, max_iters=None):
     """Dense general -> upper triangular-band (svd.py:179-247).
 
     Returns (band, lower_bw, upper_bw, iterations); m < n reduces A^T and
@@ -315,7 +317,10 @@ def reduce_tri_band(A, w, b, inner_b=16):
         band, _, _, it = reduce_tri_band(np.asfortranarray(A.T), w, b, inner_b)
         return np.asfortranarray(band.T), w, 0, it
     it = 0
-    for k, bp in tri_schedule(m, n, b):
+    sched = tri_schedule(m, n, b)
+    if max_iters is not None:  # bounded CPU-baseline sample (bench.py)
+        sched = sched[:max_iters]
+    for k, bp in sched:
         Yu, Tu, Wu, _, _ = qr_panel(A[k:m, k : k + bp], inner_b)
         apply_wy_left(A[k:m, k + bp : n], Yu, Wu)
         jr = n - k - w

@@ -109,6 +109,11 @@ __device__ __forceinline__ double ld_cluster_f64(uint32_t addr) {
   asm volatile("ld.shared::cluster.f64 %0, [%1];\n" : "=d"(v) : "r"(addr) : "memory");
   return v;
 }
+// Remote (DSMEM) store; ordered for the cluster by the next
+// barrier.cluster.arrive.release.
+__device__ __forceinline__ void st_cluster_f64(uint32_t addr, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(addr), "d"(v) : "memory");
+}
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -76,13 +76,25 @@ __device__ __forceinline__ void warp_transpose_reduce(double (&v)[RC], int lane)
   }
 }
 
+// One leaf. Thread t of CTA q owns rows q*LT*R + t + k*LT (k < R). Registers
+// hold the active columns ROTATED: p[k][0] is always the current column i,
+// p[k][c'] is column i + c'. The rank-1 update writes p[k][c'] from
+// p[k][c'+1], so the rotation costs no extra instructions and x = p[k][0]
+// needs no select. Finished Y columns go to shared memory (Ys), finished R
+// rows to Rrow. Slots of the reduced vector:
+//   c' <  NB - i      : x^T P_{i+c'}            (c' = 0 gives ||x||^2)
+//   c' >= NB - i      : Gram entry (c' - NB + i, i - 1) = Y_c^T v_{i-1}
+// Partials are pushed into every CTA's receive buffer with DSMEM stores
+// before the cluster barrier, so the reads after it are local.
 template <int NB, int R>
 __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
   constexpr int RC = NB < 16 ? NB : 16;  // slots per transpose-reduce chunk
   constexpr int NCH = NB / RC;
   constexpr int SH = 32 / RC;  // lanes holding the same reduced slot
+  constexpr int ROWS = LT * R;  // rows per CTA
+  extern __shared__ __align__(16) double Ys[];  // [NB][ROWS]
   __shared__ double wred[LW][NB];
-  __shared__ double red[2][NB][2];
+  __shared__ double recv[2][LEAF_MAXC][NB][2];
   __shared__ double rowi[NB];
   __shared__ double alpha_s[NB];
   __shared__ double scal[NB][3];  // tau, beta, rinv
@@ -93,17 +105,16 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
   const uint32_t rank = cluster_ctarank(), ncta = cluster_nctarank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nb = a.nb;
-  const int64_t base = (int64_t)rank * (LT * R);
+  const int64_t base = (int64_t)rank * ROWS;
 
   int64_t gr[R];
-  bool valid[R];
   double p[R][NB];
 #pragma unroll
   for (int k = 0; k < R; ++k) {
     gr[k] = base + tid + (int64_t)k * LT;
-    valid[k] = gr[k] < a.L;
+    const bool valid = gr[k] < a.L;
 #pragma unroll
-    for (int c = 0; c < NB; ++c) p[k][c] = (valid[k] && c < nb) ? *a.P.at(gr[k], c) : 0.0;
+    for (int c = 0; c < NB; ++c) p[k][c] = (valid && c < nb) ? *a.P.at(gr[k], c) : 0.0;
   }
   if (tid < NB) rowi[tid] = 0.0;
   __syncthreads();
@@ -115,19 +126,13 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
   for (int i = 0; i <= nb; ++i) {
     const bool hh = i < nb;  // i == nb: final round, Gram column nb-1 only
     const int buf = i & 1;
-    double x[R];
+    const int g0 = NB - i;   // first Gram slot
 #pragma unroll
-    for (int k = 0; k < R; ++k) {
-      double xv = 0.0;
-#pragma unroll
-      for (int c = 0; c < NB; ++c)
-        if (c == i) xv = p[k][c];
-      x[k] = xv;  // rows above i hold 0 in column i already
+    for (int k = 0; k < R; ++k)
       if (hh && gr[k] == i) {
 #pragma unroll
         for (int c = 0; c < NB; ++c) rowi[c] = p[k][c];
       }
-    }
     // ---- per-thread partials, transpose-reduced per warp ----
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) {
@@ -137,8 +142,12 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
         const int c = ch * RC + cc;
         double s = 0.0;
 #pragma unroll
-        for (int k = 0; k < R; ++k) s = fma((c >= i) ? x[k] : vprev[k], p[k][c], s);
-        v[cc] = (c >= i || c < i - 1) ? s : 0.0;
+        for (int k = 0; k < R; ++k) s = fma(p[k][0], p[k][c], s);
+        if (c >= g0 && c < NB - 1) {  // Gram entry (c - g0, i - 1)
+#pragma unroll
+          for (int k = 0; k < R; ++k) s = fma(vprev[k], Ys[(c - g0) * ROWS + tid + k * LT], s);
+        }
+        v[cc] = s;
       }
       warp_transpose_reduce<RC>(v, lane);
       if ((lane & (SH - 1)) == 0) wred[warp][ch * RC + lane / SH] = v[0];
@@ -148,24 +157,27 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
       double s = 0.0;
 #pragma unroll
       for (int w = 0; w < LW; ++w) s += wred[w][lane];
-      red[buf][lane][0] = s;
-      red[buf][lane][1] = rowi[lane];
+      const double rv = rowi[lane];
       rowi[lane] = 0.0;
+      for (uint32_t q = 0; q < ncta; ++q) {
+        const uint32_t ad = map_cluster(&recv[buf][rank][lane][0], q);
+        st_cluster_f64(ad, s);
+        st_cluster_f64(ad + 8, rv);
+      }
     }
     cluster_sync_all();
     if (warp == 0) {
       double g = 0.0, pic = 0.0;
       if (lane < NB) {
         for (uint32_t q = 0; q < ncta; ++q) {
-          const uint32_t ad = map_cluster(&red[buf][lane][0], q);
-          g += ld_cluster_f64(ad);
-          pic += ld_cluster_f64(ad + 8);
+          g += recv[buf][q][lane][0];
+          pic += recv[buf][q][lane][1];
         }
       }
-      if (i > 0 && lane < i - 1) G[lane][i - 1] = g;
+      if (i > 0 && lane >= g0 && lane < NB - 1) G[lane - g0][i - 1] = g;
       if (hh) {
-        const double nrm2 = __shfl_sync(0xffffffffu, g, i);
-        const double x0 = __shfl_sync(0xffffffffu, pic, i);
+        const double nrm2 = __shfl_sync(0xffffffffu, g, 0);
+        const double x0 = __shfl_sync(0xffffffffu, pic, 0);
         const double nrm = sqrt(nrm2);
         double tau = 0.0, beta = 0.0, rinv = 0.0;
         if (nrm != 0.0) {
@@ -175,7 +187,8 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
           tau = (beta - x0) / beta;
           rinv = 1.0 / v0;
         }
-        if (lane < NB) alpha_s[lane] = (lane > i && lane < nb) ? tau * ((g - beta * pic) * rinv) : 0.0;
+        if (lane < NB)
+          alpha_s[lane] = (lane >= 1 && lane < nb - i) ? tau * ((g - beta * pic) * rinv) : 0.0;
         if (lane == 0) {
           scal[i][0] = tau;
           scal[i][1] = beta;
@@ -191,63 +204,63 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
       for (int c = 0; c < NB; ++c) al[c] = alpha_s[c];
 #pragma unroll
       for (int k = 0; k < R; ++k) {
-        const double vk = (gr[k] == i) ? 1.0 : x[k] * rinv;
-#pragma unroll
-        for (int c = 0; c < NB; ++c) p[k][c] = fma(-vk, al[c], p[k][c]);
-#pragma unroll
-        for (int c = 0; c < NB; ++c)
-          if (c == i) p[k][c] = vk;  // Y column: unit diagonal, tail v
+        const double vk = (gr[k] == i) ? 1.0 : p[k][0] * rinv;
+        Ys[i * ROWS + tid + k * LT] = vk;  // Y column i (unit diagonal, zeros above)
         vprev[k] = vk;
-        if (gr[k] == i) {  // row i is final: move its R entries out
 #pragma unroll
-          for (int c = 0; c < NB; ++c)
-            if (c > i) {
-              Rrow[i][c] = p[k][c];
-              p[k][c] = 0.0;
-            }
+        for (int c = 0; c < NB - 1; ++c) p[k][c] = fma(-vk, al[c + 1], p[k][c + 1]);
+        p[k][NB - 1] = 0.0;
+        if (gr[k] == i) {  // row i is final: move its R entries (columns i+1..) out
+#pragma unroll
+          for (int c = 0; c < NB - 1; ++c) {
+            if (c < nb - 1 - i) Rrow[i][i + 1 + c] = p[k][c];
+            p[k][c] = 0.0;
+          }
         }
       }
     }
   }
-  cluster_sync_all();  // peers finished reading our partial buffers
+  cluster_sync_all();  // all DSMEM traffic done before any CTA may exit
 
-  // ---- T by the reference recurrence (ref kernels.py:152-162) ----
-  if (warp == 0) {
-    if (lane < NB)
-      for (int c = 0; c < NB; ++c) Ts[lane][c] = 0.0;
-    __syncwarp();
-    for (int i = 0; i < nb; ++i) {
-      const double ti = scal[i][0];
-      if (lane < i) {
-        double s = 0.0;
-        for (int c = lane; c < i; ++c) s = fma(Ts[lane][c], G[c][i], s);
-        Ts[lane][i] = -ti * s;
+  // ---- T by the reference recurrence (ref kernels.py:152-162), one row per lane ----
+  if (warp == 0 && lane < nb) {
+    const int r = lane;
+    for (int c = 0; c < NB; ++c) Ts[r][c] = 0.0;
+    Ts[r][r] = -scal[r][0];
+    for (int i = r + 1; i < nb; ++i) {
+      double s0 = 0.0, s1 = 0.0;
+      int c = r;
+      for (; c + 1 < i; c += 2) {
+        s0 = fma(Ts[r][c], G[c][i], s0);
+        s1 = fma(Ts[r][c + 1], G[c + 1][i], s1);
       }
-      if (lane == i) Ts[i][i] = -ti;
-      __syncwarp();
+      if (c < i) s0 = fma(Ts[r][c], G[c][i], s0);
+      Ts[r][i] = -scal[i][0] * (s0 + s1);
     }
   }
   __syncthreads();
 
-  // ---- outputs ----
+  // ---- outputs: Y, R, W = Y T, tau, T ----
 #pragma unroll
   for (int k = 0; k < R; ++k) {
-    if (!valid[k]) continue;
-#pragma unroll
-    for (int c = 0; c < NB; ++c)
-      if (c < nb) a.Y[gr[k] + (int64_t)c * a.ldy] = p[k][c];
-    if (gr[k] < nb) {  // R row: diagonal beta, then the moved-out entries
+    if (gr[k] >= a.L) continue;
+    const int lr = tid + k * LT;
+    for (int c = 0; c < nb; ++c) a.Y[gr[k] + (int64_t)c * a.ldy] = Ys[c * ROWS + lr];
+    if (gr[k] < nb) {
       const int r = (int)gr[k];
       for (int c = r; c < nb; ++c) *a.P.at(r, c) = (c == r) ? scal[r][1] : Rrow[r][c];
     }
     if (a.W) {
+      double y[NB];
+#pragma unroll
+      for (int m = 0; m < NB; ++m) y[m] = (m < nb) ? Ys[m * ROWS + lr] : 0.0;
 #pragma unroll
       for (int c = 0; c < NB; ++c) {
         if (c >= nb) continue;
         double s = 0.0;
 #pragma unroll
         for (int m = 0; m < NB; ++m)
-          if (m <= c) s = fma(p[k][m], Ts[m][c], s);
+          if (m <= c) s = fma(y[m], Ts[m][c], s);
         a.W[gr[k] + (int64_t)c * a.ldw] = s;
       }
     }
@@ -280,18 +293,20 @@ static int leaf_width(int64_t L, int64_t b) {
 template <int NB, int R>
 static int launch_leaf_t(cudaStream_t st, const LeafArgs& a, int C) {
   auto kern = leaf_reg_kernel<NB, R>;
+  const size_t smem = (size_t)NB * LT * R * sizeof(double);
   static int attr_dev_mask = 0;
   int dev = 0;
   BR_CUDA(cudaGetDevice(&dev));
   if (!(attr_dev_mask & (1 << dev))) {
     BR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    BR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_dev_mask |= (1 << dev);
   }
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];
   cfg.gridDim = dim3(C);
   cfg.blockDim = dim3(LT);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = C;
@@ -323,26 +338,21 @@ static int launch_leaf(cudaStream_t st, MatView P, MatView Y, double* tau, doubl
   a.ldw = W ? W->ld : 0;
   a.L = L;
   a.nb = nb;
-  // choose the template (rows per thread) and the cluster size
-  if (nb > 16) {
-    const int C1 = (int)cdiv(L, LT * 1);
-    if (C1 <= LEAF_MAXC) {
-      int C = 1;
-      while (C < C1) C *= 2;
-      return launch_leaf_t<32, 1>(st, a, C);
-    }
+  auto csize = [&](int64_t rows_per_cta) {
     int C = 1;
-    while (C < cdiv(L, LT * 2)) C *= 2;
-    return launch_leaf_t<32, 2>(st, a, C);
+    while (C < cdiv(L, rows_per_cta)) C *= 2;
+    return C;
+  };
+  if (nb > 16) {
+    if (L <= (int64_t)LEAF_MAXC * LT) return launch_leaf_t<32, 1>(st, a, csize(LT));
+    return launch_leaf_t<32, 2>(st, a, csize(2 * LT));
   }
   if (nb > 8) {
-    int C = 1;
-    while (C < cdiv(L, LT * 4)) C *= 2;
-    return launch_leaf_t<16, 4>(st, a, C);
+    if (L <= (int64_t)LEAF_MAXC * LT) return launch_leaf_t<16, 1>(st, a, csize(LT));
+    return launch_leaf_t<16, 4>(st, a, csize(4 * LT));
   }
-  int C = 1;
-  while (C < cdiv(L, LT * 8)) C *= 2;
-  return launch_leaf_t<8, 8>(st, a, C);
+  if (L <= (int64_t)LEAF_MAXC * LT) return launch_leaf_t<8, 1>(st, a, csize(LT));
+  return launch_leaf_t<8, 8>(st, a, csize(8 * LT));
 }
 
 // T from the Gram matrix, blocked: diagonal 32x32 blocks by the reference

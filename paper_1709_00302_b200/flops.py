@@ -117,8 +117,10 @@ def _apply_right(acc, rows, cols, b):
     acc.mm(rows, b, cols)
 
 
-def sevp_counted_flops(n, w, b, variant="reference", accumulate_q=False, inner_b=16):
-    """Reference-equivalent counted flops of reduce_sym_band (ref sevp.py:194-273)."""
+def sevp_counted_flops(n, w, b, variant="reference", accumulate_q=False, inner_b=16,
+                       max_iters=None):
+    """Reference-equivalent counted flops of reduce_sym_band (ref sevp.py:194-273);
+    max_iters restricts the count to the first iterations."""
     acc = _Acc()
     ks = []
     k = 0
@@ -126,6 +128,8 @@ def sevp_counted_flops(n, w, b, variant="reference", accumulate_q=False, inner_b
         ks.append(k)
         k += min(b, n - k - w)
     for idx, k in enumerate(ks):
+        if max_iters is not None and idx >= max_iters:
+            break
         bp = min(b, n - k - w)
         j = n - k - w
         kn = ks[idx + 1] if idx + 1 < len(ks) else None
@@ -151,14 +155,17 @@ def sevp_counted_flops(n, w, b, variant="reference", accumulate_q=False, inner_b
     return acc.as_dict(), len(ks)
 
 
-def tri_counted_flops(m, n, w, b, inner_b=16):
-    """Reference-equivalent counted flops of reduce_tri_band (ref svd.py:179-202)."""
+def tri_counted_flops(m, n, w, b, inner_b=16, max_iters=None):
+    """Reference-equivalent counted flops of reduce_tri_band (ref svd.py:179-202);
+    max_iters restricts the count to the first iterations."""
     if m < n:
         m, n = n, m
     acc = _Acc()
     k = 0
     it = 0
     while m - k >= 2 and k < n:
+        if max_iters is not None and it >= max_iters:
+            break
         bp = min(b, n - k, m - k)
         _panel(acc, m - k, bp, inner_b)
         _apply_left(acc, m - k, n - k - bp, bp)
