@@ -234,7 +234,10 @@ def run_ours(args, rank, world, local_rank):
     A0 = torch.empty((n, ld), dtype=torch.float64, device=dev)
     A0[:, :n].copy_(torch.from_numpy(A_host.T))  # column-major on the device
     A = torch.empty_like(A0)
-    stream = torch.cuda.current_stream(dev)
+    # a real (non-NULL) stream shared by torch (input restore) and the library
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.synchronize(dev)
+    torch.cuda.set_stream(stream)
     la = args.lookahead
 
     def one_step(st):

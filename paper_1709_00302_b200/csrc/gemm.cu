@@ -88,11 +88,31 @@ __global__ void __launch_bounds__(WM* WN * 32) dgemm_kernel(const GemmArgs g) {
   }
   const int64_t nmax = (EPI == EPI_LOWER) ? g.c1 : g.N;
 
+  // Accumulators start from beta*C when alpha == 1 (every rank-b update and
+  // the SYR2K): the C tile is fetched in one batch before the main loop
+  // instead of load->store pairs in the epilogue, which serialize on the
+  // possible C/Cin aliasing and leave the tensor pipe idle.
+  const bool cpre = (EPI == EPI_LOWER) || (EPI == EPI_GEN && g.alpha == 1.0 && g.beta != 0.0);
   double acc[MI][NI][2];
 #pragma unroll
   for (int i = 0; i < MI; ++i)
 #pragma unroll
     for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  if (cpre) {
+#pragma unroll
+    for (int i = 0; i < MI; ++i) {
+      const int64_t r = m0 + wm + i * 8 + gq;
+#pragma unroll
+      for (int j = 0; j < NI; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t c = n0 + wn + j * 8 + 2 * tq + h;
+          const bool ok = r < g.M && c < nmax && (EPI != EPI_LOWER || r >= c);
+          if (ok) acc[i][j][h] = (EPI == EPI_LOWER) ? g.Cin[r + c * g.ldcin]
+                                                    : g.beta * g.Cin[r + c * g.ldcin];
+        }
+    }
+  }
 
   const bool vA = g.vecA != 0, vB = g.vecB != 0;
   auto load_stage = [&](int s, int64_t k0) {
@@ -193,16 +213,18 @@ __global__ void __launch_bounds__(WM* WN * 32) dgemm_kernel(const GemmArgs g) {
         if (r >= g.M || c >= nmax) continue;
         const double v = acc[i][j][h];
         if (EPI == EPI_GEN) {
-          double out = g.alpha * v;
-          if (g.beta != 0.0) out += g.beta * g.Cin[r + c * g.ldcin];
+          double out;
+          if (cpre) {
+            out = v;
+          } else {
+            out = g.alpha * v;
+            if (g.beta != 0.0) out += g.beta * g.Cin[r + c * g.ldcin];
+          }
           g.C[r + c * g.ldc] = out;
         } else if (EPI == EPI_SPLIT) {
           g.ws[((int64_t)blockIdx.z * g.N + c) * g.M + r] = v;
         } else {
-          if (r >= c) {
-            double* p = g.C + r + c * g.ldc;
-            *p = *p + v;
-          }
+          if (r >= c) g.C[r + c * g.ldc] = v;
         }
       }
     }
@@ -268,8 +290,8 @@ static int launch_cfg(cudaStream_t st, const GemmArgs& g, dim3 grid, int cfg) {
 }
 static void cfg_tile(int cfg, int& bm, int& bn, int& ctas_per_sm) {
   if (cfg == CFG_L) { bm = 128; bn = 128; ctas_per_sm = 1; }
-  else if (cfg == CFG_NS) { bm = 128; bn = 32; ctas_per_sm = 3; }
-  else { bm = 32; bn = 128; ctas_per_sm = 3; }
+  else if (cfg == CFG_NS) { bm = 128; bn = 32; ctas_per_sm = 2; }
+  else { bm = 32; bn = 128; ctas_per_sm = 2; }
 }
 
 static inline bool al16(const void* p, int64_t ld) {
@@ -299,11 +321,25 @@ static int run_gemm(cudaStream_t st, Scratch& ws, GemmArgs g, bool btrans, int m
   const int64_t tiles = cdiv(g.M, bm) * cdiv(g.N, bn);
   const int64_t nkt = cdiv(g.K, 16);
   const int sms = ws.num_sms;
-  const int64_t target = (max_ctas > 0) ? max_ctas : (int64_t)2 * sms * cps;
+  // Split-K factor from a small cost model: waves of resident CTAs times the
+  // k-tiles each CTA runs, plus the fixed-order reduction pass. This keeps
+  // the last wave from idling most SMs (wave quantization) on the tall-skinny
+  // reductions (W^T E, D W_V, X1^T W, Y^T Y).
+  const int64_t slots = (max_ctas > 0) ? std::max(1, max_ctas) : (int64_t)sms * cps;
+  const double kt_time = (double)cps * bm * bn * 16 * 2 / 251e9;  // one k-tile, one CTA
   int64_t S = 1;
-  if (tiles < target) S = std::min<int64_t>(cdiv(target, tiles), std::max<int64_t>(1, nkt / 4));
-  // workspace bound
-  while (S > 1 && S * g.M * g.N > ws.cap) --S;
+  double best = 1e30;
+  const int64_t smax = std::min<int64_t>(64, std::max<int64_t>(1, nkt / 2));
+  for (int64_t s = 1; s <= smax; ++s) {
+    if (s > 1 && s * g.M * g.N > ws.cap) break;
+    const double waves = (double)cdiv(tiles * s, slots);
+    double t = waves * (double)cdiv(nkt, s) * kt_time;
+    if (s > 1) t += (double)(s + 1) * g.M * g.N * 8.0 / 5e12 + 3e-6;
+    if (t < best * 0.995) {
+      best = t;
+      S = s;
+    }
+  }
   if (S > 1) {
     const int64_t kps = cdiv(nkt, S) * 16;
     S = cdiv(g.K, kps);
