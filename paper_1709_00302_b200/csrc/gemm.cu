@@ -1,235 +1,14 @@
-// DMMA GEMM / SYMM / SYR2K kernels (see gemm.cuh for the contract).
+// DMMA GEMM host dispatch: tile configuration, split-K, fixed-order reduction
+// (kernel template in gemm_kernel.cuh, contract in gemm.cuh).
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "driver.cuh"
 #include "gemm.cuh"
+#include "gemm_tiles.cuh"
 
 namespace br {
-
-// Load a TX x TY tile of a column-major region into shared memory:
-// element (x, y) lives at src + x + y*ld (or src2 + x + (y-ysplit)*ld2 for
-// y >= ysplit) and goes to dst[y*LD + x]. Out-of-range elements read as 0.
-template <int TX, int TY, int LD, int NT>
-__device__ __forceinline__ void load_tile(double* dst, const double* src, int64_t ld,
-                                          const double* src2, int64_t ld2, int64_t ysplit,
-                                          int64_t x0, int64_t xmax, int64_t y0, int64_t ymax,
-                                          bool vec2, int tid) {
-  if (vec2) {
-    constexpr int CX = TX / 2;
-#pragma unroll 4
-    for (int idx = tid; idx < CX * TY; idx += NT) {
-      const int y = idx / CX, x = (idx % CX) * 2;
-      const int64_t gx = x0 + x, gy = y0 + y;
-      const double* s = src;
-      int bytes = 0;
-      if (gy < ymax && gx < xmax) {
-        s = gy < ysplit ? src + gx + gy * ld : src2 + gx + (gy - ysplit) * ld2;
-        bytes = (gx + 1 < xmax) ? 16 : 8;
-      }
-      cp_async16(dst + y * LD + x, s, bytes);
-    }
-  } else {
-#pragma unroll 4
-    for (int idx = tid; idx < TX * TY; idx += NT) {
-      const int y = idx / TX, x = idx % TX;
-      const int64_t gx = x0 + x, gy = y0 + y;
-      const double* s = src;
-      int bytes = 0;
-      if (gy < ymax && gx < xmax) {
-        s = gy < ysplit ? src + gx + gy * ld : src2 + gx + (gy - ysplit) * ld2;
-        bytes = 8;
-      }
-      cp_async8(dst + y * LD + x, s, bytes);
-    }
-  }
-}
-
-// Which layout a SYMM K-tile uses: 0 = strictly lower (direct, [k][m]),
-// 1 = strictly upper (transposed read of the lower triangle, [m][k]),
-// 2 = straddles the diagonal (element-wise select, [k][m]).
-__device__ __forceinline__ int sym_case(int64_t k0, int64_t m0, int BK, int BM) {
-  if (k0 + BK <= m0) return 0;
-  if (k0 >= m0 + BM) return 1;
-  return 2;
-}
-
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, int AM, int BMD, int EPI>
-__global__ void __launch_bounds__(WM* WN * 32) dgemm_kernel(const GemmArgs g) {
-  constexpr int NT = WM * WN * 32;
-  constexpr int WTM = BM / WM, WTN = BN / WN, MI = WTM / 8, NI = WTN / 8;
-  constexpr int LDA_KM = BM + 4, LDA_MK = BK + 4;
-  constexpr int A_STAGE = (AM == A_N)   ? BK * LDA_KM
-                          : (AM == A_T) ? BM * LDA_MK
-                                        : (BK * LDA_KM > BM * LDA_MK ? BK * LDA_KM : BM * LDA_MK);
-  constexpr int LDB_NK = BK + 4, LDB_KN = BN + 4;
-  constexpr int B_STAGE = (BMD == B_N) ? BN * LDB_NK : BK * LDB_KN;
-  static_assert(MI * 8 == WTM && NI * 8 == WTN, "warp tile must be a multiple of 8");
-
-  extern __shared__ __align__(16) double smem[];
-  double* As = smem;
-  double* Bs = smem + STAGES * A_STAGE;
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int gq = lane >> 2, tq = lane & 3;
-  const int wm = (warp % WM) * WTM, wn = (warp / WM) * WTN;
-
-  int64_t m0, n0, kbeg, kend;
-  if (EPI == EPI_LOWER) {
-    if (blockIdx.x < blockIdx.y) return;
-    m0 = g.c0 + (int64_t)blockIdx.x * BM;
-    n0 = g.c0 + (int64_t)blockIdx.y * BN;
-    kbeg = 0;
-    kend = g.K;
-  } else {
-    m0 = (int64_t)blockIdx.x * BM;
-    n0 = (int64_t)blockIdx.y * BN;
-    kbeg = (int64_t)blockIdx.z * g.k_per_split;
-    kend = min(g.K, kbeg + g.k_per_split);
-  }
-  const int64_t nmax = (EPI == EPI_LOWER) ? g.c1 : g.N;
-
-  // Accumulators start from beta*C when alpha == 1 (every rank-b update and
-  // the SYR2K): the C tile is fetched in one batch before the main loop
-  // instead of load->store pairs in the epilogue, which serialize on the
-  // possible C/Cin aliasing and leave the tensor pipe idle.
-  const bool cpre = (EPI == EPI_LOWER) || (EPI == EPI_GEN && g.alpha == 1.0 && g.beta != 0.0);
-  double acc[MI][NI][2];
-#pragma unroll
-  for (int i = 0; i < MI; ++i)
-#pragma unroll
-    for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  if (cpre) {
-#pragma unroll
-    for (int i = 0; i < MI; ++i) {
-      const int64_t r = m0 + wm + i * 8 + gq;
-#pragma unroll
-      for (int j = 0; j < NI; ++j)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int64_t c = n0 + wn + j * 8 + 2 * tq + h;
-          const bool ok = r < g.M && c < nmax && (EPI != EPI_LOWER || r >= c);
-          if (ok) acc[i][j][h] = (EPI == EPI_LOWER) ? g.Cin[r + c * g.ldcin]
-                                                    : g.beta * g.Cin[r + c * g.ldcin];
-        }
-    }
-  }
-
-  const bool vA = g.vecA != 0, vB = g.vecB != 0;
-  auto load_stage = [&](int s, int64_t k0) {
-    double* as = As + s * A_STAGE;
-    double* bs = Bs + s * B_STAGE;
-    if (AM == A_N) {
-      load_tile<BM, BK, LDA_KM, NT>(as, g.A, g.lda, g.A2, g.lda2, g.ksplitA, m0, g.M, k0, kend, vA,
-                                    tid);
-    } else if (AM == A_T) {
-      load_tile<BK, BM, LDA_MK, NT>(as, g.A, g.lda, g.A, g.lda, INT64_MAX, k0, kend, m0, g.M, vA,
-                                    tid);
-    } else {
-      const int c = sym_case(k0, m0, BK, BM);
-      if (c == 0) {
-        load_tile<BM, BK, LDA_KM, NT>(as, g.A, g.lda, g.A, g.lda, INT64_MAX, m0, g.M, k0, kend, vA,
-                                      tid);
-      } else if (c == 1) {
-        load_tile<BK, BM, LDA_MK, NT>(as, g.A, g.lda, g.A, g.lda, INT64_MAX, k0, kend, m0, g.M, vA,
-                                      tid);
-      } else {
-        for (int idx = tid; idx < BK * BM; idx += NT) {
-          const int k = idx / BM, m = idx % BM;
-          const int64_t r = m0 + m, cc = k0 + k;
-          double v = 0.0;
-          if (r < g.M && cc < kend) v = (r >= cc) ? g.A[r + cc * g.lda] : g.A[cc + r * g.lda];
-          as[k * LDA_KM + m] = v;
-        }
-      }
-    }
-    if (BMD == B_N) {
-      load_tile<BK, BN, LDB_NK, NT>(bs, g.B, g.ldb, g.B, g.ldb, INT64_MAX, k0, kend, n0, g.N, vB,
-                                    tid);
-    } else {
-      load_tile<BN, BK, LDB_KN, NT>(bs, g.B, g.ldb, g.B2, g.ldb2, g.ksplitB, n0, g.N, k0, kend, vB,
-                                    tid);
-    }
-  };
-
-  auto compute_stage = [&](int s, bool amk) {
-    const double* as = As + s * A_STAGE;
-    const double* bs = Bs + s * B_STAGE;
-#pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double af[MI], bf[NI];
-      if (amk) {
-#pragma unroll
-        for (int i = 0; i < MI; ++i) af[i] = as[(wm + i * 8 + gq) * LDA_MK + kk + tq];
-      } else {
-#pragma unroll
-        for (int i = 0; i < MI; ++i) af[i] = as[(kk + tq) * LDA_KM + wm + i * 8 + gq];
-      }
-#pragma unroll
-      for (int j = 0; j < NI; ++j)
-        bf[j] = (BMD == B_N) ? bs[(wn + j * 8 + gq) * LDB_NK + kk + tq]
-                             : bs[(kk + tq) * LDB_KN + wn + j * 8 + gq];
-#pragma unroll
-      for (int i = 0; i < MI; ++i)
-#pragma unroll
-        for (int j = 0; j < NI; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-    }
-  };
-
-  const int nkt = (int)cdiv(kend - kbeg, BK);
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nkt) load_stage(s, kbeg + (int64_t)s * BK);
-    cp_async_commit();
-  }
-  for (int kt = 0; kt < nkt; ++kt) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    const int nk = kt + STAGES - 1;
-    if (nk < nkt) load_stage(nk % STAGES, kbeg + (int64_t)nk * BK);
-    cp_async_commit();
-    const int64_t k0 = kbeg + (int64_t)kt * BK;
-    bool amk = (AM == A_T);
-    if (AM == A_SYM) amk = (sym_case(k0, m0, BK, BM) == 1);
-    if (AM == A_SYM) {
-      if (amk)
-        compute_stage(kt % STAGES, true);
-      else
-        compute_stage(kt % STAGES, false);
-    } else {
-      compute_stage(kt % STAGES, AM == A_T);
-    }
-  }
-  cp_async_wait<0>();
-
-  // ---- epilogue ----
-#pragma unroll
-  for (int i = 0; i < MI; ++i) {
-    const int64_t r = m0 + wm + i * 8 + gq;
-#pragma unroll
-    for (int j = 0; j < NI; ++j) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t c = n0 + wn + j * 8 + 2 * tq + h;
-        if (r >= g.M || c >= nmax) continue;
-        const double v = acc[i][j][h];
-        if (EPI == EPI_GEN) {
-          double out;
-          if (cpre) {
-            out = v;
-          } else {
-            out = g.alpha * v;
-            if (g.beta != 0.0) out += g.beta * g.Cin[r + c * g.ldcin];
-          }
-          g.C[r + c * g.ldc] = out;
-        } else if (EPI == EPI_SPLIT) {
-          g.ws[((int64_t)blockIdx.z * g.N + c) * g.M + r] = v;
-        } else {
-          if (r >= c) g.C[r + c * g.ldc] = v;
-        }
-      }
-    }
-  }
-}
 
 // Fixed-order split-K reduction: C = alpha * sum_z ws[z] + beta * Cin.
 __global__ void splitk_reduce_kernel(int64_t M, int64_t N, int S, const double* __restrict__ ws,
@@ -247,77 +26,54 @@ __global__ void splitk_reduce_kernel(int64_t M, int64_t N, int S, const double* 
   }
 }
 
-// ---------------------------------------------------------------------------
-// host side
-// ---------------------------------------------------------------------------
-
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, int AM, int BMD>
-constexpr int smem_bytes() {
-  constexpr int LDA_KM = BM + 4, LDA_MK = BK + 4;
-  constexpr int A_STAGE = (AM == A_N)   ? BK * LDA_KM
-                          : (AM == A_T) ? BM * LDA_MK
-                                        : (BK * LDA_KM > BM * LDA_MK ? BK * LDA_KM : BM * LDA_MK);
-  constexpr int B_STAGE = (BMD == B_N) ? BN * (BK + 4) : BK * (BN + 4);
-  return STAGES * (A_STAGE + B_STAGE) * 8;
-}
-
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, int AM, int BMD, int EPI>
-static int launch(cudaStream_t st, const GemmArgs& g, dim3 grid) {
-  constexpr int smem = smem_bytes<BM, BN, BK, WM, WN, STAGES, AM, BMD>();
-  auto kern = dgemm_kernel<BM, BN, BK, WM, WN, STAGES, AM, BMD, EPI>;
-  static int attr_dev_mask = 0;  // per-instantiation, per-device
-  int dev = 0;
-  BR_CUDA(cudaGetDevice(&dev));
-  if (!(attr_dev_mask & (1 << dev))) {
-    BR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr_dev_mask |= 1 << dev;
-  }
-  count_launch();
-  kern<<<grid, WM * WN * 32, smem, st>>>(g);
-  BR_CUDA(cudaGetLastError());
-  return 0;
-}
-
-enum TileCfg { CFG_L = 0, CFG_NS = 1, CFG_MS = 2 };
-
-template <int AM, int BMD, int EPI>
-static int launch_cfg(cudaStream_t st, const GemmArgs& g, dim3 grid, int cfg) {
-  switch (cfg) {
-    case CFG_L: return launch<128, 128, 16, 4, 2, 3, AM, BMD, EPI>(st, g, grid);
-    case CFG_NS: return launch<128, 32, 16, 4, 1, 4, AM, BMD, EPI>(st, g, grid);
-    default: return launch<32, 128, 16, 1, 4, 4, AM, BMD, EPI>(st, g, grid);
-  }
-}
-static void cfg_tile(int cfg, int& bm, int& bn, int& ctas_per_sm) {
-  if (cfg == CFG_L) { bm = 128; bn = 128; ctas_per_sm = 1; }
-  else if (cfg == CFG_NS) { bm = 128; bn = 32; ctas_per_sm = 2; }
-  else { bm = 32; bn = 128; ctas_per_sm = 2; }
-}
-
 static inline bool al16(const void* p, int64_t ld) {
   return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && (ld % 2 == 0);
 }
 
+// Tile configuration choices, measured on B200 (tools/gemm_cfg_sweep.sh):
+// 2-CTA/SM tiles win because one CTA's prologue/epilogue overlaps the other's
+// main loop. Environment overrides (tuning aid): BR_GEMM_BIG, BR_GEMM_SYMM,
+// BR_GEMM_LOWER = L|A|B|C|D.
+static int env_cfg(const char* var, int dflt) {
+  if (const char* e = std::getenv(var)) {
+    for (int c = 0; c < CFG_COUNT; ++c)
+      if (std::strcmp(e, kTiles[c].name) == 0) return c;
+  }
+  return dflt;
+}
+static int big_cfg(int am) {
+  static int gen = -1, sym = -1;
+  if (gen < 0) {
+    gen = env_cfg("BR_GEMM_BIG", CFG_C);
+    sym = env_cfg("BR_GEMM_SYMM", CFG_A);
+  }
+  return am == A_SYM ? sym : gen;
+}
+static int lower_cfg() {
+  static int cfg = -1;
+  if (cfg < 0) {
+    cfg = env_cfg("BR_GEMM_LOWER", CFG_L);
+    if (kTiles[cfg].bm != kTiles[cfg].bn) cfg = CFG_L;
+  }
+  return cfg;
+}
+
 // Dispatch a general/symm GEMM: chooses tile config and split-K.
-template <int AM>
-static int run_gemm(cudaStream_t st, Scratch& ws, GemmArgs g, bool btrans, int max_ctas) {
+static int run_gemm(int am, cudaStream_t st, Scratch& ws, GemmArgs g, bool btrans, int max_ctas) {
   if (g.M <= 0 || g.N <= 0) return 0;
   if (g.K <= 0) {  // C = beta*Cin
-    g.k_per_split = 1;
     const int64_t total = g.M * g.N;
     int blocks = (int)std::min<int64_t>(cdiv(total, 256), 4096);
-    // reuse the reduce kernel with S = 0 partials
     count_launch();
     splitk_reduce_kernel<<<blocks, 256, 0, st>>>(g.M, g.N, 0, nullptr, g.alpha, g.beta, g.Cin,
                                                  g.ldcin, g.C, g.ldc);
     BR_CUDA(cudaGetLastError());
     return 0;
   }
-  int cfg = CFG_L;
+  int cfg = big_cfg(am);
   if (g.N <= 32) cfg = CFG_NS;
   else if (g.M <= 32) cfg = CFG_MS;
-  int bm, bn, cps;
-  cfg_tile(cfg, bm, bn, cps);
+  const int bm = kTiles[cfg].bm, bn = kTiles[cfg].bn, cps = kTiles[cfg].ctas_per_sm;
   const int64_t tiles = cdiv(g.M, bm) * cdiv(g.N, bn);
   const int64_t nkt = cdiv(g.K, 16);
   const int sms = ws.num_sms;
@@ -347,23 +103,18 @@ static int run_gemm(cudaStream_t st, Scratch& ws, GemmArgs g, bool btrans, int m
   } else {
     g.k_per_split = g.K;
   }
-  if (max_ctas > 0 && tiles * S > max_ctas) {
-    // caller asked to leave SMs free; the grid is still launched in full, the
-    // hardware scheduler interleaves (persistent scheduling is a later step)
-  }
   dim3 grid((unsigned)cdiv(g.M, bm), (unsigned)cdiv(g.N, bn), (unsigned)S);
+  const int bmd = btrans ? B_T : B_N;
   if (S == 1) {
-    if (btrans) BR_CHECK((launch_cfg<AM, B_T, EPI_GEN>(st, g, grid, cfg)));
-    else BR_CHECK((launch_cfg<AM, B_N, EPI_GEN>(st, g, grid, cfg)));
+    BR_CHECK(launch_tile(cfg, am, bmd, EPI_GEN, st, g, grid));
   } else {
     g.ws = ws.p;
-    if (btrans) BR_CHECK((launch_cfg<AM, B_T, EPI_SPLIT>(st, g, grid, cfg)));
-    else BR_CHECK((launch_cfg<AM, B_N, EPI_SPLIT>(st, g, grid, cfg)));
+    BR_CHECK(launch_tile(cfg, am, bmd, EPI_SPLIT, st, g, grid));
     const int64_t total = g.M * g.N;
     int blocks = (int)std::min<int64_t>(cdiv(total, 256), (int64_t)sms * 8);
     count_launch();
-    splitk_reduce_kernel<<<blocks, 256, 0, st>>>(g.M, g.N, (int)S, ws.p, g.alpha, g.beta,
-                                                 g.Cin, g.ldcin, g.C, g.ldc);
+    splitk_reduce_kernel<<<blocks, 256, 0, st>>>(g.M, g.N, (int)S, ws.p, g.alpha, g.beta, g.Cin,
+                                                 g.ldcin, g.C, g.ldc);
     BR_CUDA(cudaGetLastError());
   }
   return 0;
@@ -411,8 +162,7 @@ int gemm(cudaStream_t st, Scratch& ws, MatView C, MatView A, MatView B, double a
   g.beta = beta;
   g.vecA = al16(A.p, A.ld);
   g.vecB = al16(B.p, B.ld);
-  if (A.trans) return run_gemm<A_T>(st, ws, g, B.trans, max_ctas);
-  return run_gemm<A_N>(st, ws, g, B.trans, max_ctas);
+  return run_gemm(A.trans ? A_T : A_N, st, ws, g, B.trans, max_ctas);
 }
 
 int symm_lower(cudaStream_t st, Scratch& ws, MatView X1, MatView A2, MatView W) {
@@ -443,7 +193,7 @@ int symm_lower(cudaStream_t st, Scratch& ws, MatView X1, MatView A2, MatView W) 
   g.beta = 0.0;
   g.vecA = al16(A2.p, A2.ld);
   g.vecB = al16(W.p, W.ld);
-  return run_gemm<A_SYM>(st, ws, g, false, 0);
+  return run_gemm(A_SYM, st, ws, g, false, 0);
 }
 
 int syr2k_lower(cudaStream_t st, MatView A2, MatView X3, MatView Y, int64_t c0, int64_t c1,
@@ -483,8 +233,9 @@ int syr2k_lower(cudaStream_t st, MatView A2, MatView X3, MatView Y, int64_t c0, 
   g.vecA = al16(X3.p, X3.ld) && al16(Y.p, Y.ld) && (c0 % 2 == 0);
   g.vecB = g.vecA;
   (void)max_ctas;
-  dim3 grid((unsigned)cdiv(j - c0, 128), (unsigned)cdiv(c1 - c0, 128), 1);
-  return launch<128, 128, 16, 4, 2, 3, A_N, B_T, EPI_LOWER>(st, g, grid);
+  const int cfg = lower_cfg();
+  dim3 grid((unsigned)cdiv(j - c0, kTiles[cfg].bm), (unsigned)cdiv(c1 - c0, kTiles[cfg].bn), 1);
+  return launch_tile(cfg, A_N, B_T, EPI_LOWER, st, g, grid);
 }
 
 }  // namespace br

@@ -1,0 +1,50 @@
+// Tile configurations of the DMMA GEMM and their launchers (one translation
+// unit per configuration so they compile in parallel).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "gemm.cuh"
+
+namespace br {
+
+enum TileCfg { CFG_L = 0, CFG_NS, CFG_MS, CFG_A, CFG_B, CFG_C, CFG_D, CFG_COUNT };
+
+struct TileInfo {
+  const char* name;
+  int bm, bn;
+  int ctas_per_sm;  // resident CTAs per SM (registers / shared memory)
+};
+
+//                 name   BM   BN  CTAs/SM
+constexpr TileInfo kTiles[CFG_COUNT] = {
+    {"L", 128, 128, 1},  // 8 warps 4x2, warp 32x64, 3 stages
+    {"NS", 128, 32, 2},  // 4 warps 4x1, warp 32x32, 4 stages (N <= 32)
+    {"MS", 32, 128, 2},  // 4 warps 1x4, warp 32x32, 4 stages (M <= 32)
+    {"A", 128, 64, 2},   // 4 warps 4x1, warp 32x64, 3 stages
+    {"B", 128, 64, 2},   // 8 warps 4x2, warp 32x32, 3 stages
+    {"C", 64, 128, 2},   // 8 warps 2x4, warp 32x32, 3 stages
+    {"D", 64, 64, 3},    // 4 warps 2x2, warp 32x32, 4 stages
+};
+
+int launch_tile_L(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
+int launch_tile_NS(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
+int launch_tile_MS(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
+int launch_tile_A(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
+int launch_tile_B(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
+int launch_tile_C(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
+int launch_tile_D(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
+
+inline int launch_tile(int cfg, int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g,
+                       dim3 grid) {
+  switch (cfg) {
+    case CFG_L: return launch_tile_L(am, bmd, epi, st, g, grid);
+    case CFG_NS: return launch_tile_NS(am, bmd, epi, st, g, grid);
+    case CFG_MS: return launch_tile_MS(am, bmd, epi, st, g, grid);
+    case CFG_A: return launch_tile_A(am, bmd, epi, st, g, grid);
+    case CFG_B: return launch_tile_B(am, bmd, epi, st, g, grid);
+    case CFG_C: return launch_tile_C(am, bmd, epi, st, g, grid);
+    default: return launch_tile_D(am, bmd, epi, st, g, grid);
+  }
+}
+
+}  // namespace br
