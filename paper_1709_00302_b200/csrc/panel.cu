@@ -7,36 +7,30 @@
 //   * compact WY with Q = H_0 ... H_{b-1} = I + W Y^T, W = Y T, T = -T_larft.
 //
 // B200 design. A "leaf" is an L x nb (nb <= 32) block held in the REGISTERS
-// of one thread-block cluster (<= 16 CTAs x 256 threads, each thread owning
-// R rows x NB columns, R*NB = 64 doubles). Each column step needs exactly one
-// cluster-wide reduction of an NB-slot vector:
-//   slots c >= i   : x^T P_c   (c == i gives ||x||^2)        -> Householder
-//   slots c <  i-1 : Y_c^T v_{i-1}  (Gram column of the last reflector) -> T
-// computed per thread with FMAs on registers, reduced across the warp with a
-// transpose-reduction (each lane ends with one slot; 31 shuffles for 32 slots),
-// across warps in shared memory, and across the cluster through DSMEM after
-// one barrier.cluster (buffers double-buffered). Every CTA sums the partials in
-// the same fixed order, so all CTAs hold bit-identical scalars; then
-//     v^T P_c = (x^T P_c - beta * P_ic) / (x0 - beta)
-// gives the rank-1 update of every owned row without a second reduction.
-// Rows above the diagonal are moved out of the registers as soon as they are
-// final (R entries), so the registers always hold Y with an explicit unit
-// diagonal and zeros above it and no per-element masking is needed.
-// T follows the reference recurrence from the Gram columns; W = Y T is formed
-// from the registers. Panels wider than the leaf are processed right-looking:
-// leaf, then the block reflector of that leaf is applied to the rest of the
-// panel with DMMA GEMMs, and the full T is assembled from the Gram matrix.
+// of one thread-block cluster (<= 16 CTAs; each thread owns R rows x NB
+// columns, R*NB = 64 doubles). Each column step needs exactly one
+// cluster-wide reduction of an NB-slot vector (see leaf_reg_kernel), one
+// barrier.cluster, and a rank-1 update of the owned rows:
+//     v^T P_c = (x^T P_c - beta P_ic) / (x0 - beta)
+// so the Householder coefficient of column c is simply
+//     alpha_c = tau v^T P_c = P_ic - (x^T P_c) / beta.
+// Every CTA sums the C partial vectors in the same fixed order, so all CTAs
+// hold bit-identical scalars. T follows the reference recurrence from Gram
+// columns folded into the same reductions; W = Y T is formed on chip.
+// Panels wider than the leaf are processed right-looking: leaf, then the
+// block reflector of that leaf is applied to the rest of the panel with
+// DMMA GEMMs, and the full T is assembled from the Gram matrix.
 #include <algorithm>
+#include <cstdlib>
 
 #include "driver.cuh"
 #include "gemm.cuh"
 
 namespace br {
 
-constexpr int LEAF_NB = 32;   // max leaf width
-constexpr int LT = 256;       // threads per CTA
-constexpr int LW = LT / 32;   // warps per CTA
-constexpr int LEAF_MAXC = 16; // max cluster size (non-portable)
+constexpr int LEAF_NB = 32;    // max leaf width
+constexpr int LEAF_MAXC = 16;  // max cluster size (non-portable)
+static long long* g_leaf_prof = nullptr;  // BR_LEAF_PROF phase counters
 
 struct LeafArgs {
   MatView P;  // L x nb leaf (a transposed view gives the LQ rows)
@@ -49,6 +43,7 @@ struct LeafArgs {
   int64_t ldw;
   int64_t L;
   int nb;
+  long long* prof;  // optional per-phase cycle counters (BR_LEAF_PROF=1)
 };
 
 // Transpose-reduce RC values across a warp: afterwards v[0] of lane l holds
@@ -76,27 +71,37 @@ __device__ __forceinline__ void warp_transpose_reduce(double (&v)[RC], int lane)
   }
 }
 
+__device__ __forceinline__ void st_cluster_v2(uint32_t addr, double a, double b) {
+  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};\n" ::"r"(addr), "d"(a), "d"(b)
+               : "memory");
+}
+
 // One leaf. Thread t of CTA q owns rows q*LT*R + t + k*LT (k < R). Registers
 // hold the active columns ROTATED: p[k][0] is always the current column i,
 // p[k][c'] is column i + c'. The rank-1 update writes p[k][c'] from
 // p[k][c'+1], so the rotation costs no extra instructions and x = p[k][0]
 // needs no select. Finished Y columns go to shared memory (Ys), finished R
-// rows to Rrow. Slots of the reduced vector:
+// rows to Rrow, and rows above the diagonal are zeroed as they finish, so
+// no per-element masking is needed. Slots of the reduced vector:
 //   c' <  NB - i      : x^T P_{i+c'}            (c' = 0 gives ||x||^2)
 //   c' >= NB - i      : Gram entry (c' - NB + i, i - 1) = Y_c^T v_{i-1}
-// Partials are pushed into every CTA's receive buffer with DSMEM stores
-// before the cluster barrier, so the reads after it are local.
-template <int NB, int R>
+// Each CTA pushes its partial vector into every CTA's receive buffer with
+// 16-byte DSMEM stores (spread over the warps) before the cluster barrier,
+// and only the CTA that owns row i pushes that row, so the reads after the
+// barrier are local and the all-to-all traffic is C * NB doubles per CTA.
+template <int NB, int R, int LT>
 __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
+  constexpr int LW = LT / 32;
   constexpr int RC = NB < 16 ? NB : 16;  // slots per transpose-reduce chunk
   constexpr int NCH = NB / RC;
   constexpr int SH = 32 / RC;  // lanes holding the same reduced slot
   constexpr int ROWS = LT * R;  // rows per CTA
   extern __shared__ __align__(16) double Ys[];  // [NB][ROWS]
   __shared__ double wred[LW][NB];
-  __shared__ double recv[2][LEAF_MAXC][NB][2];
-  __shared__ double rowi[NB];
-  __shared__ double alpha_s[NB];
+  __shared__ __align__(16) double recv[2][LEAF_MAXC][NB];
+  __shared__ __align__(16) double recv_row[2][NB];
+  __shared__ __align__(16) double rowi[NB];
+  __shared__ __align__(16) double alpha_s[NB];
   __shared__ double scal[NB][3];  // tau, beta, rinv
   __shared__ double G[NB][NB + 1];
   __shared__ double Ts[NB][NB + 1];
@@ -116,13 +121,23 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
 #pragma unroll
     for (int c = 0; c < NB; ++c) p[k][c] = (valid && c < nb) ? *a.P.at(gr[k], c) : 0.0;
   }
-  if (tid < NB) rowi[tid] = 0.0;
   __syncthreads();
 
   double vprev[R];
 #pragma unroll
   for (int k = 0; k < R; ++k) vprev[k] = 0.0;
 
+  const bool pr = a.prof != nullptr && rank == 0 && tid == 0;
+  long long tp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tc = pr ? clock64() : 0;
+#define BR_PHASE(k)                 \
+  if (pr) {                         \
+    const long long t_ = clock64(); \
+    tp[k] += t_ - tc;               \
+    tc = t_;                        \
+  }
+  // the CTA owning row i (i < nb <= 32 <= ROWS rows per CTA): always CTA 0
+  const bool owner_cta = (base == 0);
   for (int i = 0; i <= nb; ++i) {
     const bool hh = i < nb;  // i == nb: final round, Gram column nb-1 only
     const int buf = i & 1;
@@ -152,56 +167,64 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
       warp_transpose_reduce<RC>(v, lane);
       if ((lane & (SH - 1)) == 0) wred[warp][ch * RC + lane / SH] = v[0];
     }
+    BR_PHASE(0);
     __syncthreads();
-    if (warp == 0 && lane < NB) {
-      double s = 0.0;
+    BR_PHASE(1);
+    // ---- CTA partial (every warp sums the same way), pushed to all CTAs ----
+    if (lane < NB / 2) {
+      double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-      for (int w = 0; w < LW; ++w) s += wred[w][lane];
-      const double rv = rowi[lane];
-      rowi[lane] = 0.0;
-      for (uint32_t q = 0; q < ncta; ++q) {
-        const uint32_t ad = map_cluster(&recv[buf][rank][lane][0], q);
-        st_cluster_f64(ad, s);
-        st_cluster_f64(ad + 8, rv);
+      for (int w = 0; w < LW; ++w) {
+        s0 += wred[w][2 * lane];
+        s1 += wred[w][2 * lane + 1];
+      }
+      const bool push_row = hh && owner_cta;
+      const double r0 = push_row ? rowi[2 * lane] : 0.0, r1 = push_row ? rowi[2 * lane + 1] : 0.0;
+      for (uint32_t q = warp; q < ncta; q += LW) {
+        st_cluster_v2(map_cluster(&recv[buf][rank][2 * lane], q), s0, s1);
+        if (push_row) st_cluster_v2(map_cluster(&recv_row[buf][2 * lane], q), r0, r1);
       }
     }
+    BR_PHASE(2);
     cluster_sync_all();
+    BR_PHASE(3);
     if (warp == 0) {
-      double g = 0.0, pic = 0.0;
-      if (lane < NB) {
-        for (uint32_t q = 0; q < ncta; ++q) {
-          g += recv[buf][q][lane][0];
-          pic += recv[buf][q][lane][1];
-        }
-      }
+      double g = 0.0;
+      const double pic = (lane < NB) ? recv_row[buf][lane] : 0.0;
+      if (lane < NB)
+        for (uint32_t q = 0; q < ncta; ++q) g += recv[buf][q][lane];
       if (i > 0 && lane >= g0 && lane < NB - 1) G[lane - g0][i - 1] = g;
       if (hh) {
         const double nrm2 = __shfl_sync(0xffffffffu, g, 0);
         const double x0 = __shfl_sync(0xffffffffu, pic, 0);
         const double nrm = sqrt(nrm2);
-        double tau = 0.0, beta = 0.0, rinv = 0.0;
+        double beta = 0.0, rb = 0.0, rinv = 0.0;
         if (nrm != 0.0) {
-          const double sign = (x0 < 0.0) ? -1.0 : 1.0;
-          beta = -sign * nrm;
-          const double v0 = x0 - beta;
-          tau = (beta - x0) / beta;
-          rinv = 1.0 / v0;
+          beta = (x0 < 0.0) ? nrm : -nrm;
+          rb = 1.0 / beta;
+          rinv = 1.0 / (x0 - beta);
         }
-        if (lane < NB)
-          alpha_s[lane] = (lane >= 1 && lane < nb - i) ? tau * ((g - beta * pic) * rinv) : 0.0;
+        if (lane < NB)  // tau == 0 (zero column): identity reflector, no update
+          alpha_s[lane] = (nrm != 0.0 && lane >= 1 && lane < nb - i) ? fma(-g, rb, pic) : 0.0;
         if (lane == 0) {
-          scal[i][0] = tau;
+          scal[i][0] = (nrm != 0.0) ? (beta - x0) / beta : 0.0;  // tau (ref kernels.py:109)
           scal[i][1] = beta;
           scal[i][2] = rinv;
         }
       }
     }
+    BR_PHASE(4);
     __syncthreads();
+    BR_PHASE(5);
     if (hh) {
       const double rinv = scal[i][2];
       double al[NB];
 #pragma unroll
-      for (int c = 0; c < NB; ++c) al[c] = alpha_s[c];
+      for (int c = 0; c < NB; c += 2) {
+        const double2 t2 = *reinterpret_cast<const double2*>(&alpha_s[c]);
+        al[c] = t2.x;
+        al[c + 1] = t2.y;
+      }
 #pragma unroll
       for (int k = 0; k < R; ++k) {
         const double vk = (gr[k] == i) ? 1.0 : p[k][0] * rinv;
@@ -219,8 +242,14 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
         }
       }
     }
+    BR_PHASE(6);
   }
+#undef BR_PHASE
   cluster_sync_all();  // all DSMEM traffic done before any CTA may exit
+  if (pr) {
+    for (int k = 0; k < 7; ++k) atomicAdd((unsigned long long*)&a.prof[k], (unsigned long long)tp[k]);
+    atomicAdd((unsigned long long*)&a.prof[7], (unsigned long long)(nb + 1));
+  }
 
   // ---- T by the reference recurrence (ref kernels.py:152-162), one row per lane ----
   if (warp == 0 && lane < nb) {
@@ -275,9 +304,10 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
   }
 }
 
-// rows one cluster holds at leaf width nb: 16 CTAs x 256 threads x R rows
+// Rows one cluster holds at leaf width nb: 16 CTAs x 256 threads x R rows
+// with R * NB = 64 register doubles per thread.
 static int leaf_rows_per_thread(int nb) { return nb > 16 ? 2 : (nb > 8 ? 4 : 8); }
-static int64_t leaf_capacity(int nb) { return (int64_t)LEAF_MAXC * LT * leaf_rows_per_thread(nb); }
+static int64_t leaf_capacity(int nb) { return (int64_t)LEAF_MAXC * 256 * leaf_rows_per_thread(nb); }
 
 // Leaf width for a j x b panel: the widest of {32, 16, 8} (or b if narrower)
 // whose L rows fit one cluster.
@@ -290,10 +320,13 @@ static int leaf_width(int64_t L, int64_t b) {
   return -1;
 }
 
-template <int NB, int R>
-static int launch_leaf_t(cudaStream_t st, const LeafArgs& a, int C) {
-  auto kern = leaf_reg_kernel<NB, R>;
-  const size_t smem = (size_t)NB * LT * R * sizeof(double);
+template <int NB, int R, int LT>
+static int launch_leaf_t(cudaStream_t st, const LeafArgs& a) {
+  auto kern = leaf_reg_kernel<NB, R, LT>;
+  constexpr int ROWS = LT * R;
+  int C = 1;
+  while (C < cdiv(a.L, ROWS)) C *= 2;
+  const size_t smem = (size_t)NB * ROWS * sizeof(double);
   static int attr_dev_mask = 0;
   int dev = 0;
   BR_CUDA(cudaGetDevice(&dev));
@@ -338,26 +371,50 @@ static int launch_leaf(cudaStream_t st, MatView P, MatView Y, double* tau, doubl
   a.ldw = W ? W->ld : 0;
   a.L = L;
   a.nb = nb;
-  auto csize = [&](int64_t rows_per_cta) {
-    int C = 1;
-    while (C < cdiv(L, rows_per_cta)) C *= 2;
-    return C;
-  };
+  a.prof = nullptr;
+  static const bool prof_on = std::getenv("BR_LEAF_PROF") != nullptr;
+  if (prof_on) {
+    if (!g_leaf_prof) {
+      BR_CUDA(cudaMalloc(&g_leaf_prof, 8 * sizeof(long long)));
+      BR_CUDA(cudaMemset(g_leaf_prof, 0, 8 * sizeof(long long)));
+    }
+    a.prof = g_leaf_prof;
+  }
+  // 128-thread CTAs (one warp per SM sub-partition: the per-step reduction is
+  // issue-bound per warp) while one cluster of them holds the leaf; 256
+  // threads for the tallest leaves.
   if (nb > 16) {
-    if (L <= (int64_t)LEAF_MAXC * LT) return launch_leaf_t<32, 1>(st, a, csize(LT));
-    return launch_leaf_t<32, 2>(st, a, csize(2 * LT));
+    if (L <= (int64_t)LEAF_MAXC * 128 * 2) return launch_leaf_t<32, 2, 128>(st, a);
+    return launch_leaf_t<32, 2, 256>(st, a);
   }
   if (nb > 8) {
-    if (L <= (int64_t)LEAF_MAXC * LT) return launch_leaf_t<16, 1>(st, a, csize(LT));
-    return launch_leaf_t<16, 4>(st, a, csize(4 * LT));
+    if (L <= (int64_t)LEAF_MAXC * 128 * 4) return launch_leaf_t<16, 4, 128>(st, a);
+    return launch_leaf_t<16, 4, 256>(st, a);
   }
-  if (L <= (int64_t)LEAF_MAXC * LT) return launch_leaf_t<8, 1>(st, a, csize(LT));
-  return launch_leaf_t<8, 8>(st, a, csize(8 * LT));
+  if (L <= (int64_t)LEAF_MAXC * 128 * 8) return launch_leaf_t<8, 8, 128>(st, a);
+  return launch_leaf_t<8, 8, 256>(st, a);
 }
+
+}  // namespace br
+
+// Print and reset the leaf phase counters (collected when BR_LEAF_PROF is set;
+// development aid, not part of include/bandred_b200.h).
+extern "C" int br_leaf_prof_dump() {
+  if (!br::g_leaf_prof) return 0;
+  long long h[8];
+  if (cudaMemcpy(h, br::g_leaf_prof, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) return 1;
+  const double st = h[7] ? (double)h[7] : 1.0;
+  printf("leaf phases (cycles/step over %lld steps): reduce %.0f sync1 %.0f push %.0f cbar %.0f "
+         "scalars %.0f sync2 %.0f update %.0f\n",
+         h[7], h[0] / st, h[1] / st, h[2] / st, h[3] / st, h[4] / st, h[5] / st, h[6] / st);
+  cudaMemset(br::g_leaf_prof, 0, sizeof(h));
+  return 0;
+}
+
+namespace br {
 
 // T from the Gram matrix, blocked: diagonal 32x32 blocks by the reference
 // recurrence, then T[0:s, s:e] = T[0:s,0:s] * G[0:s, s:e] * T[s:e, s:e].
-// One CTA; b <= 256 keeps everything in L2-resident global scratch.
 __global__ void t_diag_kernel(const double* G, int64_t ldg, const double* tau, int64_t b,
                               double* T, int64_t ldt) {
   // one warp per 32-column diagonal block
@@ -421,12 +478,9 @@ int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView 
   for (int64_t s = 0; s < b; s += nbl) {
     const int64_t e = std::min<int64_t>(s + nbl, b);
     const int64_t w = e - s;
-    const int64_t Ls = j - std::max<int64_t>(s, 0);
     MatView leafP = P.sub(s, s, j - s, w);
     MatView leafY = Y.sub(s, s, j - s, w);
-    // leaf width may need re-evaluation as rows shrink
     BR_CHECK(launch_leaf(st, leafP, leafY, tau + s, tblk, LEAF_NB, nullptr));
-    (void)Ls;
     if (e < b) {
       // P[s:, e:b] += Y_blk (T_blk^T (Y_blk^T P[s:, e:b]))
       MatView rest = P.sub(s, e, j - s, b - e);

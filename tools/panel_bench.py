@@ -23,4 +23,6 @@ for j, b in cases:
                                    W.data_ptr(), ld, tau.data_ptr()), "qr")
         _lib.check(lib.br_sync(h), "sync")
         ts.append(time.perf_counter() - t0)
+    if os.environ.get("BR_LEAF_PROF"):
+        lib.br_leaf_prof_dump()
     print(f"qr_panel {j}x{b}: best {min(ts)*1e6:.1f} us  per column {min(ts)*1e6/b:.2f} us", flush=True)
