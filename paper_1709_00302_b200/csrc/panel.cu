@@ -46,263 +46,9 @@ struct LeafArgs {
   long long* prof;  // optional per-phase cycle counters (BR_LEAF_PROF=1)
 };
 
-// Transpose-reduce RC values across a warp: afterwards v[0] of lane l holds
-// the warp total of slot (l / (32/RC)). Fixed summation tree (deterministic).
-template <int RC>
-__device__ __forceinline__ void warp_transpose_reduce(double (&v)[RC], int lane) {
-  int n = RC;
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
-    if (n > 1) {
-      const bool up = (lane & o) != 0;
-      const int h = n / 2;
-#pragma unroll
-      for (int q = 0; q < RC / 2; ++q) {
-        if (q < h) {
-          const double send = up ? v[q] : v[q + h];
-          const double keep = up ? v[q + h] : v[q];
-          v[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-        }
-      }
-      n = h;
-    } else {
-      v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
-    }
-  }
-}
-
-__device__ __forceinline__ void st_cluster_v2(uint32_t addr, double a, double b) {
-  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};\n" ::"r"(addr), "d"(a), "d"(b)
-               : "memory");
-}
-
-// One leaf. Thread t of CTA q owns rows q*LT*R + t + k*LT (k < R). Registers
-// hold the active columns ROTATED: p[k][0] is always the current column i,
-// p[k][c'] is column i + c'. The rank-1 update writes p[k][c'] from
-// p[k][c'+1], so the rotation costs no extra instructions and x = p[k][0]
-// needs no select. Finished Y columns go to shared memory (Ys), finished R
-// rows to Rrow, and rows above the diagonal are zeroed as they finish, so
-// no per-element masking is needed. Slots of the reduced vector:
-//   c' <  NB - i      : x^T P_{i+c'}            (c' = 0 gives ||x||^2)
-//   c' >= NB - i      : Gram entry (c' - NB + i, i - 1) = Y_c^T v_{i-1}
-// Each CTA pushes its partial vector into every CTA's receive buffer with
-// 16-byte DSMEM stores (spread over the warps) before the cluster barrier,
-// and only the CTA that owns row i pushes that row, so the reads after the
-// barrier are local and the all-to-all traffic is C * NB doubles per CTA.
-template <int NB, int R, int LT>
-__global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
-  constexpr int LW = LT / 32;
-  constexpr int RC = NB < 16 ? NB : 16;  // slots per transpose-reduce chunk
-  constexpr int NCH = NB / RC;
-  constexpr int SH = 32 / RC;  // lanes holding the same reduced slot
-  constexpr int ROWS = LT * R;  // rows per CTA
-  extern __shared__ __align__(16) double Ys[];  // [NB][ROWS]
-  __shared__ double wred[LW][NB];
-  __shared__ __align__(16) double recv[2][LEAF_MAXC][NB];
-  __shared__ __align__(16) double recv_row[2][NB];
-  __shared__ __align__(16) double rowi[NB];
-  __shared__ __align__(16) double alpha_s[NB];
-  __shared__ double scal[NB][3];  // tau, beta, rinv
-  __shared__ double G[NB][NB + 1];
-  __shared__ double Ts[NB][NB + 1];
-  __shared__ double Rrow[NB][NB + 1];
-
-  const uint32_t rank = cluster_ctarank(), ncta = cluster_nctarank();
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nb = a.nb;
-  const int64_t base = (int64_t)rank * ROWS;
-
-  int64_t gr[R];
-  double p[R][NB];
-#pragma unroll
-  for (int k = 0; k < R; ++k) {
-    gr[k] = base + tid + (int64_t)k * LT;
-    const bool valid = gr[k] < a.L;
-#pragma unroll
-    for (int c = 0; c < NB; ++c) p[k][c] = (valid && c < nb) ? *a.P.at(gr[k], c) : 0.0;
-  }
-  __syncthreads();
-
-  double vprev[R];
-#pragma unroll
-  for (int k = 0; k < R; ++k) vprev[k] = 0.0;
-
-  const bool pr = a.prof != nullptr && rank == 0 && tid == 0;
-  long long tp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  long long tc = pr ? clock64() : 0;
-#define BR_PHASE(k)                 \
-  if (pr) {                         \
-    const long long t_ = clock64(); \
-    tp[k] += t_ - tc;               \
-    tc = t_;                        \
-  }
-  // the CTA owning row i (i < nb <= 32 <= ROWS rows per CTA): always CTA 0
-  const bool owner_cta = (base == 0);
-  for (int i = 0; i <= nb; ++i) {
-    const bool hh = i < nb;  // i == nb: final round, Gram column nb-1 only
-    const int buf = i & 1;
-    const int g0 = NB - i;   // first Gram slot
-#pragma unroll
-    for (int k = 0; k < R; ++k)
-      if (hh && gr[k] == i) {
-#pragma unroll
-        for (int c = 0; c < NB; ++c) rowi[c] = p[k][c];
-      }
-    // ---- per-thread partials, transpose-reduced per warp ----
-#pragma unroll
-    for (int ch = 0; ch < NCH; ++ch) {
-      double v[RC];
-#pragma unroll
-      for (int cc = 0; cc < RC; ++cc) {
-        const int c = ch * RC + cc;
-        double s = 0.0;
-#pragma unroll
-        for (int k = 0; k < R; ++k) s = fma(p[k][0], p[k][c], s);
-        if (c >= g0 && c < NB - 1) {  // Gram entry (c - g0, i - 1)
-#pragma unroll
-          for (int k = 0; k < R; ++k) s = fma(vprev[k], Ys[(c - g0) * ROWS + tid + k * LT], s);
-        }
-        v[cc] = s;
-      }
-      warp_transpose_reduce<RC>(v, lane);
-      if ((lane & (SH - 1)) == 0) wred[warp][ch * RC + lane / SH] = v[0];
-    }
-    BR_PHASE(0);
-    __syncthreads();
-    BR_PHASE(1);
-    // ---- CTA partial (every warp sums the same way), pushed to all CTAs ----
-    if (lane < NB / 2) {
-      double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-      for (int w = 0; w < LW; ++w) {
-        s0 += wred[w][2 * lane];
-        s1 += wred[w][2 * lane + 1];
-      }
-      const bool push_row = hh && owner_cta;
-      const double r0 = push_row ? rowi[2 * lane] : 0.0, r1 = push_row ? rowi[2 * lane + 1] : 0.0;
-      for (uint32_t q = warp; q < ncta; q += LW) {
-        st_cluster_v2(map_cluster(&recv[buf][rank][2 * lane], q), s0, s1);
-        if (push_row) st_cluster_v2(map_cluster(&recv_row[buf][2 * lane], q), r0, r1);
-      }
-    }
-    BR_PHASE(2);
-    cluster_sync_all();
-    BR_PHASE(3);
-    if (warp == 0) {
-      double g = 0.0;
-      const double pic = (lane < NB) ? recv_row[buf][lane] : 0.0;
-      if (lane < NB)
-        for (uint32_t q = 0; q < ncta; ++q) g += recv[buf][q][lane];
-      if (i > 0 && lane >= g0 && lane < NB - 1) G[lane - g0][i - 1] = g;
-      if (hh) {
-        const double nrm2 = __shfl_sync(0xffffffffu, g, 0);
-        const double x0 = __shfl_sync(0xffffffffu, pic, 0);
-        const double nrm = sqrt(nrm2);
-        double beta = 0.0, rb = 0.0, rinv = 0.0;
-        if (nrm != 0.0) {
-          beta = (x0 < 0.0) ? nrm : -nrm;
-          rb = 1.0 / beta;
-          rinv = 1.0 / (x0 - beta);
-        }
-        if (lane < NB)  // tau == 0 (zero column): identity reflector, no update
-          alpha_s[lane] = (nrm != 0.0 && lane >= 1 && lane < nb - i) ? fma(-g, rb, pic) : 0.0;
-        if (lane == 0) {
-          scal[i][0] = (nrm != 0.0) ? (beta - x0) / beta : 0.0;  // tau (ref kernels.py:109)
-          scal[i][1] = beta;
-          scal[i][2] = rinv;
-        }
-      }
-    }
-    BR_PHASE(4);
-    __syncthreads();
-    BR_PHASE(5);
-    if (hh) {
-      const double rinv = scal[i][2];
-      double al[NB];
-#pragma unroll
-      for (int c = 0; c < NB; c += 2) {
-        const double2 t2 = *reinterpret_cast<const double2*>(&alpha_s[c]);
-        al[c] = t2.x;
-        al[c + 1] = t2.y;
-      }
-#pragma unroll
-      for (int k = 0; k < R; ++k) {
-        const double vk = (gr[k] == i) ? 1.0 : p[k][0] * rinv;
-        Ys[i * ROWS + tid + k * LT] = vk;  // Y column i (unit diagonal, zeros above)
-        vprev[k] = vk;
-#pragma unroll
-        for (int c = 0; c < NB - 1; ++c) p[k][c] = fma(-vk, al[c + 1], p[k][c + 1]);
-        p[k][NB - 1] = 0.0;
-        if (gr[k] == i) {  // row i is final: move its R entries (columns i+1..) out
-#pragma unroll
-          for (int c = 0; c < NB - 1; ++c) {
-            if (c < nb - 1 - i) Rrow[i][i + 1 + c] = p[k][c];
-            p[k][c] = 0.0;
-          }
-        }
-      }
-    }
-    BR_PHASE(6);
-  }
-#undef BR_PHASE
-  cluster_sync_all();  // all DSMEM traffic done before any CTA may exit
-  if (pr) {
-    for (int k = 0; k < 7; ++k) atomicAdd((unsigned long long*)&a.prof[k], (unsigned long long)tp[k]);
-    atomicAdd((unsigned long long*)&a.prof[7], (unsigned long long)(nb + 1));
-  }
-
-  // ---- T by the reference recurrence (ref kernels.py:152-162), one row per lane ----
-  if (warp == 0 && lane < nb) {
-    const int r = lane;
-    for (int c = 0; c < NB; ++c) Ts[r][c] = 0.0;
-    Ts[r][r] = -scal[r][0];
-    for (int i = r + 1; i < nb; ++i) {
-      double s0 = 0.0, s1 = 0.0;
-      int c = r;
-      for (; c + 1 < i; c += 2) {
-        s0 = fma(Ts[r][c], G[c][i], s0);
-        s1 = fma(Ts[r][c + 1], G[c + 1][i], s1);
-      }
-      if (c < i) s0 = fma(Ts[r][c], G[c][i], s0);
-      Ts[r][i] = -scal[i][0] * (s0 + s1);
-    }
-  }
-  __syncthreads();
-
-  // ---- outputs: Y, R, W = Y T, tau, T ----
-#pragma unroll
-  for (int k = 0; k < R; ++k) {
-    if (gr[k] >= a.L) continue;
-    const int lr = tid + k * LT;
-    for (int c = 0; c < nb; ++c) a.Y[gr[k] + (int64_t)c * a.ldy] = Ys[c * ROWS + lr];
-    if (gr[k] < nb) {
-      const int r = (int)gr[k];
-      for (int c = r; c < nb; ++c) *a.P.at(r, c) = (c == r) ? scal[r][1] : Rrow[r][c];
-    }
-    if (a.W) {
-      double y[NB];
-#pragma unroll
-      for (int m = 0; m < NB; ++m) y[m] = (m < nb) ? Ys[m * ROWS + lr] : 0.0;
-#pragma unroll
-      for (int c = 0; c < NB; ++c) {
-        if (c >= nb) continue;
-        double s = 0.0;
-#pragma unroll
-        for (int m = 0; m < NB; ++m)
-          if (m <= c) s = fma(y[m], Ts[m][c], s);
-        a.W[gr[k] + (int64_t)c * a.ldw] = s;
-      }
-    }
-  }
-  if (rank == 0) {
-    if (tid < nb) a.tau[tid] = scal[tid][0];
-    if (a.T)
-      for (int q = tid; q < nb * nb; q += LT) {
-        const int r = q % nb, c = q / nb;
-        a.T[r + (int64_t)c * a.ldt] = Ts[r][c];
-      }
-  }
-}
+}  // namespace br
+#include "panel_leaf.cuh"  // leaf_reg_kernel<NB, R, LT>
+namespace br {
 
 // Rows one cluster holds at leaf width nb: 16 CTAs x 256 threads x R rows
 // with R * NB = 64 register doubles per thread.

@@ -1,0 +1,349 @@
+// Register-resident cluster leaf of the Householder panel (included by panel.cu).
+#pragma once
+#include "common.cuh"
+
+namespace br {
+
+__device__ __forceinline__ void mbar_init(uint64_t* m, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* m, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   smem_u32(m)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* m, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; "
+      "selp.u32 %0, 1, 0, p; }"
+      : "=r"(ok)
+      : "r"(smem_u32(m)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// Stores into another CTA's shared memory that complete their bytes on that
+// CTA's mbarrier transaction count (no cluster barrier, no fence).
+__device__ __forceinline__ void st_async_v2(uint32_t raddr, double a, double b, uint32_t rmbar) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(
+          raddr),
+      "d"(a), "d"(b), "r"(rmbar)
+      : "memory");
+}
+
+// Transpose-reduce RC values across a warp: afterwards v[0] of lane l holds
+// the warp total of slot (l / (32/RC)). Fixed summation tree (deterministic).
+template <int RC>
+__device__ __forceinline__ void warp_transpose_reduce(double (&v)[RC], int lane) {
+  int n = RC;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    if (n > 1) {
+      const bool up = (lane & o) != 0;
+      const int h = n / 2;
+#pragma unroll
+      for (int q = 0; q < RC / 2; ++q) {
+        if (q < h) {
+          const double send = up ? v[q] : v[q + h];
+          const double keep = up ? v[q + h] : v[q];
+          v[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+      n = h;
+    } else {
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+    }
+  }
+}
+
+// One leaf (L x nb, nb <= NB) of a Householder panel.
+//
+// Thread t of CTA q owns rows q*LT*R + t + k*LT (k < R). Its registers p[k][]
+// hold, ROTATED, the active columns followed by the finished Y columns:
+// at step i, p[k][0..nb-i) are columns i..nb-1 (p[k][0] = current column),
+// and p[k][NB-i..NB) are Y_0..Y_{i-1} (explicit unit diagonal, zeros above).
+// The rank-1 update writes p[k][c] from p[k][c+1] and appends the new Y
+// column at NB-1, so the rotation is free and no element ever needs a mask.
+// Slots of the per-step reduced vector:
+//   c <  NB - i : x^T P_{i+c}                  (c = 0 gives ||x||^2)
+//   c >= NB - i : Y_{c-NB+i}^T v_{i-1}          (Gram column i-1, for T)
+// Per step: FMAs on registers, a warp transpose-reduction (shuffles), the
+// per-warp partials through shared memory, then warp w pushes its slots with
+// st.async into every CTA of the cluster, completing bytes on that CTA's
+// mbarrier (double-buffered). The CTA owning row i also pushes row i. Every
+// thread waits on its own mbarrier - no cluster barrier, no fence - and every
+// warp forms the same scalars from the received vectors in the same order:
+//   beta = -sign(x0)||x||,  alpha_c = tau v^T P_c = P_ic - (x^T P_c)/beta,
+//   v = x / (x0 - beta)
+// so all CTAs hold bit-identical reflectors.
+template <int NB, int R, int LT>
+__global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
+  constexpr int LW = LT / 32;
+  constexpr int RC = NB < 16 ? NB : 16;  // slots per transpose-reduce chunk
+  constexpr int NCH = NB / RC;
+  constexpr int SH = 32 / RC;    // lanes holding the same reduced slot
+  constexpr int SPW = (NB / LW >= 2) ? NB / LW : 2;  // slots pushed by each pushing warp
+  constexpr int NPW = NB / SPW;                       // pushing warps
+  constexpr int ROWS = LT * R;                        // rows per CTA
+  static_assert(SPW * NPW == NB && NPW <= LW, "slot split");
+  extern __shared__ __align__(16) double Ys[];  // [NB][ROWS], epilogue only
+  __shared__ double wred[LW][NB];
+  __shared__ __align__(16) double recv[2][LEAF_MAXC][NB];
+  __shared__ __align__(16) double recv_row[2][NB];
+  __shared__ __align__(16) double rowi[NB];
+  __shared__ __align__(16) double alw[LW][NB];
+  __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ double scal[NB][3];  // tau, beta, rinv
+  __shared__ double G[NB][NB + 1];
+  __shared__ double Ts[NB][NB + 1];
+  __shared__ double Rrow[NB][NB + 1];
+
+  const uint32_t rank = cluster_ctarank(), ncta = cluster_nctarank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nb = a.nb;
+  const int64_t base = (int64_t)rank * ROWS;
+  const bool owner_cta = (base == 0);  // row i < nb <= 32 always lives in CTA 0
+
+  int64_t gr[R];
+  double p[R][NB];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    gr[k] = base + tid + (int64_t)k * LT;
+    const bool valid = gr[k] < a.L;
+#pragma unroll
+    for (int c = 0; c < NB; ++c) p[k][c] = (valid && c < nb) ? *a.P.at(gr[k], c) : 0.0;
+  }
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  cluster_sync_all();  // mbarriers initialized cluster-wide before any st.async
+
+  const bool pr = a.prof != nullptr && rank == 0 && tid == 0;
+  long long tp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tc = pr ? clock64() : 0;
+#define BR_PHASE(k)                 \
+  if (pr) {                         \
+    const long long t_ = clock64(); \
+    tp[k] += t_ - tc;               \
+    tc = t_;                        \
+  }
+  for (int i = 0; i <= nb; ++i) {
+    const bool hh = i < nb;  // i == nb: final round, Gram column nb-1 only
+    const int buf = i & 1;
+    const int g0 = NB - i;  // first Gram slot
+    if (tid == 0) mbar_arrive_expect_tx(&mbar[buf], ncta * NB * 8 + (hh ? NB * 8 : 0));
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+      if (hh && gr[k] == i) {
+#pragma unroll
+        for (int c = 0; c < NB; c += 2)
+          *reinterpret_cast<double2*>(&rowi[c]) = make_double2(p[k][c], p[k][c + 1]);
+      }
+    // ---- per-thread partials, transpose-reduced per warp ----
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) {
+      double v[RC];
+#pragma unroll
+      for (int cc = 0; cc < RC; ++cc) {
+        const int c = ch * RC + cc;
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < R; ++k) s = fma((c < g0) ? p[k][0] : p[k][NB - 1], p[k][c], s);
+        v[cc] = s;
+      }
+      warp_transpose_reduce<RC>(v, lane);
+      if ((lane & (SH - 1)) == 0) wred[warp][ch * RC + lane / SH] = v[0];
+    }
+    BR_PHASE(0);
+    __syncthreads();
+    BR_PHASE(1);
+    // ---- warp w sums and pushes slots [w*SPW, (w+1)*SPW) to every CTA ----
+    if (warp < NPW) {
+      constexpr int NP = SPW / 2;  // slot pairs per warp
+      const int ntask = NP * (int)ncta;
+      const bool push_row = hh && owner_cta;
+      for (int t0 = 0; t0 < ntask; t0 += 32) {
+        const int t = t0 + lane;
+        if (t < ntask) {
+          const int pp = t / (int)ncta;
+          const uint32_t q = (uint32_t)(t % (int)ncta);
+          const int c = warp * SPW + 2 * pp;
+          double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+          for (int w = 0; w < LW; ++w) {
+            s0 += wred[w][c];
+            s1 += wred[w][c + 1];
+          }
+          const uint32_t rm = map_cluster(&mbar[buf], q);
+          st_async_v2(map_cluster(&recv[buf][rank][c], q), s0, s1, rm);
+          if (push_row) st_async_v2(map_cluster(&recv_row[buf][c], q), rowi[c], rowi[c + 1], rm);
+        }
+      }
+    }
+    BR_PHASE(2);
+    while (!mbar_try_wait(&mbar[buf], (i >> 1) & 1)) {
+    }
+    BR_PHASE(3);
+    // ---- every warp: the same scalars from the same received vectors ----
+    double rinv = 0.0;
+    {
+      double g0s = 0.0, g1s = 0.0;
+      const double pic = (lane < NB) ? recv_row[buf][lane] : 0.0;
+      if (lane < NB) {
+        uint32_t q = 0;
+        for (; q + 1 < ncta; q += 2) {
+          g0s += recv[buf][q][lane];
+          g1s += recv[buf][q + 1][lane];
+        }
+        if (q < ncta) g0s += recv[buf][q][lane];
+      }
+      const double g = g0s + g1s;
+      if (warp == 0 && i > 0 && lane >= g0 && lane < NB - 1) G[lane - g0][i - 1] = g;
+      if (hh) {
+        const double nrm2 = __shfl_sync(0xffffffffu, g, 0);
+        const double x0 = __shfl_sync(0xffffffffu, pic, 0);
+        // beta from the correctly rounded sqrt (it is the R diagonal); the
+        // two reciprocals on the critical path use rsqrt / rcp (~1 ulp)
+        double beta = 0.0, rb = 0.0;
+        if (nrm2 != 0.0) {
+          const double nrm = sqrt(nrm2), rs = rsqrt(nrm2);
+          beta = (x0 < 0.0) ? nrm : -nrm;
+          rb = (x0 < 0.0) ? rs : -rs;
+          rinv = __drcp_rn(x0 - beta);
+        }
+        if (lane < NB)  // tau == 0 (zero column): identity reflector, no update
+          alw[warp][lane] = (nrm2 != 0.0 && lane >= 1 && lane < nb - i) ? fma(-g, rb, pic) : 0.0;
+        if (warp == 0 && lane == 0) {
+          scal[i][0] = (nrm2 != 0.0) ? (beta - x0) / beta : 0.0;  // tau (ref kernels.py:109)
+          scal[i][1] = beta;
+          scal[i][2] = rinv;
+        }
+        __syncwarp();
+      }
+    }
+    BR_PHASE(4);
+    if (hh) {
+      double al[NB];
+#pragma unroll
+      for (int c = 0; c < NB; c += 2) {
+        const double2 t2 = *reinterpret_cast<const double2*>(&alw[warp][c]);
+        al[c] = t2.x;
+        al[c + 1] = t2.y;
+      }
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const double vk = (gr[k] == i) ? 1.0 : p[k][0] * rinv;
+#pragma unroll
+        for (int c = 0; c < NB - 1; ++c) p[k][c] = fma(-vk, al[c + 1], p[k][c + 1]);
+        p[k][NB - 1] = vk;  // Y column i (unit diagonal, zeros above)
+        if (gr[k] == i) {  // row i is final: move its R entries (columns i+1..) out
+#pragma unroll
+          for (int c = 0; c < NB - 1; ++c)
+            if (c < nb - 1 - i) {
+              Rrow[i][i + 1 + c] = p[k][c];
+              p[k][c] = 0.0;
+            }
+        }
+      }
+    }
+    BR_PHASE(6);
+  }
+#undef BR_PHASE
+  if (pr) {
+    for (int k = 0; k < 7; ++k) atomicAdd((unsigned long long*)&a.prof[k], (unsigned long long)tp[k]);
+    atomicAdd((unsigned long long*)&a.prof[7], (unsigned long long)(nb + 1));
+  }
+
+  // ---- Y from the register tail: column c at p[k][NB - nb + c] ----
+  if (nb == NB) {
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+#pragma unroll
+      for (int c = 0; c < NB; ++c) Ys[c * ROWS + tid + k * LT] = p[k][c];
+  } else {
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+#pragma unroll
+      for (int c = 0; c < NB; ++c) {
+        const int src = NB - nb + c;  // runtime-dependent: select from the array
+        double y = 0.0;
+#pragma unroll
+        for (int m = 0; m < NB; ++m)
+          if (m == src) y = p[k][m];
+        Ys[c * ROWS + tid + k * LT] = (c < nb) ? y : 0.0;
+      }
+    }
+  }
+  // ---- T by the reference recurrence (ref kernels.py:152-162), one row per lane ----
+  if (warp == 0 && lane < NB) {
+    const int r = lane;
+    for (int c = 0; c < NB; ++c) Ts[r][c] = 0.0;
+    if (r < nb) {
+      Ts[r][r] = -scal[r][0];
+      for (int i = r + 1; i < nb; ++i) {
+        double s0 = 0.0, s1 = 0.0;
+        int c = r;
+        for (; c + 1 < i; c += 2) {
+          s0 = fma(Ts[r][c], G[c][i], s0);
+          s1 = fma(Ts[r][c + 1], G[c + 1][i], s1);
+        }
+        if (c < i) s0 = fma(Ts[r][c], G[c][i], s0);
+        Ts[r][i] = -scal[i][0] * (s0 + s1);
+      }
+    }
+  }
+  __syncthreads();
+  cluster_sync_all();  // no remote traffic is in flight when any CTA exits
+
+  // ---- outputs: Y, R ----
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    if (gr[k] >= a.L) continue;
+    const int lr = tid + k * LT;
+    for (int c = 0; c < nb; ++c) a.Y[gr[k] + (int64_t)c * a.ldy] = Ys[c * ROWS + lr];
+    if (gr[k] < nb) {
+      const int r = (int)gr[k];
+      for (int c = r; c < nb; ++c) *a.P.at(r, c) = (c == r) ? scal[r][1] : Rrow[r][c];
+    }
+  }
+  // ---- W = Y T on the tensor cores: each warp 8-row slabs x NB columns ----
+  if (a.W) {
+    for (int r0 = warp * 8; r0 < ROWS; r0 += LW * 8) {
+      if (base + r0 >= a.L) break;
+      double acc[NB / 8][2];
+#pragma unroll
+      for (int n = 0; n < NB / 8; ++n) acc[n][0] = acc[n][1] = 0.0;
+      const int gq = lane >> 2, tq = lane & 3;
+#pragma unroll
+      for (int k0 = 0; k0 < NB; k0 += 4) {
+        const double av = Ys[(k0 + tq) * ROWS + r0 + gq];  // A = Y (8 x 4)
+#pragma unroll
+        for (int n = 0; n < NB / 8; ++n) dmma884(acc[n][0], acc[n][1], av, Ts[k0 + tq][n * 8 + gq]);
+      }
+      const int64_t row = base + r0 + gq;
+      if (row < a.L) {
+#pragma unroll
+        for (int n = 0; n < NB / 8; ++n)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = n * 8 + 2 * tq + h;
+            if (c < nb) a.W[row + (int64_t)c * a.ldw] = acc[n][h];
+          }
+      }
+    }
+  }
+  if (rank == 0) {
+    if (tid < nb) a.tau[tid] = scal[tid][0];
+    if (a.T)
+      for (int q = tid; q < nb * nb; q += LT) {
+        const int r = q % nb, c = q / nb;
+        a.T[r + (int64_t)c * a.ldt] = Ts[r][c];
+      }
+  }
+}
+
+}  // namespace br
