@@ -58,8 +58,6 @@ def house_gen(x, device=None):
 
 
 def _panel(P, lq, device):
-    h, dev = _dev.ctx(device)
-    lib = _lib.load()
     if lq:
         b, j = P.shape
     else:
@@ -67,6 +65,8 @@ def _panel(P, lq, device):
     if j < b or b < 1:
         kind = "lq_panel needs b x j with" if lq else "qr_panel needs"
         raise ValueError(f"{kind} j >= b >= 1, got {P.shape[0]} x {P.shape[1]}")
+    h, dev = _dev.ctx(device)
+    lib = _lib.load()
     D = _dev.DevMat.from_host(P, dev)
     Y = _dev.DevMat(j, b, dev)
     T = _dev.DevMat(b, b, dev, zero=True)

@@ -1,0 +1,123 @@
+"""Host-side logic of the drop-in that runs without a GPU: configs and their
+validation (same errors as the reference), schedules, reference-equivalent
+flop accounting, and the no-CPU-fallback rule."""
+import os
+import warnings
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1709_00302_b200 as br
+from paper_1709_00302_b200 import flops as F
+from paper_1709_00302_b200 import sevp as S
+
+G = os.path.join(os.path.dirname(__file__), "golden")
+RED = np.load(os.path.join(G, "reductions.npz"))
+
+SEVP = [("s64_8_8", "reference"), ("s100_12_5", "reference"), ("s130_16_16", "v2"),
+        ("s97_16_16", "reference"), ("s256_32_32", "v2"), ("s200_40_10", "v1"),
+        ("s300_64_64", "reference")]
+TRI = ["t64_8_8", "t100_80_12_5", "t70_90_6_6", "t256_32_32", "t97_16_16", "t300_64_64"]
+
+
+@pytest.mark.parametrize("name,variant", SEVP)
+def test_sevp_flops_equal_reference_counter(name, variant):
+    n, w, b, iters, flops = (int(x) for x in RED[f"{name}_meta"])
+    got, it = F.sevp_counted_flops(n, w, b, variant)
+    assert it == iters and got["total"] == flops
+
+
+@pytest.mark.parametrize("name", TRI)
+def test_tri_flops_equal_reference_counter(name):
+    m, n, w, b, iters, flops, _, _ = (int(x) for x in RED[f"{name}_meta"])
+    got, it = F.tri_counted_flops(m, n, w, b)
+    assert it == iters and got["total"] == flops
+
+
+def test_counted_flops_track_nominal():
+    # pkg/tests/test_sevp.py:237-241 and AC5 (5% / 8% / 10%)
+    got, _ = F.sevp_counted_flops(1000, 16, 8)
+    assert abs(got["total"] - F.sevp_nominal_flops(1000)) <= 0.05 * F.sevp_nominal_flops(1000)
+    got, _ = F.tri_counted_flops(1000, 1000, 16, 8)
+    assert abs(got["total"] - F.svd_nominal_flops(1000, 1000)) <= 0.08 * F.svd_nominal_flops(1000, 1000)
+
+
+def test_nominal_flops_formulas():
+    assert br.sevp_nominal_flops(0) == 0 and br.sevp_nominal_flops(3) == 36
+    assert br.svd_nominal_flops(9, 9) == 1944 and br.svd_nominal_flops(12, 8) == 2389
+    with pytest.raises(ValueError):
+        br.sevp_nominal_flops(-1)
+    with pytest.raises(ValueError):
+        br.svd_nominal_flops(8, 12)
+
+
+def test_schedules_match_oracle():
+    for n, w, b in ((2048, 32, 32), (130, 16, 16), (97, 16, 16), (100, 12, 5), (5, 4, 2)):
+        assert S._schedule(n, w, b) == O.sevp_schedule(n, w, b)
+
+
+def test_config_validation_like_reference():
+    # pkg/tests/test_sevp.py:207-220
+    with pytest.raises(ValueError):
+        br.SevpConfig(20, 4, 3, br.SevpVariant.V1).validate()
+    with pytest.warns(RuntimeWarning):
+        br.SevpConfig(20, 6, 2, br.SevpVariant.V2).validate()
+    for bad in (br.SevpConfig(0, 2, 1), br.SevpConfig(8, 0, 1), br.SevpConfig(8, 2, 3)):
+        with pytest.raises(ValueError):
+            bad.validate()
+    # pkg/tests/test_svd.py:302-304: triband accepts only the reference schedule
+    with pytest.raises(ValueError):
+        br.SvdConfig(8, 8, 2, 2, br.SvdForm.TRIANGULAR_BAND, br.SvdVariant.V2).validate()
+    with pytest.raises(ValueError):
+        br.SvdConfig(8, 8, 4, 3, br.SvdForm.BAND, br.SvdVariant.V1).validate()
+
+
+def test_input_validation_precedes_device_work():
+    """Shape / argument errors are ValueError with no GPU involved."""
+    with pytest.raises(ValueError):
+        br.reduce_sym_band(np.zeros((4, 5)), br.SevpConfig(4, 2, 1))
+    with pytest.raises(ValueError):
+        br.reduce_sym_band(np.zeros((8, 8)), br.SevpConfig(9, 2, 1))
+    with pytest.raises(ValueError):
+        br.reduce_sym_band(np.zeros((8, 8)), br.SevpConfig(8, 2, 3))
+    with pytest.raises(ValueError):
+        br.reduce_tri_band(np.zeros((8, 6)), w=0, b=1)
+    with pytest.raises(ValueError):
+        br.reduce_tri_band(np.zeros((8, 6)), w=2, b=3)
+    with pytest.raises(ValueError):
+        br.reduce_tri_band(np.zeros(5), w=2, b=1)
+    with pytest.raises(ValueError):
+        br.qr_panel(np.zeros((2, 3)))
+    with pytest.raises(ValueError):
+        br.lq_panel(np.zeros((3, 2)))
+    with pytest.raises(ValueError):
+        br.reduce_sym_band(np.zeros((8, 8)), br.SevpConfig(8, 2, 1), lookahead=2)
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: covered by the gpu tests")
+    A = np.eye(40)
+    with pytest.raises(RuntimeError):
+        br.reduce_sym_band(A, br.SevpConfig(40, 4, 4))
+    with pytest.raises(RuntimeError):
+        br.reduce_tri_band(A, 4, 4)
+    with pytest.raises(RuntimeError):
+        br.qr_panel(np.ones((8, 2)))
+
+
+def test_band_form_not_silently_computed_on_cpu():
+    with pytest.raises((NotImplementedError, RuntimeError)):
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            br.reduce_band_svd(np.ones((20, 20)), br.SvdConfig(20, 20, 4, 4))
+
+
+def test_exec_groups_maps_to_lookahead_depth():
+    assert S._depth(br.SevpConfig(8, 4, 4), br.ExecGroups(4, 0), None) == 0
+    assert S._depth(br.SevpConfig(8, 4, 4, br.SevpVariant.V2), br.ExecGroups(4, 1), None) == 1
+    assert S._depth(br.SevpConfig(8, 4, 4), None, None) == 0
+    assert S._depth(br.SevpConfig(8, 4, 4), None, 1) == 1
