@@ -1,0 +1,22 @@
+#!/bin/bash
+# Round profiling pass (run under gpurun). Each ncu command follows a plain run
+# of the same command that exited 0.
+set -x
+mkdir -p gpurun_out
+CMD="python bench.py --config c4 --steps 1 --warmup 1 --no-cpu --e2e-steps 1"
+$CMD > gpurun_out/prof_plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none -c 40000 --csv \
+    --log-file gpurun_out/launches_c4.csv $CMD > gpurun_out/ncu_launch.log 2>&1
+CMD1="python bench.py --config c1 --steps 1 --warmup 1 --no-cpu --e2e-steps 1"
+$CMD1 > gpurun_out/prof_plain1.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv \
+    --log-file gpurun_out/launches_c1.csv $CMD1 > gpurun_out/ncu_launch1.log 2>&1
+CMD2="python tools/gemm_bench.py left 16384 16128 256 1"
+$CMD2 > /dev/null 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:dgemm -c 2 \
+    -o gpurun_out/prof_gemm $CMD2 > gpurun_out/ncu_full_gemm.log 2>&1
+CMD3="python tools/panel_bench.py 16384x16"
+$CMD3 > /dev/null 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:leaf -c 1 \
+    -o gpurun_out/prof_leaf $CMD3 > gpurun_out/ncu_full_leaf.log 2>&1
+ls -la gpurun_out
