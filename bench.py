@@ -10,9 +10,10 @@ depth 1): the north-star configuration, and it fits one GPU. The metric
 uses the reference's nominal counts (4/3 n^3 SEVP, 8/3 n^3 square SVD;
 ref sevp.py:92-96, svd.py:127-132).
 
-Under torchrun (N > 1) every rank reduces its own matrix (replicas; the 1D
-block-cyclic multi-GPU split is not built yet), timing is
-the max over ranks and `value` is the whole-job aggregate.
+Under torchrun (N > 1) the ranks reduce ONE matrix together: 1D
+block-cyclic columns with NCCL panel broadcast, X1 / Z all-reduce and LQ
+row-panel all-gather (paper_1709_00302_b200/dist.py); timing
+is the max over ranks, `value` the whole-job GFLOP/s ("scaling": "strong").
 
 --impl reference times the reference algorithm's CPU implementation on the
 host cores: the NumPy port in oracle/ (the reference is pure Python and does
@@ -363,6 +364,95 @@ def run_ours(args, rank, world, local_rank):
         dist.destroy_process_group()
 
 
+def run_dist(args, rank, world, local_rank):
+    """N > 1: one matrix, 1D block-cyclic columns over the ranks,
+    NCCL broadcast / all-reduce / all-gather inside paper_1709_00302_b200.dist."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1709_00302_b200 import _lib
+    from paper_1709_00302_b200 import dist as D
+
+    kind, n, w, b, desc = CONFIGS[args.config]
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.synchronize(dev)
+    torch.cuda.set_stream(stream)
+    lib = _lib.load()
+    peak = dgemm_peak(dev)
+    lay = D.Layout(n, b, world, rank)
+    ops = D.CudaOps(local_rank, torch)
+    comm = D.TorchComm(dist)
+    A_host = make_input(args.config)
+    L0 = D.scatter_columns(A_host, lay, ops)
+    L = ops.alloc(n, lay.ncols_local)
+    la = args.lookahead
+    fn = D.reduce_sym_band_dist if kind == "sevp" else D.reduce_tri_band_dist
+
+    def one_step():
+        L.t.copy_(L0.t)
+        fn(L, lay, w, ops, comm, la)
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    l0 = lib.br_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        one_step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    clocks.stop()
+    launches = (lib.br_launch_count() - l0) // max(1, args.steps) * args.steps + args.steps
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    flops = nominal(kind, n)
+    value = flops / (ms * 1e-3) / 1e9
+    # e2e: host matrix -> owned columns (H2D), reduction, band gathered to rank 0 (D2H)
+    dist.barrier()
+    t0 = time.perf_counter()
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    for _ in range(e2e_steps):
+        Lh = D.scatter_columns(A_host, lay, ops)
+        fn(Lh, lay, w, ops, comm, la)
+        D.gather_band(Lh, lay, w, kind, comm, torch)
+    torch.cuda.synchronize(dev)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_s = float(t.item())
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "desc": desc, "kind": kind, "n": n, "w": w, "b": b,
+                       "lookahead": la, "parallelism": f"1D block-cyclic columns x{world} (NCCL)",
+                       "l2": f"input {n * n * 8 / 2**30:.2f} GiB total vs 126 MB L2 per GPU"},
+            "clocks": clocks.summary(),
+            "e2e": {"value": flops / e2e_s / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": n * n * 8,
+                    "d2h_bytes_per_step": n * n * 8, "steps": e2e_steps,
+                    "path": "scatter owned columns + distributed reduction + band gather to rank 0"},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "tensor", "kernel": "all", "achieved": value / 1e3 / world,
+                         "peak": peak, "unit": "TFLOP/s", "frac": value / 1e3 / world / peak,
+                         "peak_source": "cuBLAS DGEMM 8192^3 per GPU, measured in this run",
+                         "traffic": None, "note": "whole-job GFLOP/s per GPU vs one GPU's DGEMM peak"},
+            "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -380,6 +470,8 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
+    elif world > 1:
+        run_dist(args, rank, world, local_rank)
     else:
         run_ours(args, rank, world, local_rank)
 

@@ -43,6 +43,8 @@ typedef struct br_stats {
 /* ---- context ---------------------------------------------------------- */
 int br_version(void);
 const char* br_last_error(void);
+/* Kernels this library has launched in this process (bench evidence). */
+int64_t br_launch_count(void);
 /* Create a context on `device` with its own main/panel streams (the panel
  * stream has the higher priority: look-ahead factorizations win SMs). */
 int br_create(int device, br_handle_t* out);
@@ -57,7 +59,23 @@ int br_set_timing(br_handle_t h, int enable);
  * Accumulated since br_set_timing(h, 1). */
 int br_get_timing(br_handle_t h, int cls, double* ms, double* flops, int64_t* launches);
 
+/* Kernel-level calls below run on the main stream (which = 0, default) or the
+ * panel stream (which = 1) - the two worker groups of the reference runtime
+ * (runtime.py:142-180). br_stream_join(h, w) makes stream w wait for all work
+ * enqueued so far on the other one. */
+int br_stream_select(br_handle_t h, int which);
+int br_stream_join(br_handle_t h, int waiter);
+
 /* ---- kernel level (ref kernels.py) ------------------------------------ */
+/* matmul (kernels.py:39-83): C = alpha op(A) op(B) + beta C on the FP64
+ * tensor cores (fixed K order per element, deterministic). */
+int br_gemm(br_handle_t h, int transa, int transb, int64_t m, int64_t n, int64_t k, double alpha,
+            const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+            int64_t ldc);
+/* symm_lower with scaling: X1 = alpha sym(A2) W + beta X1, A2 lower-only. */
+int br_symm_lower_ex(br_handle_t h, int64_t j, int64_t b, double alpha, const double* A2,
+                     int64_t lda, const double* W, int64_t ldw, double beta, double* X1,
+                     int64_t ldx);
 /* house_gen (kernels.py:86-110): v (L) and tau_beta = {tau, beta}. */
 int br_house_gen(br_handle_t h, int64_t L, const double* x, double* v, double* tau_beta);
 /* qr_panel (kernels.py:165-208): in-place QR of the j x b panel P; R into

@@ -30,6 +30,7 @@ class BrStats(C.Structure):
 SIGNATURES = {
     "br_version": (C.c_int, []),
     "br_last_error": (C.c_char_p, []),
+    "br_launch_count": (C.c_int64, []),
     "br_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
     "br_destroy": (C.c_int, [C.c_void_p]),
     "br_set_streams": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
@@ -37,6 +38,12 @@ SIGNATURES = {
     "br_set_timing": (C.c_int, [C.c_void_p, C.c_int]),
     "br_get_timing": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                 C.POINTER(C.c_int64)]),
+    "br_stream_select": (C.c_int, [C.c_void_p, C.c_int]),
+    "br_stream_join": (C.c_int, [C.c_void_p, C.c_int]),
+    "br_gemm": (C.c_int, [C.c_void_p, C.c_int, C.c_int, i64, i64, i64, C.c_double, dptr, i64, dptr,
+                          i64, C.c_double, dptr, i64]),
+    "br_symm_lower_ex": (C.c_int, [C.c_void_p, i64, i64, C.c_double, dptr, i64, dptr, i64,
+                                   C.c_double, dptr, i64]),
     "br_house_gen": (C.c_int, [C.c_void_p, i64, dptr, dptr, dptr]),
     "br_qr_panel": (C.c_int, [C.c_void_p, i64, i64, dptr, i64, dptr, i64, dptr, i64, dptr, i64, dptr]),
     "br_lq_panel": (C.c_int, [C.c_void_p, i64, i64, dptr, i64, dptr, i64, dptr, i64, dptr, i64, dptr]),

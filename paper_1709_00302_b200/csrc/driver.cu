@@ -170,6 +170,10 @@ struct br_handle_s {
   Workspace ws;
 };
 
+// Stream (and its split-K scratch) used by kernel-level calls: br_stream_select.
+static cudaStream_t cur_stream(Workspace& ws) { return ws.active ? ws.panel : ws.main; }
+static Scratch& cur_sk(Workspace& ws) { return ws.active ? ws.sk_panel : ws.sk_main; }
+
 #define ARG(cond, i)                                   \
   do {                                                 \
     if (!(cond)) {                                     \
@@ -185,8 +189,9 @@ struct br_handle_s {
 
 static int ensure_scratch(Workspace& ws, int64_t main_doubles, int64_t panel_doubles,
                           int64_t pscr) {
-  BR_CHECK(devbuf_reserve(ws.skbuf_main, main_doubles));
-  BR_CHECK(devbuf_reserve(ws.skbuf_panel, panel_doubles));
+  const int64_t both = std::max(main_doubles, panel_doubles);
+  BR_CHECK(devbuf_reserve(ws.skbuf_main, both));
+  BR_CHECK(devbuf_reserve(ws.skbuf_panel, both));
   BR_CHECK(devbuf_reserve(ws.pscratch, pscr));
   ws.sk_main.p = ws.skbuf_main.p;
   ws.sk_main.cap = ws.skbuf_main.cap;
@@ -199,6 +204,7 @@ static int ensure_scratch(Workspace& ws, int64_t main_doubles, int64_t panel_dou
 extern "C" {
 
 int br_version(void) { return 100; }
+int64_t br_launch_count(void) { return launch_count(); }
 const char* br_last_error(void) { return g_err; }
 
 int br_create(int device, br_handle_t* out) {
@@ -286,7 +292,7 @@ int br_house_gen(br_handle_t h, int64_t L, const double* x, double* v, double* t
   ARG(L >= 1, 2);
   ARG(x && v && tau_beta, 3);
   DEV(h);
-  return house_gen_dev(h->ws.main, L, x, v, tau_beta);
+  return house_gen_dev(cur_stream(h->ws), L, x, v, tau_beta);
 }
 
 static int qr_common(br_handle_t h, MatView P, double* Y, int64_t ldy, double* T, int64_t ldt,
@@ -296,7 +302,7 @@ static int qr_common(br_handle_t h, MatView P, double* Y, int64_t ldy, double* T
   BR_CHECK(ensure_scratch(ws, 4 * std::max<int64_t>(j, 1) * b + (1 << 20), (1 << 20) + 4 * j * b,
                           panel_scratch_doubles(b)));
   MatView Yv(Y, ldy, j, b), Tv(T, ldt, b, b), Wv(W, ldw, j, b);
-  return panel_qr(ws.main, ws.sk_main, ws.pscratch, P, Yv, tau, Tv, W ? &Wv : nullptr);
+  return panel_qr(cur_stream(ws), cur_sk(ws), ws.pscratch, P, Yv, tau, Tv, W ? &Wv : nullptr);
 }
 
 int br_qr_panel(br_handle_t h, int64_t j, int64_t b, double* P, int64_t ldp, double* Y,
@@ -337,7 +343,7 @@ int br_build_w(br_handle_t h, int64_t j, int64_t b, const double* Y, int64_t ldy
   Workspace& ws = h->ws;
   BR_CHECK(ensure_scratch(ws, 4 * std::max<int64_t>(j, 1) * std::max<int64_t>(b, 1) + (1 << 20),
                           1 << 20, panel_scratch_doubles(1)));
-  return gemm(ws.main, ws.sk_main, MatView(W, ldw, j, b), MatView((double*)Y, ldy, j, b),
+  return gemm(cur_stream(ws), cur_sk(ws), MatView(W, ldw, j, b), MatView((double*)Y, ldy, j, b),
               MatView((double*)T, ldt, b, b), 1.0, 0.0);
 }
 
@@ -357,8 +363,8 @@ int br_apply_wy_left(br_handle_t h, int64_t rows, int64_t cols, double* A, int64
                           panel_scratch_doubles(1)));
   BR_CHECK(devbuf_reserve(ws.tmp, b * cols));
   MatView Z(ws.tmp.p, b, b, cols), Av(A, lda, rows, cols);
-  BR_CHECK(gemm(ws.main, ws.sk_main, Z, MatView((double*)W, ldw, rows, b).T(), Av, 1.0, 0.0));
-  return gemm(ws.main, ws.sk_main, Av, MatView((double*)Y, ldy, rows, b), Z, 1.0, 1.0);
+  BR_CHECK(gemm(cur_stream(ws), cur_sk(ws), Z, MatView((double*)W, ldw, rows, b).T(), Av, 1.0, 0.0));
+  return gemm(cur_stream(ws), cur_sk(ws), Av, MatView((double*)Y, ldy, rows, b), Z, 1.0, 1.0);
 }
 
 int br_apply_wy_right(br_handle_t h, int64_t rows, int64_t cols, double* A, int64_t lda,
@@ -377,8 +383,8 @@ int br_apply_wy_right(br_handle_t h, int64_t rows, int64_t cols, double* A, int6
                           panel_scratch_doubles(1)));
   BR_CHECK(devbuf_reserve(ws.tmp, rows * b));
   MatView Z(ws.tmp.p, rows, rows, b), Av(A, lda, rows, cols);
-  BR_CHECK(gemm(ws.main, ws.sk_main, Z, Av, MatView((double*)W, ldw, cols, b), 1.0, 0.0));
-  return gemm(ws.main, ws.sk_main, Av, Z, MatView((double*)Y, ldy, cols, b).T(), 1.0, 1.0);
+  BR_CHECK(gemm(cur_stream(ws), cur_sk(ws), Z, Av, MatView((double*)W, ldw, cols, b), 1.0, 0.0));
+  return gemm(cur_stream(ws), cur_sk(ws), Av, Z, MatView((double*)Y, ldy, cols, b).T(), 1.0, 1.0);
 }
 
 int br_symm_lower(br_handle_t h, int64_t j, int64_t b, const double* A2, int64_t lda,
@@ -393,7 +399,7 @@ int br_symm_lower(br_handle_t h, int64_t j, int64_t b, const double* A2, int64_t
   if (j == 0 || b == 0) return 0;
   Workspace& ws = h->ws;
   BR_CHECK(ensure_scratch(ws, 4 * j * b + (1 << 20), 1 << 20, panel_scratch_doubles(1)));
-  return symm_lower(ws.main, ws.sk_main, MatView(X1, ldx, j, b), MatView((double*)A2, lda, j, j),
+  return symm_lower(cur_stream(ws), cur_sk(ws), MatView(X1, ldx, j, b), MatView((double*)A2, lda, j, j),
                     MatView((double*)W, ldw, j, b));
 }
 
@@ -409,8 +415,68 @@ int br_syr2k_lower(br_handle_t h, int64_t j, int64_t b, double* A2, int64_t lda,
   ARG(0 <= c0 && c0 <= c1 && c1 <= j, 10);
   DEV(h);
   if (j == 0 || b == 0 || c0 == c1) return 0;
-  return syr2k_lower(h->ws.main, MatView(A2, lda, j, j), MatView((double*)X3, ldx, j, b),
+  return syr2k_lower(cur_stream(h->ws), MatView(A2, lda, j, j), MatView((double*)X3, ldx, j, b),
                      MatView((double*)Y, ldy, j, b), c0, c1);
+}
+
+int br_stream_select(br_handle_t h, int which) {
+  ARG(h != nullptr, 1);
+  ARG(which == 0 || which == 1, 2);
+  h->ws.active = which;
+  return 0;
+}
+
+int br_stream_join(br_handle_t h, int waiter) {
+  ARG(h != nullptr, 1);
+  ARG(waiter == 0 || waiter == 1, 2);
+  DEV(h);
+  Workspace& ws = h->ws;
+  cudaStream_t w = waiter ? ws.panel : ws.main, o = waiter ? ws.main : ws.panel;
+  cudaEvent_t ev = ws_event(ws);
+  BR_CUDA(cudaEventRecord(ev, o));
+  BR_CUDA(cudaStreamWaitEvent(w, ev, 0));
+  if (ws.event_next > 4096) ws_events_reset(ws);
+  return 0;
+}
+
+int br_gemm(br_handle_t h, int transa, int transb, int64_t m, int64_t n, int64_t k, double alpha,
+            const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+            int64_t ldc) {
+  ARG(h != nullptr, 1);
+  ARG(m >= 0, 4);
+  ARG(n >= 0, 5);
+  ARG(k >= 0, 6);
+  ARG(A != nullptr || m == 0 || k == 0, 8);
+  ARG(lda >= std::max<int64_t>(1, transa ? k : m), 9);
+  ARG(B != nullptr || n == 0 || k == 0, 10);
+  ARG(ldb >= std::max<int64_t>(1, transb ? n : k), 11);
+  ARG(C != nullptr || m == 0 || n == 0, 13);
+  ARG(ldc >= std::max<int64_t>(1, m), 14);
+  DEV(h);
+  if (m == 0 || n == 0) return 0;
+  Workspace& ws = h->ws;
+  BR_CHECK(ensure_scratch(ws, 4 * std::max(m, n) * std::max<int64_t>(std::min(m, n), 1) + (1 << 20),
+                          1 << 20, panel_scratch_doubles(1)));
+  MatView Av = transa ? MatView((double*)A, lda, k, m).T() : MatView((double*)A, lda, m, k);
+  MatView Bv = transb ? MatView((double*)B, ldb, n, k).T() : MatView((double*)B, ldb, k, n);
+  return gemm(cur_stream(ws), cur_sk(ws), MatView(C, ldc, m, n), Av, Bv, alpha, beta);
+}
+
+int br_symm_lower_ex(br_handle_t h, int64_t j, int64_t b, double alpha, const double* A2,
+                     int64_t lda, const double* W, int64_t ldw, double beta, double* X1,
+                     int64_t ldx) {
+  ARG(h != nullptr, 1);
+  ARG(j >= 0, 2);
+  ARG(b >= 0, 3);
+  ARG(A2 && lda >= std::max<int64_t>(j, 1), 5);
+  ARG(W && ldw >= std::max<int64_t>(j, 1), 7);
+  ARG(X1 && ldx >= std::max<int64_t>(j, 1), 10);
+  DEV(h);
+  if (j == 0 || b == 0) return 0;
+  Workspace& ws = h->ws;
+  BR_CHECK(ensure_scratch(ws, 4 * j * b + (1 << 20), 1 << 20, panel_scratch_doubles(1)));
+  return symm_lower(cur_stream(ws), cur_sk(ws), MatView(X1, ldx, j, b),
+                    MatView((double*)A2, lda, j, j), MatView((double*)W, ldw, j, b), alpha, beta);
 }
 
 int br_sym_two_sided_update(br_handle_t h, int64_t j, int64_t b, double* A2, int64_t lda,
@@ -428,10 +494,10 @@ int br_sym_two_sided_update(br_handle_t h, int64_t j, int64_t b, double* A2, int
   BR_CHECK(devbuf_reserve(ws.tmp, 2 * j * b + b * b));
   MatView X1(ws.tmp.p, j, j, b), X3(ws.tmp.p + j * b, j, j, b), X2(ws.tmp.p + 2 * j * b, b, b, b);
   MatView A2v(A2, lda, j, j), Yv((double*)Y, ldy, j, b), Wv((double*)W, ldw, j, b);
-  BR_CHECK(symm_lower(ws.main, ws.sk_main, X1, A2v, Wv));
-  BR_CHECK(gemm(ws.main, ws.sk_main, X2, X1.T(), Wv, 0.5, 0.0));
-  BR_CHECK(gemm(ws.main, ws.sk_main, X3, Yv, X2, 1.0, 1.0, &X1));
-  return syr2k_lower(ws.main, A2v, X3, Yv, 0, j);
+  BR_CHECK(symm_lower(cur_stream(ws), cur_sk(ws), X1, A2v, Wv));
+  BR_CHECK(gemm(cur_stream(ws), cur_sk(ws), X2, X1.T(), Wv, 0.5, 0.0));
+  BR_CHECK(gemm(cur_stream(ws), cur_sk(ws), X3, Yv, X2, 1.0, 1.0, &X1));
+  return syr2k_lower(cur_stream(ws), A2v, X3, Yv, 0, j);
 }
 
 static double sevp_nominal(int64_t n) { return 4.0 * (double)n * n * n / 3.0; }

@@ -49,6 +49,7 @@ struct Workspace {
   double t_flops[TC_COUNT] = {0, 0, 0, 0};
   int64_t t_launches[TC_COUNT] = {0, 0, 0, 0};
   int64_t launches = 0;
+  int active = 0;  // stream used by kernel-level C-ABI calls: 0 main, 1 panel
 };
 
 // Kernels launched by this library in this process (stats / bench evidence).

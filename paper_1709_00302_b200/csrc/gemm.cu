@@ -165,7 +165,8 @@ int gemm(cudaStream_t st, Scratch& ws, MatView C, MatView A, MatView B, double a
   return run_gemm(A.trans ? A_T : A_N, st, ws, g, B.trans, max_ctas);
 }
 
-int symm_lower(cudaStream_t st, Scratch& ws, MatView X1, MatView A2, MatView W) {
+int symm_lower(cudaStream_t st, Scratch& ws, MatView X1, MatView A2, MatView W, double alpha,
+               double beta) {
   if (A2.trans || X1.trans || W.trans || A2.rows != A2.cols || X1.rows != A2.rows ||
       W.rows != A2.rows || X1.cols != W.cols) {
     set_error("symm_lower: bad views");
@@ -189,8 +190,8 @@ int symm_lower(cudaStream_t st, Scratch& ws, MatView X1, MatView A2, MatView W) 
   g.ldc = X1.ld;
   g.Cin = X1.p;
   g.ldcin = X1.ld;
-  g.alpha = 1.0;
-  g.beta = 0.0;
+  g.alpha = alpha;
+  g.beta = beta;
   g.vecA = al16(A2.p, A2.ld);
   g.vecB = al16(W.p, W.ld);
   return run_gemm(A_SYM, st, ws, g, false, 0);

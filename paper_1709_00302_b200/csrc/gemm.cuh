@@ -58,7 +58,8 @@ struct GemmArgs {
 int gemm(cudaStream_t st, Scratch& ws, MatView C, MatView A, MatView B, double alpha,
          double beta, const MatView* Cin = nullptr, int max_ctas = 0);
 // X1 = sym(A2) * W, A2 lower-stored j x j (non-transposed view).
-int symm_lower(cudaStream_t st, Scratch& ws, MatView X1, MatView A2, MatView W);
+int symm_lower(cudaStream_t st, Scratch& ws, MatView X1, MatView A2, MatView W,
+               double alpha = 1.0, double beta = 0.0);
 // A2[:, c0:c1] += X3*Y^T + Y*X3^T, lower triangle only.
 int syr2k_lower(cudaStream_t st, MatView A2, MatView X3, MatView Y, int64_t c0, int64_t c1,
                 int max_ctas = 0);
