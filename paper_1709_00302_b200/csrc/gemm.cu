@@ -75,14 +75,15 @@ static int run_gemm(int am, cudaStream_t st, Scratch& ws, GemmArgs g, bool btran
   else if (g.M <= 32) cfg = CFG_MS;
   const int bm = kTiles[cfg].bm, bn = kTiles[cfg].bn, cps = kTiles[cfg].ctas_per_sm;
   const int64_t tiles = cdiv(g.M, bm) * cdiv(g.N, bn);
-  const int64_t nkt = cdiv(g.K, 16);
+  const int bk = kTileBK[cfg];
+  const int64_t nkt = cdiv(g.K, bk);
   const int sms = ws.num_sms;
   // Split-K factor from a small cost model: waves of resident CTAs times the
   // k-tiles each CTA runs, plus the fixed-order reduction pass. This keeps
   // the last wave from idling most SMs (wave quantization) on the tall-skinny
   // reductions (W^T E, D W_V, X1^T W, Y^T Y).
   const int64_t slots = (max_ctas > 0) ? std::max(1, max_ctas) : (int64_t)sms * cps;
-  const double kt_time = (double)cps * bm * bn * 16 * 2 / 251e9;  // one k-tile, one CTA
+  const double kt_time = (double)cps * bm * bn * bk * 2 / 251e9;  // one k-tile, one CTA
   int64_t S = 1;
   double best = 1e30;
   const int64_t smax = std::min<int64_t>(64, std::max<int64_t>(1, nkt / 2));
@@ -97,7 +98,7 @@ static int run_gemm(int am, cudaStream_t st, Scratch& ws, GemmArgs g, bool btran
     }
   }
   if (S > 1) {
-    const int64_t kps = cdiv(nkt, S) * 16;
+    const int64_t kps = cdiv(nkt, S) * bk;
     S = cdiv(g.K, kps);
     g.k_per_split = kps;
   } else {

@@ -7,7 +7,7 @@
 
 namespace br {
 
-enum TileCfg { CFG_L = 0, CFG_NS, CFG_MS, CFG_A, CFG_B, CFG_C, CFG_D, CFG_COUNT };
+enum TileCfg { CFG_L = 0, CFG_NS, CFG_MS, CFG_A, CFG_B, CFG_C, CFG_D, CFG_E, CFG_F, CFG_COUNT };
 
 struct TileInfo {
   const char* name;
@@ -24,7 +24,11 @@ constexpr TileInfo kTiles[CFG_COUNT] = {
     {"B", 128, 64, 2},   // 8 warps 4x2, warp 32x32, 3 stages
     {"C", 64, 128, 2},   // 8 warps 2x4, warp 32x32, 3 stages
     {"D", 64, 64, 3},    // 4 warps 2x2, warp 32x32, 4 stages
+    {"E", 64, 128, 2},   // 8 warps 2x4, warp 32x32, BK=32, 2 stages
+    {"F", 128, 64, 2},   // 8 warps 4x2, warp 32x32, BK=32, 2 stages
 };
+// K depth of one pipeline stage per configuration (split-K granularity)
+constexpr int kTileBK[CFG_COUNT] = {16, 16, 16, 16, 16, 16, 16, 32, 32};
 
 int launch_tile_L(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
 int launch_tile_NS(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
@@ -33,6 +37,8 @@ int launch_tile_A(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, 
 int launch_tile_B(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
 int launch_tile_C(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
 int launch_tile_D(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
+int launch_tile_E(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
+int launch_tile_F(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
 
 inline int launch_tile(int cfg, int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g,
                        dim3 grid) {
@@ -43,7 +49,9 @@ inline int launch_tile(int cfg, int am, int bmd, int epi, cudaStream_t st, const
     case CFG_A: return launch_tile_A(am, bmd, epi, st, g, grid);
     case CFG_B: return launch_tile_B(am, bmd, epi, st, g, grid);
     case CFG_C: return launch_tile_C(am, bmd, epi, st, g, grid);
-    default: return launch_tile_D(am, bmd, epi, st, g, grid);
+    case CFG_D: return launch_tile_D(am, bmd, epi, st, g, grid);
+    case CFG_E: return launch_tile_E(am, bmd, epi, st, g, grid);
+    default: return launch_tile_F(am, bmd, epi, st, g, grid);
   }
 }
 

@@ -143,6 +143,14 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
         for (int c = 0; c < NB; c += 2)
           *reinterpret_cast<double2*>(&rowi[c]) = make_double2(p[k][c], p[k][c + 1]);
       }
+    // rows above i keep their final R entries in the registers (captured into
+    // Rrow when they reach column 0); masking x removes them from every sum
+    double xk[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      xk[k] = (gr[k] >= i) ? p[k][0] : 0.0;
+      if (hh && gr[k] < i) Rrow[gr[k]][i] = p[k][0];
+    }
     // ---- per-thread partials, transpose-reduced per warp ----
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) {
@@ -152,7 +160,7 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
         const int c = ch * RC + cc;
         double s = 0.0;
 #pragma unroll
-        for (int k = 0; k < R; ++k) s = fma((c < g0) ? p[k][0] : p[k][NB - 1], p[k][c], s);
+        for (int k = 0; k < R; ++k) s = fma((c < g0) ? xk[k] : p[k][NB - 1], p[k][c], s);
         v[cc] = s;
       }
       warp_transpose_reduce<RC>(v, lane);
@@ -217,8 +225,8 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
         }
         if (lane < NB)  // tau == 0 (zero column): identity reflector, no update
           alw[warp][lane] = (nrm2 != 0.0 && lane >= 1 && lane < nb - i) ? fma(-g, rb, pic) : 0.0;
-        if (warp == 0 && lane == 0) {
-          scal[i][0] = (nrm2 != 0.0) ? (beta - x0) / beta : 0.0;  // tau (ref kernels.py:109)
+        if (warp == 0 && lane == 0) {  // tau = (beta - x0) / beta later, off the critical path
+          scal[i][0] = x0;
           scal[i][1] = beta;
           scal[i][2] = rinv;
         }
@@ -236,18 +244,10 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
       }
 #pragma unroll
       for (int k = 0; k < R; ++k) {
-        const double vk = (gr[k] == i) ? 1.0 : p[k][0] * rinv;
+        const double vk = (gr[k] == i) ? 1.0 : xk[k] * rinv;  // 0 above row i
 #pragma unroll
         for (int c = 0; c < NB - 1; ++c) p[k][c] = fma(-vk, al[c + 1], p[k][c + 1]);
         p[k][NB - 1] = vk;  // Y column i (unit diagonal, zeros above)
-        if (gr[k] == i) {  // row i is final: move its R entries (columns i+1..) out
-#pragma unroll
-          for (int c = 0; c < NB - 1; ++c)
-            if (c < nb - 1 - i) {
-              Rrow[i][i + 1 + c] = p[k][c];
-              p[k][c] = 0.0;
-            }
-        }
       }
     }
     BR_PHASE(6);
@@ -278,6 +278,12 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
       }
     }
   }
+  // ---- tau = (beta - x0) / beta (ref kernels.py:109) ----
+  if (tid < nb) {
+    const double be = scal[tid][1];
+    scal[tid][0] = (be != 0.0) ? (be - scal[tid][0]) / be : 0.0;
+  }
+  __syncthreads();
   // ---- T by the reference recurrence (ref kernels.py:152-162), one row per lane ----
   if (warp == 0 && lane < NB) {
     const int r = lane;
