@@ -43,6 +43,7 @@ struct LeafArgs {
   int64_t ldw;
   int64_t L;
   int nb;
+  int wt;           // W output: 0 -> Y T, 1 -> Y T^T (block reflector Q^T = I + Y T^T Y^T)
   long long* prof;  // optional per-phase cycle counters (BR_LEAF_PROF=1)
 };
 
@@ -99,7 +100,7 @@ static int launch_leaf_t(cudaStream_t st, const LeafArgs& a) {
 }
 
 static int launch_leaf(cudaStream_t st, MatView P, MatView Y, double* tau, double* T, int64_t ldt,
-                       MatView* W) {
+                       MatView* W, int wt = 0) {
   const int64_t L = P.rows;
   const int nb = (int)P.cols;
   if (nb < 1 || nb > LEAF_NB || L > leaf_capacity(nb)) {
@@ -117,6 +118,7 @@ static int launch_leaf(cudaStream_t st, MatView P, MatView Y, double* tau, doubl
   a.ldw = W ? W->ld : 0;
   a.L = L;
   a.nb = nb;
+  a.wt = wt;
   a.prof = nullptr;
   static const bool prof_on = std::getenv("BR_LEAF_PROF") != nullptr;
   if (prof_on) {
@@ -163,29 +165,45 @@ namespace br {
 // recurrence, then T[0:s, s:e] = T[0:s,0:s] * G[0:s, s:e] * T[s:e, s:e].
 __global__ void t_diag_kernel(const double* G, int64_t ldg, const double* tau, int64_t b,
                               double* T, int64_t ldt) {
-  // one warp per 32-column diagonal block
-  const int lane = threadIdx.x & 31, blk = threadIdx.x >> 5;
-  const int64_t s = (int64_t)blk * 32;
-  if (s >= b) return;
+  // one CTA (one warp) per 32-column diagonal block, staged in shared memory;
+  // lane r computes row r of the block (rows are independent in the
+  // recurrence T[r][i] = -tau_i sum_{c=r}^{i-1} T[r][c] G[c][i])
+  __shared__ double Gs[32][33];
+  __shared__ double Tr[32][33];
+  __shared__ double ts[32];
+  const int lane = threadIdx.x;
+  const int64_t s = (int64_t)blockIdx.x * 32;
   const int nb = (int)std::min<int64_t>(32, b - s);
-  for (int i = 0; i < nb; ++i) {
-    const double ti = tau[s + i];
-    if (lane < i) {
-      double acc = 0.0;
-      for (int c = lane; c < i; ++c) acc = fma(T[(s + lane) + (s + c) * ldt], G[(s + c) + (s + i) * ldg], acc);
-      T[(s + lane) + (s + i) * ldt] = -ti * acc;
+  for (int c = 0; c < nb; ++c)
+    if (lane < nb) Gs[lane][c] = G[(s + lane) + (s + c) * ldg];
+  if (lane < nb) ts[lane] = tau[s + lane];
+  __syncwarp();
+  if (lane < nb) {
+    const int r = lane;
+    for (int c = 0; c < 32; ++c) Tr[r][c] = 0.0;
+    Tr[r][r] = -ts[r];
+    for (int i = r + 1; i < nb; ++i) {
+      double s0 = 0.0, s1 = 0.0;
+      int c = r;
+      for (; c + 1 < i; c += 2) {
+        s0 = fma(Tr[r][c], Gs[c][i], s0);
+        s1 = fma(Tr[r][c + 1], Gs[c + 1][i], s1);
+      }
+      if (c < i) s0 = fma(Tr[r][c], Gs[c][i], s0);
+      Tr[r][i] = -ts[i] * (s0 + s1);
     }
-    if (lane == i) T[(s + i) + (s + i) * ldt] = -ti;
-    __syncwarp();
   }
+  __syncwarp();
+  for (int c = 0; c < nb; ++c)
+    if (lane < nb) T[(s + lane) + (s + c) * ldt] = Tr[lane][c];
 }
 
 int t_from_gram(cudaStream_t st, const double* G, int64_t ldg, const double* tau, int64_t b,
                 double* T, int64_t ldt) {
-  // caller zero-fills T
+  // caller zero-fills T (the blocks above the diagonal are filled later)
   const int nblk = (int)cdiv(b, 32);
   count_launch();
-  t_diag_kernel<<<1, 32 * nblk, 0, st>>>(G, ldg, tau, b, T, ldt);
+  t_diag_kernel<<<nblk, 32, 0, st>>>(G, ldg, tau, b, T, ldt);
   BR_CUDA(cudaGetLastError());
   return 0;
 }
@@ -226,6 +244,17 @@ int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView 
     const int64_t w = e - s;
     MatView leafP = P.sub(s, s, j - s, w);
     MatView leafY = Y.sub(s, s, j - s, w);
+    if (e < b && W) {
+      // P[s:, e:b] += (Y_blk T_blk^T)(Y_blk^T P[s:, e:b]); the leaf writes
+      // Y_blk T_blk^T into W's columns (W itself is formed at the end)
+      MatView What = W->sub(s, s, j - s, w);
+      BR_CHECK(launch_leaf(st, leafP, leafY, tau + s, tblk, LEAF_NB, &What, 1));
+      MatView rest = P.sub(s, e, j - s, b - e);
+      MatView Zs = Z.sub(0, 0, w, b - e);
+      BR_CHECK(gemm(st, ws, Zs, leafY.T(), rest, 1.0, 0.0));
+      BR_CHECK(gemm(st, ws, rest, What, Zs, 1.0, 1.0));
+      continue;
+    }
     BR_CHECK(launch_leaf(st, leafP, leafY, tau + s, tblk, LEAF_NB, nullptr));
     if (e < b) {
       // P[s:, e:b] += Y_blk (T_blk^T (Y_blk^T P[s:, e:b]))

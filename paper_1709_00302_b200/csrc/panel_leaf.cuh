@@ -328,7 +328,9 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
       for (int k0 = 0; k0 < NB; k0 += 4) {
         const double av = Ys[(k0 + tq) * ROWS + r0 + gq];  // A = Y (8 x 4)
 #pragma unroll
-        for (int n = 0; n < NB / 8; ++n) dmma884(acc[n][0], acc[n][1], av, Ts[k0 + tq][n * 8 + gq]);
+        for (int n = 0; n < NB / 8; ++n)  // B = T, or T^T for the block-reflector form Y T^T
+          dmma884(acc[n][0], acc[n][1], av,
+                  a.wt ? Ts[n * 8 + gq][k0 + tq] : Ts[k0 + tq][n * 8 + gq]);
       }
       const int64_t row = base + r0 + gq;
       if (row < a.L) {
