@@ -41,21 +41,26 @@ static int env_cfg(const char* var, int dflt) {
   }
   return dflt;
 }
-static int big_cfg(int am) {
-  static int gen = -1, sym = -1;
+static int big_cfg(int am, bool rank_update) {
+  static int gen = -1, sym = -1, rku = -1;
   if (gen < 0) {
     gen = env_cfg("BR_GEMM_BIG", CFG_C);
     sym = env_cfg("BR_GEMM_SYMM", CFG_A);
+    rku = env_cfg("BR_GEMM_RANKB", CFG_D);
   }
-  return am == A_SYM ? sym : gen;
+  if (am == A_SYM) return sym;
+  return rank_update ? rku : gen;
 }
-static int lower_cfg() {
-  static int cfg = -1;
-  if (cfg < 0) {
-    cfg = env_cfg("BR_GEMM_LOWER", CFG_L);
-    if (kTiles[cfg].bm != kTiles[cfg].bn) cfg = CFG_L;
+static int lower_cfg(int64_t j) {
+  // 64x64 tiles (3 CTAs/SM) for large trailing blocks, 128x128 for small ones
+  static int cfg = -2;
+  if (cfg == -2) {
+    cfg = -1;
+    if (std::getenv("BR_GEMM_LOWER")) cfg = env_cfg("BR_GEMM_LOWER", CFG_L);
+    if (cfg >= 0 && kTiles[cfg].bm != kTiles[cfg].bn) cfg = CFG_L;
   }
-  return cfg;
+  if (cfg >= 0) return cfg;
+  return j >= 4096 ? CFG_D : CFG_L;
 }
 
 // Dispatch a general/symm GEMM: chooses tile config and split-K.
@@ -70,7 +75,9 @@ static int run_gemm(int am, cudaStream_t st, Scratch& ws, GemmArgs g, bool btran
     BR_CUDA(cudaGetLastError());
     return 0;
   }
-  int cfg = big_cfg(am);
+  // rank-b updates: short K (the band width) accumulated onto a large C
+  const bool rank_update = g.beta != 0.0 && g.K <= 512 && g.M * g.N >= (int64_t)1 << 20;
+  int cfg = big_cfg(am, rank_update);
   if (g.N <= 32) cfg = CFG_NS;
   else if (g.M <= 32) cfg = CFG_MS;
   const int bm = kTiles[cfg].bm, bn = kTiles[cfg].bn, cps = kTiles[cfg].ctas_per_sm;
@@ -235,7 +242,7 @@ int syr2k_lower(cudaStream_t st, MatView A2, MatView X3, MatView Y, int64_t c0, 
   g.vecA = al16(X3.p, X3.ld) && al16(Y.p, Y.ld) && (c0 % 2 == 0);
   g.vecB = g.vecA;
   (void)max_ctas;
-  const int cfg = lower_cfg();
+  const int cfg = lower_cfg(j);
   dim3 grid((unsigned)cdiv(j - c0, kTiles[cfg].bm), (unsigned)cdiv(c1 - c0, kTiles[cfg].bn), 1);
   return launch_tile(cfg, A_N, B_T, EPI_LOWER, st, g, grid);
 }

@@ -107,8 +107,9 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB) dgemm_kernel(const GemmArgs
         for (int h = 0; h < 2; ++h) {
           const int64_t c = n0 + wn + j * 8 + 2 * tq + h;
           const bool ok = r < g.M && c < nmax && (EPI != EPI_LOWER || r >= c);
-          if (ok) acc[i][j][h] = (EPI == EPI_LOWER) ? g.Cin[r + c * g.ldcin]
-                                                    : g.beta * g.Cin[r + c * g.ldcin];
+          if (ok) acc[i][j][h] = (EPI == EPI_LOWER || g.beta == 1.0)
+                                     ? g.Cin[r + c * g.ldcin]
+                                     : g.beta * g.Cin[r + c * g.ldcin];
         }
     }
   }
