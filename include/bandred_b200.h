@@ -130,6 +130,21 @@ int br_reduce_tri_band_host(br_handle_t h, int64_t m, int64_t n, int64_t w, int6
                             int lookahead, const double* A, int64_t lda, double* band,
                             int64_t ldb, br_stats* stats);
 
+/* Equal-bandwidth band form of the SVD (replaces the band branch of
+ * reduce_band_svd, ref pkg/src/bandred/svd.py:515-589, task bodies
+ * svd.py:250-391). Column-major device A (m x n, m >= n, lda >= m) is
+ * reduced in place to band form: A[i,j] = 0 exactly for |i-j| > w; m <= w+1
+ * returns A unchanged. simultaneous 0 = reference order (left then right
+ * update of the trailing block, SvdVariant.REFERENCE / V1), 1 = fused
+ * two-sided trailing update (SvdVariant.SIMULTANEOUS / V2). lookahead 1 =
+ * static look-ahead (V1 / V2 schedules, svd.py:394-492): bitwise equal to
+ * lookahead 0 with the same `simultaneous`. Needs 1 <= b <= w. */
+int br_reduce_band(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b, int simultaneous,
+                   int lookahead, double* A, int64_t lda, br_stats* stats);
+int br_reduce_band_host(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b,
+                        int simultaneous, int lookahead, const double* A, int64_t lda,
+                        double* band, int64_t ldb, br_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

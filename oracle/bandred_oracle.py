@@ -30,6 +30,8 @@ __all__ = [
     "tri_schedule",
     "reduce_sym_band",
     "reduce_tri_band",
+    "reduce_band_svd",
+    "band_schedule",
     "finalize_sym",
     "mask_tri_band",
     "band_check",
@@ -330,6 +332,62 @@ def reduce_tri_band(A, w, b, inner_b=16, max_iters=None):
             apply_wy_right(A[k + bq : m, k + w : n], Yv, Wv)
         it += 1
     return mask_tri_band(A, w), 0, w, it
+
+
+def band_schedule(m, n, w, b):
+    """(k, bp, jr, bq) of the equal-bandwidth band form (svd.py:265-278)."""
+    out, k = [], 0
+    while m - k - w >= 2 and k < n:
+        bp = min(b, m - k - w, n - k)
+        jr = n - k - w
+        bq = min(bp, jr) if jr >= 1 else 0
+        out.append((k, bp, jr, bq))
+        k += bp
+    return out
+
+
+def reduce_band_svd(A, w, b, simultaneous=False, inner_b=16):
+    """Dense general -> band with lower = upper bandwidth w (svd.py:515-589).
+
+    Reference order (svd.py:359-373): QR(B0), left(B1), left(D), LQ(C0),
+    right(C1), right(D). Simultaneous (svd.py:376-391, 317-356): the two D
+    applications fused, Z_L = D^T W_U, Z_R = D W_V, X = Z_R + Y_U (Z_L^T W_V),
+    D += X Y_V^T + Y_U Z_L^T. m < n reduces A^T; m <= w + 1 returns the copy
+    unchanged. Returns (band, lower_bw, upper_bw, iterations).
+    """
+    A = np.array(A, dtype=np.float64, order="F")
+    m, n = A.shape
+    if m < n:
+        band, lo, up, it = reduce_band_svd(np.asfortranarray(A.T), w, b, simultaneous, inner_b)
+        return np.asfortranarray(band.T), up, lo, it
+    sched = band_schedule(m, n, w, b)
+    if not sched:
+        return A, w, w, 0
+    for k, bp, jr, bq in sched:
+        Yu, Tu, Wu, _, _ = qr_panel(A[k + w : m, k : k + bp], inner_b)
+        b1end = min(k + w, n)
+        if k + bp < b1end:
+            apply_wy_left(A[k + w : m, k + bp : b1end], Yu, Wu)
+        if jr < 1:
+            continue
+        D = A[k + w : m, k + w : n]
+        if not simultaneous:
+            apply_wy_left(D, Yu, Wu)
+        Yv, Tv, Wv, _, _ = lq_panel(A[k : k + bq, k + w : n], inner_b)
+        if k + bq < k + w:
+            apply_wy_right(A[k + bq : k + w, k + w : n], Yv, Wv)
+        if not simultaneous:
+            apply_wy_right(D, Yv, Wv)
+        else:
+            ZL = D.T @ Wu
+            ZR = D @ Wv
+            X = ZR + Yu @ (ZL.T @ Wv)
+            D += X @ Yv.T
+            D += Yu @ ZL.T
+    i = np.arange(m)[:, None]
+    jj = np.arange(n)[None, :]
+    A[np.abs(i - jj) > w] = 0.0
+    return A, w, w, len(sched)
 
 
 def band_check(B, lower_bw, upper_bw):

@@ -61,6 +61,10 @@ SIGNATURES = {
                                           dptr, i64, C.POINTER(BrStats)]),
     "br_reduce_tri_band_host": (C.c_int, [C.c_void_p, i64, i64, i64, i64, C.c_int, dptr, i64, dptr,
                                           i64, C.POINTER(BrStats)]),
+    "br_reduce_band": (C.c_int, [C.c_void_p, i64, i64, i64, i64, C.c_int, C.c_int, dptr, i64,
+                                 C.POINTER(BrStats)]),
+    "br_reduce_band_host": (C.c_int, [C.c_void_p, i64, i64, i64, i64, C.c_int, C.c_int, dptr, i64,
+                                      dptr, i64, C.POINTER(BrStats)]),
 }
 
 _lib = None

@@ -587,6 +587,48 @@ int br_reduce_tri_band(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b
   return 0;
 }
 
+int br_reduce_band(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b, int simultaneous,
+                   int lookahead, double* A, int64_t lda, br_stats* stats) {
+  ARG(h != nullptr, 1);
+  ARG(m >= 1 && m >= n, 2);
+  ARG(n >= 1, 3);
+  ARG(w >= 1, 4);
+  ARG(b >= 1 && b <= w, 5);
+  ARG(simultaneous == 0 || simultaneous == 1, 6);
+  ARG(lookahead == 0 || lookahead == 1, 7);
+  ARG(A != nullptr && lda >= m, 8);
+  DEV(h);
+  Workspace& ws = h->ws;
+  cudaEvent_t e0, e1;
+  BR_CUDA(cudaEventCreate(&e0));
+  BR_CUDA(cudaEventCreate(&e1));
+  const int64_t l0 = launch_count();
+  BR_CUDA(cudaEventRecord(e0, ws.main));
+  int64_t iters = 0;
+  int rc = band_reduce(ws, m, n, w, b, simultaneous, lookahead, A, lda, &iters);
+  if (rc) {
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return rc;
+  }
+  BR_CUDA(cudaEventRecord(e1, ws.main));
+  BR_CUDA(cudaEventSynchronize(e1));
+  BR_CUDA(cudaStreamSynchronize(ws.panel));
+  BR_CUDA(cudaGetLastError());
+  float ms = 0;
+  BR_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (ws.timing) BR_CHECK(ws_collect_timing(ws));
+  if (stats) {
+    stats->iterations = iters;
+    stats->device_ms = ms;
+    stats->nominal_flops = svd_nominal(m, n);
+    stats->launches = launch_count() - l0;
+  }
+  return 0;
+}
+
 static int host_stage_in(Workspace& ws, int64_t m, int64_t n, const double* A, int64_t lda,
                          DevBuf& dev, int64_t& ldd) {
   ldd = (m + 31) / 32 * 32;
@@ -639,6 +681,26 @@ int br_reduce_tri_band_host(br_handle_t h, int64_t m, int64_t n, int64_t w, int6
   int64_t ldd = 0;
   BR_CHECK(host_stage_in(ws, m, n, A, lda, dA, ldd));
   BR_CHECK(br_reduce_tri_band(h, m, n, w, b, lookahead, dA.p, ldd, stats));
+  BR_CUDA(cudaMemcpy2DAsync(band, ldb * sizeof(double), dA.p, ldd * sizeof(double),
+                            m * sizeof(double), n, cudaMemcpyDeviceToHost, ws.main));
+  BR_CUDA(cudaStreamSynchronize(ws.main));
+  return 0;
+}
+
+int br_reduce_band_host(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b,
+                        int simultaneous, int lookahead, const double* A, int64_t lda,
+                        double* band, int64_t ldb, br_stats* stats) {
+  ARG(h != nullptr, 1);
+  ARG(m >= 1 && m >= n, 2);
+  ARG(n >= 1, 3);
+  ARG(A != nullptr && lda >= m, 8);
+  ARG(band != nullptr && ldb >= m, 10);
+  DEV(h);
+  Workspace& ws = h->ws;
+  DevBuf& dA = ws.stageA;
+  int64_t ldd = 0;
+  BR_CHECK(host_stage_in(ws, m, n, A, lda, dA, ldd));
+  BR_CHECK(br_reduce_band(h, m, n, w, b, simultaneous, lookahead, dA.p, ldd, stats));
   BR_CUDA(cudaMemcpy2DAsync(band, ldb * sizeof(double), dA.p, ldd * sizeof(double),
                             m * sizeof(double), n, cudaMemcpyDeviceToHost, ws.main));
   BR_CUDA(cudaStreamSynchronize(ws.main));

@@ -96,5 +96,7 @@ int sevp_reduce(Workspace& ws, int64_t n, int64_t w, int64_t b, int lookahead, d
                 int64_t lda, double* Q, int64_t ldq, int64_t* iterations);
 int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lookahead,
                double* A, int64_t lda, int64_t* iterations);
+int band_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int fused,
+                int lookahead, double* A, int64_t lda, int64_t* iterations);
 
 }  // namespace br

@@ -63,33 +63,27 @@ static int lower_cfg(int64_t j) {
   return j >= 4096 ? CFG_D : CFG_L;
 }
 
-// Dispatch a general/symm GEMM: chooses tile config and split-K.
-static int run_gemm(int am, cudaStream_t st, Scratch& ws, GemmArgs g, bool btrans, int max_ctas) {
-  if (g.M <= 0 || g.N <= 0) return 0;
-  if (g.K <= 0) {  // C = beta*Cin
-    const int64_t total = g.M * g.N;
-    int blocks = (int)std::min<int64_t>(cdiv(total, 256), 4096);
-    count_launch();
-    splitk_reduce_kernel<<<blocks, 256, 0, st>>>(g.M, g.N, 0, nullptr, g.alpha, g.beta, g.Cin,
-                                                 g.ldcin, g.C, g.ldc);
-    BR_CUDA(cudaGetLastError());
-    return 0;
-  }
+// Tile configuration of a general/symm GEMM of shape (M, N, K).
+static int pick_cfg(int am, const GemmArgs& g) {
   // rank-b updates: short K (the band width) accumulated onto a large C
   const bool rank_update = g.beta != 0.0 && g.K <= 512 && g.M * g.N >= (int64_t)1 << 20;
   int cfg = big_cfg(am, rank_update);
   if (g.N <= 32) cfg = CFG_NS;
   else if (g.M <= 32) cfg = CFG_MS;
+  return cfg;
+}
+
+// Split-K chunk (k_per_split; == K means no split) from a small cost model:
+// waves of resident CTAs times the k-tiles each CTA runs, plus the
+// fixed-order reduction pass. This keeps the last wave from idling most SMs
+// (wave quantization) on the tall-skinny reductions (W^T E, D W_V, X1^T W,
+// Y^T Y).
+static int64_t pick_kps(int cfg, const Scratch& ws, const GemmArgs& g, int max_ctas) {
   const int bm = kTiles[cfg].bm, bn = kTiles[cfg].bn, cps = kTiles[cfg].ctas_per_sm;
   const int64_t tiles = cdiv(g.M, bm) * cdiv(g.N, bn);
   const int bk = kTileBK[cfg];
   const int64_t nkt = cdiv(g.K, bk);
-  const int sms = ws.num_sms;
-  // Split-K factor from a small cost model: waves of resident CTAs times the
-  // k-tiles each CTA runs, plus the fixed-order reduction pass. This keeps
-  // the last wave from idling most SMs (wave quantization) on the tall-skinny
-  // reductions (W^T E, D W_V, X1^T W, Y^T Y).
-  const int64_t slots = (max_ctas > 0) ? std::max(1, max_ctas) : (int64_t)sms * cps;
+  const int64_t slots = (max_ctas > 0) ? std::max(1, max_ctas) : (int64_t)ws.num_sms * cps;
   const double kt_time = (double)cps * bm * bn * bk * 2 / 251e9;  // one k-tile, one CTA
   int64_t S = 1;
   double best = 1e30;
@@ -104,13 +98,36 @@ static int run_gemm(int am, cudaStream_t st, Scratch& ws, GemmArgs g, bool btran
       S = s;
     }
   }
-  if (S > 1) {
-    const int64_t kps = cdiv(nkt, S) * bk;
-    S = cdiv(g.K, kps);
-    g.k_per_split = kps;
-  } else {
-    g.k_per_split = g.K;
+  return S > 1 ? cdiv(nkt, S) * bk : g.K;
+}
+
+// Dispatch a general/symm GEMM: chooses tile config and split-K. A caller
+// that updates one logical product in pieces passes the k_per_split planned
+// for the whole product (gemm_plan_kps), so every element is summed in the
+// same order whatever the pieces are (bitwise split invariance).
+static int run_gemm(int am, cudaStream_t st, Scratch& ws, GemmArgs g, bool btrans, int max_ctas,
+                    int64_t fixed_kps) {
+  if (g.M <= 0 || g.N <= 0) return 0;
+  if (g.K <= 0) {  // C = beta*Cin
+    const int64_t total = g.M * g.N;
+    int blocks = (int)std::min<int64_t>(cdiv(total, 256), 4096);
+    count_launch();
+    splitk_reduce_kernel<<<blocks, 256, 0, st>>>(g.M, g.N, 0, nullptr, g.alpha, g.beta, g.Cin,
+                                                 g.ldcin, g.C, g.ldc);
+    BR_CUDA(cudaGetLastError());
+    return 0;
   }
+  const int cfg = pick_cfg(am, g);
+  const int bm = kTiles[cfg].bm, bn = kTiles[cfg].bn;
+  const int sms = ws.num_sms;
+  int64_t kps = fixed_kps > 0 ? std::min(fixed_kps, g.K) : pick_kps(cfg, ws, g, max_ctas);
+  int64_t S = cdiv(g.K, kps);
+  if (S > 1 && S * g.M * g.N > ws.cap) {
+    set_error("gemm: split-K scratch too small (%lld x %lld x %lld)", (long long)S,
+              (long long)g.M, (long long)g.N);
+    return -1;
+  }
+  g.k_per_split = S > 1 ? kps : g.K;
   dim3 grid((unsigned)cdiv(g.M, bm), (unsigned)cdiv(g.N, bn), (unsigned)S);
   const int bmd = btrans ? B_T : B_N;
   if (S == 1) {
@@ -128,10 +145,11 @@ static int run_gemm(int am, cudaStream_t st, Scratch& ws, GemmArgs g, bool btran
   return 0;
 }
 
-int gemm(cudaStream_t st, Scratch& ws, MatView C, MatView A, MatView B, double alpha,
-         double beta, const MatView* Cin_, int max_ctas) {
+// Normalizes orientation (C^T = op(B)^T op(A)^T) and fills GemmArgs.
+static int make_args(MatView C, MatView A, MatView B, double alpha, double beta,
+                     const MatView* Cin_, GemmArgs& g, int& am, bool& btrans) {
   MatView Cin = Cin_ ? *Cin_ : C;
-  if (C.trans) {  // C^T = op(B)^T op(A)^T
+  if (C.trans) {
     MatView t = A.T();
     A = B.T();
     B = t;
@@ -148,7 +166,7 @@ int gemm(cudaStream_t st, Scratch& ws, MatView C, MatView A, MatView B, double a
               (long long)B.cols);
     return -1;
   }
-  GemmArgs g{};
+  g = GemmArgs{};
   g.M = C.rows;
   g.N = C.cols;
   g.K = A.cols;
@@ -170,7 +188,27 @@ int gemm(cudaStream_t st, Scratch& ws, MatView C, MatView A, MatView B, double a
   g.beta = beta;
   g.vecA = al16(A.p, A.ld);
   g.vecB = al16(B.p, B.ld);
-  return run_gemm(A.trans ? A_T : A_N, st, ws, g, B.trans, max_ctas);
+  am = A.trans ? A_T : A_N;
+  btrans = B.trans;
+  return 0;
+}
+
+int gemm(cudaStream_t st, Scratch& ws, MatView C, MatView A, MatView B, double alpha,
+         double beta, const MatView* Cin, int max_ctas, int64_t kps) {
+  GemmArgs g;
+  int am = 0;
+  bool bt = false;
+  BR_CHECK(make_args(C, A, B, alpha, beta, Cin, g, am, bt));
+  return run_gemm(am, st, ws, g, bt, max_ctas, kps);
+}
+
+int64_t gemm_plan_kps(const Scratch& ws, MatView C, MatView A, MatView B, double beta) {
+  GemmArgs g;
+  int am = 0;
+  bool bt = false;
+  if (make_args(C, A, B, 1.0, beta, nullptr, g, am, bt) || g.M <= 0 || g.N <= 0 || g.K <= 0)
+    return 0;
+  return pick_kps(pick_cfg(am, g), ws, g, 0);
 }
 
 int symm_lower(cudaStream_t st, Scratch& ws, MatView X1, MatView A2, MatView W, double alpha,
@@ -202,7 +240,7 @@ int symm_lower(cudaStream_t st, Scratch& ws, MatView X1, MatView A2, MatView W, 
   g.beta = beta;
   g.vecA = al16(A2.p, A2.ld);
   g.vecB = al16(W.p, W.ld);
-  return run_gemm(A_SYM, st, ws, g, false, 0);
+  return run_gemm(A_SYM, st, ws, g, false, 0, 0);
 }
 
 int syr2k_lower(cudaStream_t st, MatView A2, MatView X3, MatView Y, int64_t c0, int64_t c1,

@@ -55,8 +55,13 @@ struct GemmArgs {
 // Host-side launch helpers (gemm.cu). All return 0 or a positive CUDA error.
 // C = alpha*op(A)*op(B) + beta*Cin (Cin defaults to C). Views carry the
 // transposition; a transposed C is handled by transposing the product.
+// kps > 0 pins the split-K chunk (see gemm_plan_kps).
 int gemm(cudaStream_t st, Scratch& ws, MatView C, MatView A, MatView B, double alpha,
-         double beta, const MatView* Cin = nullptr, int max_ctas = 0);
+         double beta, const MatView* Cin = nullptr, int max_ctas = 0, int64_t kps = 0);
+// The split-K chunk gemm() would choose for this whole product. Updating the
+// product in row/column pieces with this kps sums every element in the same
+// order as the whole call, so the result is bitwise independent of the pieces.
+int64_t gemm_plan_kps(const Scratch& ws, MatView C, MatView A, MatView B, double beta);
 // X1 = sym(A2) * W, A2 lower-stored j x j (non-transposed view).
 int symm_lower(cudaStream_t st, Scratch& ws, MatView X1, MatView A2, MatView W,
                double alpha = 1.0, double beta = 0.0);

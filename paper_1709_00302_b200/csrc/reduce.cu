@@ -100,13 +100,18 @@ int sevp_reduce(Workspace& ws, int64_t n, int64_t w, int64_t b, int lookahead, d
     const bool la = lookahead && has_next;
 
     // mid block A[k+w:n, k+bp:k+w] := Q^T mid (ref sevp.py:147-153)
+    // split-K chunks of the whole mid-block products: pieces sum in the same order
+    const int64_t kps_z = gemm_plan_kps(ws.sk_main, MatView(Zm, b, bp, w - bp), W.T(),
+                                        MatView(Aat(k + w, k + bp), lda, j, w - bp), 0.0);
+    const int64_t kps_u = gemm_plan_kps(ws.sk_main, MatView(Aat(k + w, k + bp), lda, j, w - bp), Y,
+                                        MatView(Zm, b, bp, w - bp), 1.0);
     auto mid = [&](int64_t c0, int64_t c1) -> int {
       if (c0 >= c1) return 0;
       MatView M(Aat(k + w, c0), lda, j, c1 - c0);
-      MatView Z(Zm, b, bp, c1 - c0);
+      MatView Z(Zm + (c0 - k - bp) * b, b, bp, c1 - c0);
       TimeScope ts(ws, ws.main, TC_GEMM, 2 * gemm_flops(bp, c1 - c0, j));
-      BR_CHECK(gemm(ws.main, ws.sk_main, Z, W.T(), M, 1.0, 0.0));
-      return gemm(ws.main, ws.sk_main, M, Y, Z, 1.0, 1.0);
+      BR_CHECK(gemm(ws.main, ws.sk_main, Z, W.T(), M, 1.0, 0.0, nullptr, 0, kps_z));
+      return gemm(ws.main, ws.sk_main, M, Y, Z, 1.0, 1.0, nullptr, 0, kps_u);
     };
     // X1 = sym(A2) W; X2 = 1/2 X1^T W; X3 = X1 + Y X2 (ref sevp.py:156-176)
     auto xprods = [&]() -> int {
@@ -314,16 +319,17 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
           }
           if (la && !next_issued && splitc > 0) {
             const int64_t sc = std::min(splitc, jr);
+            const int64_t kps = gemm_plan_kps(ws.sk_main, D, Zr, Yvv.T(), 1.0);
             {
               TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, sc, bq));
               BR_CHECK(gemm(ws.main, ws.sk_main, D.sub(0, 0, i - bq, sc), Zr,
-                            Yvv.sub(0, 0, sc, bq).T(), 1.0, 1.0));
+                            Yvv.sub(0, 0, sc, bq).T(), 1.0, 1.0, nullptr, 0, kps));
             }
             BR_CHECK(next_qr_on_panel());
             if (sc < jr) {
               TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, jr - sc, bq));
               BR_CHECK(gemm(ws.main, ws.sk_main, D.sub(0, sc, i - bq, jr - sc), Zr,
-                            Yvv.sub(sc, 0, jr - sc, bq).T(), 1.0, 1.0));
+                            Yvv.sub(sc, 0, jr - sc, bq).T(), 1.0, 1.0, nullptr, 0, kps));
             }
           } else {
             TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, jr, bq));
@@ -343,6 +349,239 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
   if (ev_qr) BR_CHECK(join(ev_qr));
   ws_events_reset(ws);
   return mask_tri(ws.main, A, lda, m, n, 0, w);
+}
+
+// ---------------------------------------------------------------------------
+// Equal-bandwidth band form of the SVD (ref svd.py:250-589), m >= n
+// ---------------------------------------------------------------------------
+// Iteration k (bp = min(b, m-k-w, n-k), jr = n-k-w, bq = min(bp, jr)):
+//   QR of A[k+w:m, k:k+bp]      -> Q_U = I + W_U Y_U^T (ref svd.py:275-283)
+//   LQ of A[k:k+bq, k+w:n]      -> Q_V = I + W_V Y_V^T (ref svd.py:295-306)
+//   left:  ML = A[k+w:m, k+bp:n] = [B1 | D] += Y_U (W_U^T ML)
+//   right: MR = A[k+bq:m, k+w:n] = [C1 ; D] += (MR W_V) Y_V^T
+// The LQ rows lie above the rows the left update touches, so both panels of
+// an iteration are factored together. fused == 0 applies left then right
+// (Reference / V1 order, ref svd.py:359-376); fused == 1 updates D once from
+// its old value (Simultaneous / V2, ref svd.py:377-391):
+//   Z_L = W_U^T D, Z_R = D W_V, X = Z_R + Y_U (Z_L W_V),
+//   D += X Y_V^T, then D += Y_U Z_L.
+// Look-ahead (ref svd.py:394-492): the parts of this iteration's update that
+// the next QR columns / LQ rows read are issued first, both next panels are
+// factored on the panel stream, and main finishes the rest. Every piece uses
+// the split-K chunk planned for its whole product, so depth 1 is bitwise
+// equal to depth 0.
+int band_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int fused,
+                int lookahead, double* A, int64_t lda, int64_t* iterations) {
+  struct It {
+    int64_t k, bp, jr, bq;
+  };
+  std::vector<It> its;
+  for (int64_t k = 0; m - k - w >= 2 && k < n;) {
+    const int64_t bp = std::min({b, m - k - w, n - k});
+    const int64_t jr = n - k - w;
+    its.push_back({k, bp, jr, jr >= 1 ? std::min(bp, jr) : 0});
+    k += bp;
+  }
+  *iterations = (int64_t)its.size();
+  if (its.empty()) return 0;  // m <= w + 1: returned unchanged (ref svd.py:561-564)
+
+  const int64_t nYu = m * b, nYv = n * b, nT = b * b;
+  const int64_t total = 4 * nYu + 4 * nYv + 4 * nT + 4 * b + b * n + 2 * m * b + nT;
+  BR_CHECK(devbuf_reserve(ws.factors, total));
+  BR_CHECK(devbuf_reserve(ws.skbuf_main, 4 * std::max(m, n) * b + (1 << 20)));
+  BR_CHECK(devbuf_reserve(ws.skbuf_panel, 4 * std::max(m, n) * b + (1 << 20)));
+  BR_CHECK(devbuf_reserve(ws.pscratch, panel_scratch_doubles(b)));
+  ws.sk_main = Scratch{ws.skbuf_main.p, ws.skbuf_main.cap, ws.num_sms};
+  ws.sk_panel = Scratch{ws.skbuf_panel.p, ws.skbuf_panel.cap, ws.num_sms};
+  double* f = ws.factors.p;
+  double *Yu[2], *Wu[2], *Tu[2], *tauu[2], *Yv[2], *Wv[2], *Tv[2], *tauv[2];
+  for (int p = 0; p < 2; ++p) {
+    Yu[p] = f; f += nYu;
+    Wu[p] = f; f += nYu;
+    Yv[p] = f; f += nYv;
+    Wv[p] = f; f += nYv;
+    Tu[p] = f; f += nT;
+    Tv[p] = f; f += nT;
+    tauu[p] = f; f += b;
+    tauv[p] = f; f += b;
+  }
+  double* ZLb = f; f += b * n;  // W_U^T ML  (bp x (n-k-bp), ld b)
+  double* ZRb = f; f += m * b;  // MR W_V    ((m-k-bq) x bq, ld m)
+  double* Xb = f; f += m * b;   // X         (i x bq, ld m)
+  double* Tmb = f; f += nT;     // Z_L W_V   (bp x bq, ld b)
+
+  auto Aat = [&](int64_t r, int64_t c) { return A + r + c * lda; };
+  auto qr = [&](cudaStream_t st, Scratch& sk, const It& t, int par) -> int {
+    const int64_t i = m - t.k - w;
+    MatView P(Aat(t.k + w, t.k), lda, i, t.bp);
+    MatView Y(Yu[par], m, i, t.bp), T(Tu[par], b, t.bp, t.bp), W(Wu[par], m, i, t.bp);
+    TimeScope ts(ws, st, TC_PANEL, panel_flops(i, t.bp));
+    return panel_qr(st, sk, ws.pscratch, P, Y, tauu[par], T, &W);
+  };
+  auto lq = [&](cudaStream_t st, Scratch& sk, const It& t, int par) -> int {
+    MatView P(Aat(t.k, t.k + w), lda, t.jr, t.bq, true);  // transposed view of the bq x jr rows
+    MatView Y(Yv[par], n, t.jr, t.bq), T(Tv[par], b, t.bq, t.bq), W(Wv[par], n, t.jr, t.bq);
+    TimeScope ts(ws, st, TC_PANEL, panel_flops(t.jr, t.bq));
+    return panel_qr(st, sk, ws.pscratch, P, Y, tauv[par], T, &W);
+  };
+  auto panels = [&](cudaStream_t st, Scratch& sk, const It& t, int par) -> int {
+    BR_CHECK(qr(st, sk, t, par));
+    return t.jr >= 1 ? lq(st, sk, t, par) : 0;
+  };
+
+  cudaEvent_t ev_panels = nullptr;
+  BR_CHECK(panels(ws.main, ws.sk_main, its[0], 0));
+  for (size_t idx = 0; idx < its.size(); ++idx) {
+    const It t = its[idx];
+    const int par = (int)(idx & 1);
+    if (ev_panels) {
+      BR_CUDA(cudaStreamWaitEvent(ws.main, ev_panels, 0));
+      ev_panels = nullptr;
+    }
+    const bool has_next = idx + 1 < its.size();
+    const It tn = has_next ? its[idx + 1] : It{0, 0, 0, 0};
+    const bool la = lookahead && has_next;
+    cudaStream_t st = ws.main;
+    Scratch& sk = ws.sk_main;
+    const int64_t i = m - t.k - w;           // rows of D (and of ML)
+    const int64_t ncL = n - t.k - t.bp;      // columns of ML = [B1 | D]
+    const int64_t b1w = std::min(w - t.bp, ncL);  // columns of B1
+    const int64_t jr = std::max<int64_t>(t.jr, 0), bq = t.bq;
+    const int64_t c1r = w - bq;              // rows of C1
+    const int64_t nrR = c1r + i;             // rows of MR = [C1 ; D]
+
+    MatView ML(Aat(t.k + w, t.k + t.bp), lda, i, ncL);
+    MatView MR(Aat(t.k + bq, t.k + w), lda, nrR, jr);
+    MatView Yuv(Yu[par], m, i, t.bp), Wuv(Wu[par], m, i, t.bp);
+    MatView Yvv(Yv[par], n, jr, bq), Wvv(Wv[par], n, jr, bq);
+    MatView ZL(ZLb, b, t.bp, ncL), ZR(ZRb, m, nrR, bq), X(Xb, m, i, bq), Tm(Tmb, b, t.bp, bq);
+
+    // whole-product split-K plans
+    const int64_t kz_l = gemm_plan_kps(sk, ZL, Wuv.T(), ML, 0.0);
+    const int64_t ku_l = gemm_plan_kps(sk, ML, Yuv, ZL, 1.0);
+    const int64_t kz_r = jr ? gemm_plan_kps(sk, ZR, MR, Wvv, 0.0) : 0;
+    const int64_t ku_r = jr ? gemm_plan_kps(sk, MR, ZR, Yvv.T(), 1.0) : 0;
+    const int64_t ku_x = jr ? gemm_plan_kps(sk, MR.sub(c1r, 0, i, jr), X, Yvv.T(), 1.0) : 0;
+
+    // ZL[:, c0:c1] = W_U^T ML[:, c0:c1]
+    auto zl = [&](int64_t c0, int64_t c1) -> int {
+      if (c0 >= c1) return 0;
+      TimeScope ts(ws, st, TC_GEMM, gemm_flops(t.bp, c1 - c0, i));
+      return gemm(st, sk, ZL.sub(0, c0, t.bp, c1 - c0), Wuv.T(), ML.sub(0, c0, i, c1 - c0), 1.0,
+                  0.0, nullptr, 0, kz_l);
+    };
+    // ML[r0:r1, c0:c1] += Y_U[r0:r1] ZL[:, c0:c1]
+    auto ul = [&](int64_t r0, int64_t r1, int64_t c0, int64_t c1) -> int {
+      if (c0 >= c1 || r0 >= r1) return 0;
+      TimeScope ts(ws, st, TC_GEMM, gemm_flops(r1 - r0, c1 - c0, t.bp));
+      return gemm(st, sk, ML.sub(r0, c0, r1 - r0, c1 - c0), Yuv.sub(r0, 0, r1 - r0, t.bp),
+                  ZL.sub(0, c0, t.bp, c1 - c0), 1.0, 1.0, nullptr, 0, ku_l);
+    };
+    // ZR[r0:r1] = MR[r0:r1] W_V
+    auto zr = [&](int64_t r0, int64_t r1) -> int {
+      if (r0 >= r1 || !jr) return 0;
+      TimeScope ts(ws, st, TC_GEMM, gemm_flops(r1 - r0, bq, jr));
+      return gemm(st, sk, ZR.sub(r0, 0, r1 - r0, bq), MR.sub(r0, 0, r1 - r0, jr), Wvv, 1.0, 0.0,
+                  nullptr, 0, kz_r);
+    };
+    // MR[r0:r1, c0:c1] += ZR[r0:r1] Y_V[c0:c1]^T
+    auto ur = [&](int64_t r0, int64_t r1, int64_t c0, int64_t c1) -> int {
+      if (r0 >= r1 || c0 >= c1) return 0;
+      TimeScope ts(ws, st, TC_GEMM, gemm_flops(r1 - r0, c1 - c0, bq));
+      return gemm(st, sk, MR.sub(r0, c0, r1 - r0, c1 - c0), ZR.sub(r0, 0, r1 - r0, bq),
+                  Yvv.sub(c0, 0, c1 - c0, bq).T(), 1.0, 1.0, nullptr, 0, ku_r);
+    };
+    // Simultaneous D block [r0:r1, c0:c1] (D coordinates): += X Y_V^T, += Y_U Z_L
+    auto dsim = [&](int64_t r0, int64_t r1, int64_t c0, int64_t c1) -> int {
+      if (r0 >= r1 || c0 >= c1) return 0;
+      {
+        TimeScope ts(ws, st, TC_GEMM, gemm_flops(r1 - r0, c1 - c0, bq));
+        BR_CHECK(gemm(st, sk, MR.sub(c1r + r0, c0, r1 - r0, c1 - c0), X.sub(r0, 0, r1 - r0, bq),
+                      Yvv.sub(c0, 0, c1 - c0, bq).T(), 1.0, 1.0, nullptr, 0, ku_x));
+      }
+      return ul(r0, r1, b1w + c0, b1w + c1);
+    };
+    auto issue_next = [&]() -> int {  // both next panels on the panel stream
+      cudaEvent_t ev = ws_event(ws);
+      BR_CUDA(cudaEventRecord(ev, ws.main));
+      BR_CUDA(cudaStreamWaitEvent(ws.panel, ev, 0));
+      BR_CHECK(panels(ws.panel, ws.sk_panel, tn, par ^ 1));
+      ev_panels = ws_event(ws);
+      BR_CUDA(cudaEventRecord(ev_panels, ws.panel));
+      return 0;
+    };
+
+    // footprints of the next panels: QR columns ML[:, 0:bpn), LQ rows
+    // MR[bp-bq : bp-bq+bqn) (ref svd.py:394-420)
+    const int64_t bpn = tn.bp, bqn = tn.jr >= 1 ? tn.bq : 0;
+    const int64_t hc = la ? std::min(bpn, ncL) : 0;                        // ML head columns
+    const int64_t hr = la ? std::min(t.bp - bq + bqn, nrR) : 0;            // MR head rows
+    const int64_t sc = la ? std::max<int64_t>(0, std::min(bpn - b1w, jr)) : 0;  // D cols of next QR
+    const int64_t sr = la ? std::max<int64_t>(0, std::min(hr - c1r, i)) : 0;    // D rows of next LQ
+    bool issued = false;
+
+    BR_CHECK(zl(0, ncL));
+    if (!fused || !jr) {
+      if (jr && sc == 0 && sr == 0 && la) {
+        // V1 regime: next QR inside B1, next LQ inside C1
+        BR_CHECK(ul(0, i, 0, hc));
+        BR_CHECK(zr(0, hr));
+        BR_CHECK(ur(0, hr, 0, jr));
+        BR_CHECK(issue_next());
+        issued = true;
+        BR_CHECK(ul(0, i, hc, ncL));
+        BR_CHECK(zr(hr, nrR));
+        BR_CHECK(ur(hr, nrR, 0, jr));
+      } else if (!jr && la) {
+        BR_CHECK(ul(0, i, 0, hc));
+        BR_CHECK(issue_next());
+        issued = true;
+        BR_CHECK(ul(0, i, hc, ncL));
+      } else {
+        BR_CHECK(ul(0, i, 0, ncL));
+        BR_CHECK(zr(0, nrR));
+        if (la) {  // V2 regime: heads (LQ rows, then QR columns of D) first
+          BR_CHECK(ur(0, hr, 0, jr));
+          BR_CHECK(ur(hr, nrR, 0, c1r < hr ? sc : std::min(sc, jr)));
+          BR_CHECK(issue_next());
+          issued = true;
+          BR_CHECK(ur(hr, nrR, sc, jr));
+        } else {
+          BR_CHECK(ur(0, nrR, 0, jr));
+        }
+      }
+    } else {
+      // Simultaneous: ZL, ZR from the old D; X = ZR_D + Y_U (ZL_D W_V)
+      BR_CHECK(zr(0, nrR));
+      {
+        TimeScope ts(ws, st, TC_GEMM, gemm_flops(t.bp, bq, jr) + gemm_flops(i, bq, t.bp));
+        BR_CHECK(gemm(st, sk, Tm, ZL.sub(0, b1w, t.bp, jr), Wvv, 1.0, 0.0));
+        MatView ZRD = ZR.sub(c1r, 0, i, bq);
+        BR_CHECK(gemm(st, sk, X, Yuv, Tm, 1.0, 1.0, &ZRD));
+      }
+      if (la) {
+        const int64_t hb = std::min(hc, b1w), hcr = std::min(hr, c1r);
+        BR_CHECK(ul(0, i, 0, hb));           // B1 head
+        BR_CHECK(ur(0, hcr, 0, jr));         // C1 head
+        BR_CHECK(dsim(0, sr, 0, sc));        // D11
+        BR_CHECK(dsim(sr, i, 0, sc));        // D21
+        BR_CHECK(dsim(0, sr, sc, jr));       // D12
+        BR_CHECK(issue_next());
+        issued = true;
+        BR_CHECK(ul(0, i, hb, b1w));         // B1 rest
+        BR_CHECK(ur(hcr, c1r, 0, jr));       // C1 rest
+        BR_CHECK(dsim(sr, i, sc, jr));       // D22
+      } else {
+        BR_CHECK(ul(0, i, 0, b1w));
+        BR_CHECK(ur(0, c1r, 0, jr));
+        BR_CHECK(dsim(0, i, 0, jr));
+      }
+    }
+    if (has_next && !issued) BR_CHECK(panels(ws.main, ws.sk_main, tn, par ^ 1));
+  }
+  if (ev_panels) BR_CUDA(cudaStreamWaitEvent(ws.main, ev_panels, 0));
+  ws_events_reset(ws);
+  return mask_tri(ws.main, A, lda, m, n, w, w);
 }
 
 }  // namespace br

@@ -179,6 +179,44 @@ def tri_counted_flops(m, n, w, b, inner_b=16, max_iters=None):
     return acc.as_dict(), it
 
 
+def band_counted_flops(m, n, w, b, simultaneous=False, inner_b=16):
+    """Reference-equivalent counted flops of reduce_band_svd's band form
+    (ref svd.py:359-391; V1 counts as Reference and V2 as Simultaneous since
+    their splits are linear in the matmul dimensions)."""
+    if m < n:
+        m, n = n, m
+    acc = _Acc()
+    k = 0
+    it = 0
+    while m - k - w >= 2 and k < n:
+        bp = min(b, m - k - w, n - k)
+        jr = n - k - w
+        bq = min(bp, jr) if jr >= 1 else 0
+        i = m - k - w
+        _panel(acc, i, bp, inner_b)
+        b1end = min(k + w, n)
+        if k + bp < b1end:
+            _apply_left(acc, i, b1end - k - bp, bp)
+        if jr >= 1:
+            if not simultaneous:
+                _apply_left(acc, i, jr, bp)
+            _panel(acc, jr, bq, inner_b)
+            if k + bq < k + w:
+                _apply_right(acc, w - bq, jr, bq)
+            if not simultaneous:
+                _apply_right(acc, i, jr, bq)
+            else:
+                acc.mm(jr, i, bp)  # Z_L = D^T W_U
+                acc.mm(i, jr, bq)  # Z_R = D W_V
+                acc.mm(bp, jr, bq)  # Z_L^T W_V
+                acc.mm(i, bp, bq)  # Y_U (.)
+                acc.mm(i, bq, jr)  # X Y_V^T
+                acc.mm(i, bp, jr)  # Y_U Z_L^T
+        k += bp
+        it += 1
+    return acc.as_dict(), it
+
+
 def sevp_nominal_flops(n):
     """Nominal cost 4n^3/3 (ref sevp.py:92-96)."""
     if n < 0:

@@ -10,9 +10,11 @@ left/right updates run. The split updates are bitwise identical to the
 sequential order on the same GPU.
 
 `reduce_band_svd(A, cfg)` dispatches cfg.form == TRIANGULAR_BAND to
-reduce_tri_band exactly like ref svd.py:552-553; the equal-bandwidth BAND
-form (ref svd.py:250-589) is ranked "next" in SURVEY.md 8(f) and not built
-yet, so it raises NotImplementedError rather than computing on the CPU.
+reduce_tri_band exactly like ref svd.py:552-553 and runs the equal-bandwidth
+BAND form (ref svd.py:250-589) on the GPU: REFERENCE / V1 apply the left
+then the right trailing update, SIMULTANEOUS / V2 the fused two-sided
+update; V1 / V2 add static look-ahead (both next panels factored on the
+panel stream), bitwise equal to REFERENCE / SIMULTANEOUS on the same GPU.
 """
 from __future__ import annotations
 
@@ -23,7 +25,7 @@ from enum import Enum
 import numpy as np
 
 from . import _dev, _lib
-from .flops import FLOPS, svd_nominal_flops, tri_counted_flops  # noqa: F401
+from .flops import FLOPS, band_counted_flops, svd_nominal_flops, tri_counted_flops  # noqa: F401
 from .sevp import V2Mapping
 
 
@@ -129,16 +131,58 @@ def reduce_tri_band(A, w, b, groups=None, range_log=None, inner_b=16, *, lookahe
                      iterations=int(st.iterations))
 
 
-def reduce_band_svd(A, cfg, groups=None, range_log=None, *, lookahead=None, device=None):
-    """Dispatch on cfg.form (ref svd.py:515-589)."""
+def reduce_band_svd(A, cfg, groups=None, range_log=None, *, lookahead=None, device=None,
+                    stats=None):
+    """Dispatch on cfg.form (ref svd.py:515-589); m < n reduces A^T and swaps
+    the bandwidth tags (ref svd.py:530-550); m <= w + 1 returns A unchanged."""
     cfg.validate()
     A = np.array(A, dtype=np.float64, order="F")
     if A.ndim != 2:
         raise ValueError("reduce_band_svd needs a 2-D matrix")
     if A.shape != (cfg.m, cfg.n):
         raise ValueError(f"cfg says {cfg.m} x {cfg.n} but the matrix is {A.shape[0]} x {A.shape[1]}")
+    if cfg.m < cfg.n:
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", RuntimeWarning)  # already warned once
+            tcfg = SvdConfig(m=cfg.n, n=cfg.m, w=cfg.w, b=cfg.b, form=cfg.form,
+                             variant=cfg.variant, v2_mapping=cfg.v2_mapping, inner_b=cfg.inner_b)
+            inner = reduce_band_svd(np.asfortranarray(A.T), tcfg, groups, range_log,
+                                    lookahead=lookahead, device=device, stats=stats)
+        return SvdResult(band=np.asfortranarray(inner.band.T), flops=inner.flops, form=cfg.form,
+                         lower_bw=inner.upper_bw, upper_bw=inner.lower_bw,
+                         iterations=inner.iterations)
     if cfg.form == SvdForm.TRIANGULAR_BAND:
         return reduce_tri_band(A, cfg.w, cfg.b, groups, range_log, cfg.inner_b,
-                               lookahead=lookahead, device=device)
-    raise NotImplementedError(
-        "equal-bandwidth BAND form is not built on the B200 path yet (SURVEY.md 8(f) next #1)")
+                               lookahead=lookahead, device=device, stats=stats)
+    if range_log is not None:
+        if cfg.variant != SvdVariant.REFERENCE:
+            raise ValueError("range logging is defined for the reference schedule")
+        if cfg.w % cfg.b != 0:
+            raise ValueError("range logging requires w to be a multiple of b")
+        raise ValueError("range_log instrumentation is a CPU-reference analysis feature; "
+                         "not supported on the GPU path")
+    simultaneous = cfg.variant in (SvdVariant.SIMULTANEOUS, SvdVariant.V2)
+    if lookahead is None:
+        # V1 / V2 are the look-ahead schedules; REFERENCE / SIMULTANEOUS are
+        # sequential (results are bitwise identical either way)
+        lookahead = _depth(groups, None) if cfg.variant in (SvdVariant.V1, SvdVariant.V2) else 0
+    depth = _depth(groups, lookahead)
+    m, n, w, b = cfg.m, cfg.n, cfg.w, cfg.b
+    lib = _lib.load()
+    h, _ = _dev.ctx(device)
+    band = np.empty((m, n), order="F")
+    st = _lib.BrStats()
+    rc = lib.br_reduce_band_host(h, m, n, w, b, int(simultaneous), depth, A.ctypes.data, m,
+                                 band.ctypes.data, m, st)
+    _lib.check(rc, "reduce_band_svd")
+    if st.iterations == 0:
+        flops = {"total": 0}
+    else:
+        flops, _ = band_counted_flops(m, n, w, b, simultaneous, cfg.inner_b)
+        for key, val in flops.items():
+            if key != "total":
+                FLOPS.add(key, val)
+    if stats is not None:
+        stats.update(device_ms=st.device_ms, launches=st.launches, iterations=st.iterations)
+    return SvdResult(band=band, flops=flops, form=SvdForm.BAND, lower_bw=w, upper_bw=w,
+                     iterations=int(st.iterations))

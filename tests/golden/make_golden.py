@@ -171,6 +171,39 @@ def reductions_golden():
     print("reductions.npz", len(d), "arrays")
 
 
+BAND_CASES = [
+    # (name, m, n, w, b, seed, variant)
+    ("b64_8_8_ref", 64, 64, 8, 8, 400, "reference"),
+    ("b64_8_8_sim", 64, 64, 8, 8, 400, "simultaneous"),
+    ("b64_8_8_v2", 64, 64, 8, 8, 400, "v2"),
+    ("b80_12_4_v1", 80, 80, 12, 4, 401, "v1"),
+    ("b80_12_4_ref", 80, 80, 12, 4, 401, "reference"),
+    ("b96_70_8_6_ref", 96, 70, 8, 6, 402, "reference"),  # rectangular m > n
+    ("b50_90_6_6_sim", 50, 90, 6, 6, 403, "simultaneous"),  # wide: transpose
+    ("b256_32_32_v2", 256, 256, 32, 32, 404, "v2"),
+    ("b130_16_16_ref", 130, 130, 16, 16, 405, "reference"),
+]
+
+
+def band_golden():
+    d = {}
+    V = {"reference": bandred.SvdVariant.REFERENCE, "simultaneous": bandred.SvdVariant.SIMULTANEOUS,
+         "v1": bandred.SvdVariant.V1, "v2": bandred.SvdVariant.V2}
+    for name, m, n, w, b, seed, var in BAND_CASES:
+        A = rand(m, n, seed)
+        cfg = bandred.SvdConfig(m=m, n=n, w=w, b=b, form=bandred.SvdForm.BAND, variant=V[var])
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            res = bandred.reduce_band_svd(A, cfg)
+        d[f"{name}_A"] = A
+        d[f"{name}_band"] = res.band
+        d[f"{name}_meta"] = np.array([m, n, w, b, res.iterations, res.flops["total"], res.lower_bw,
+                                      res.upper_bw], dtype=np.int64)
+    np.savez_compressed(os.path.join(OUT, "band.npz"), **d)
+    print("band.npz", len(d), "arrays")
+
+
 if __name__ == "__main__":
     kernels_golden()
     reductions_golden()
+    band_golden()

@@ -316,3 +316,82 @@ def test_c2_full_vs_oracle(br):
     sa = np.linalg.svd(A, compute_uv=False)
     sb = np.linalg.svd(res.band, compute_uv=False)
     assert np.max(np.abs(sa - sb)) <= 1e-10 * sa[0]
+
+
+# --- equal-bandwidth band form --------------------------
+
+BAND = np.load(os.path.join(G, "band.npz"))
+BAND_CASES = sorted({k[: -len("_meta")] for k in BAND.files if k.endswith("_meta")})
+SVDV = {"ref": "REFERENCE", "sim": "SIMULTANEOUS", "v1": "V1", "v2": "V2"}
+
+
+@pytest.mark.parametrize("name", BAND_CASES)
+@pytest.mark.parametrize("lookahead", [None, 0, 1])
+def test_reduce_band_svd_golden(br, name, lookahead):
+    m, n, w, b, iters, flops, lbw, ubw = (int(x) for x in BAND[f"{name}_meta"])
+    A = BAND[f"{name}_A"]
+    var = getattr(br.SvdVariant, SVDV[name.rsplit("_", 1)[1]])
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        res = br.reduce_band_svd(A, br.SvdConfig(m, n, w, b, variant=var), lookahead=lookahead)
+    assert (res.lower_bw, res.upper_bw, res.iterations) == (lbw, ubw, iters)
+    assert res.form == br.SvdForm.BAND
+    assert br.band_check(res.band, lbw, ubw) == 0.0
+    assert rel(res.band, BAND[f"{name}_band"], np.linalg.norm(A)) <= 1e-13
+    assert res.flops["total"] == flops
+
+
+@pytest.mark.parametrize("m,n,w,b", [(600, 600, 32, 32), (600, 600, 48, 16), (700, 520, 40, 12),
+                                     (520, 700, 24, 24), (400, 400, 64, 40)])
+def test_band_lookahead_bitwise(br, m, n, w, b):
+    """V1 == Reference and V2 == Simultaneous bit for bit (the look-ahead
+    pieces reuse the whole-product split-K plan)."""
+    A = rand(m, n, m + n + w + b)
+    R = br.SvdVariant
+    seq = {v: br.reduce_band_svd(A, br.SvdConfig(m, n, w, b, variant=v), lookahead=0)
+           for v in (R.REFERENCE, R.SIMULTANEOUS)}
+    la = {v: br.reduce_band_svd(A, br.SvdConfig(m, n, w, b, variant=v), lookahead=1)
+          for v in (R.REFERENCE, R.SIMULTANEOUS)}
+    for v in seq:
+        assert np.array_equal(seq[v].band, la[v].band)
+    if 2 * b <= w:
+        v1 = br.reduce_band_svd(A, br.SvdConfig(m, n, w, b, variant=R.V1))
+        assert np.array_equal(v1.band, seq[R.REFERENCE].band)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        v2 = br.reduce_band_svd(A, br.SvdConfig(m, n, w, b, variant=R.V2))
+    assert np.array_equal(v2.band, seq[R.SIMULTANEOUS].band)
+    # both orders agree with the oracle and each other to rounding
+    ref, lo, up, it = O.reduce_band_svd(A, w, b)
+    assert seq[R.REFERENCE].iterations == it
+    scale = np.linalg.norm(A)
+    assert rel(seq[R.REFERENCE].band, ref, scale) <= 1e-13
+    assert rel(seq[R.SIMULTANEOUS].band, ref, scale) <= 1e-13
+    sa = np.linalg.svd(A, compute_uv=False)
+    sb = np.linalg.svd(la[R.SIMULTANEOUS].band, compute_uv=False)
+    assert np.max(np.abs(sa - sb)) <= 1e-11 * sa[0]
+
+
+def test_band_edge_cases(br):
+    # m <= w + 1: returned unchanged, no iterations (ref svd.py:561-564)
+    A = rand(9, 7, 1)
+    res = br.reduce_band_svd(A, br.SvdConfig(9, 7, 8, 4))
+    assert res.iterations == 0 and res.flops["total"] == 0 and np.array_equal(res.band, A)
+    # diagonal input: band form of a band matrix keeps its singular values
+    D = np.asfortranarray(np.diag(np.arange(1.0, 41.0)))
+    res = br.reduce_band_svd(D, br.SvdConfig(40, 40, 4, 4))
+    ref, _, _, _ = O.reduce_band_svd(D, 4, 4)
+    assert np.array_equal(res.band, ref)
+    # zero matrix stays exactly zero; a column of zeros is harmless
+    Z = np.zeros((50, 50))
+    assert np.array_equal(br.reduce_band_svd(Z, br.SvdConfig(50, 50, 6, 3)).band, Z)
+    A = rand(80, 60, 2)
+    A[:, 10] = 0.0
+    res = br.reduce_band_svd(A, br.SvdConfig(80, 60, 8, 8, variant=br.SvdVariant.SIMULTANEOUS))
+    ref, _, _, _ = O.reduce_band_svd(A, 8, 8, simultaneous=True)
+    assert rel(res.band, ref, np.linalg.norm(A)) <= 1e-13
+    # tall-skinny: jr < 1 from the first iteration (left-only iterations)
+    A = rand(200, 10, 5)
+    res = br.reduce_band_svd(A, br.SvdConfig(200, 10, 12, 6))
+    ref, _, _, it = O.reduce_band_svd(A, 12, 6)
+    assert res.iterations == it and rel(res.band, ref, np.linalg.norm(A)) <= 1e-13

@@ -110,10 +110,30 @@ def test_no_cpu_fallback_without_gpu():
 
 
 def test_band_form_not_silently_computed_on_cpu():
-    with pytest.raises((NotImplementedError, RuntimeError)):
-        with warnings.catch_warnings():
-            warnings.simplefilter("ignore")
-            br.reduce_band_svd(np.ones((20, 20)), br.SvdConfig(20, 20, 4, 4))
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: covered by the gpu tests")
+    for var in br.SvdVariant:
+        with pytest.raises(RuntimeError):
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                br.reduce_band_svd(np.ones((20, 20)), br.SvdConfig(20, 20, 4, 2, variant=var))
+    with pytest.raises(RuntimeError):  # wide input reduces the transpose, same path
+        br.reduce_band_svd(np.ones((10, 20)), br.SvdConfig(10, 20, 4, 2))
+
+
+def test_band_form_validation_matches_reference():
+    with pytest.raises(ValueError, match="V1 requires 2b <= w"):
+        br.reduce_band_svd(np.ones((20, 20)), br.SvdConfig(20, 20, 4, 3, variant=br.SvdVariant.V1))
+    with pytest.raises(ValueError, match="need 1 <= b <= w"):
+        br.reduce_band_svd(np.ones((20, 20)), br.SvdConfig(20, 20, 4, 5))
+    with pytest.raises(ValueError, match="range logging is defined for the reference"):
+        br.reduce_band_svd(np.ones((20, 20)),
+                           br.SvdConfig(20, 20, 4, 2, variant=br.SvdVariant.SIMULTANEOUS),
+                           range_log=[])
+    with pytest.raises(ValueError, match="cfg says"):
+        br.reduce_band_svd(np.ones((20, 21)), br.SvdConfig(20, 20, 4, 2))
 
 
 def test_exec_groups_maps_to_lookahead_depth():

@@ -123,3 +123,34 @@ def test_nominal_flops():
     assert O.sevp_nominal_flops(3) == 36
     assert O.svd_nominal_flops(9, 9) == 1944
     assert O.svd_nominal_flops(12, 8) == 2389
+
+
+BAND = np.load(os.path.join(G, "band.npz"))
+BAND_CASES = sorted({k[: -len("_meta")] for k in BAND.files if k.endswith("_meta")})
+
+
+@pytest.mark.parametrize("name", BAND_CASES)
+def test_reduce_band_svd_matches_reference(name):
+    m, n, w, b, iters, flops, lbw, ubw = (int(x) for x in BAND[f"{name}_meta"])
+    A = BAND[f"{name}_A"]
+    sim = name.endswith(("_sim", "_v2"))
+    band, lo, up, it = O.reduce_band_svd(A, w, b, simultaneous=sim)
+    assert (lo, up, it) == (lbw, ubw, iters)
+    assert O.band_check(band, lo, up) == 0.0
+    assert rel(band, BAND[f"{name}_band"], np.linalg.norm(A)) <= 1e-13
+
+
+@pytest.mark.parametrize("name", BAND_CASES)
+def test_band_counted_flops_match_reference(name):
+    from paper_1709_00302_b200.flops import band_counted_flops
+
+    m, n, w, b, iters, flops, _, _ = (int(x) for x in BAND[f"{name}_meta"])
+    got, it = band_counted_flops(m, n, w, b, simultaneous=name.endswith(("_sim", "_v2")))
+    assert (got["total"], it) == (flops, iters)
+
+
+def test_band_form_small_input_unchanged():
+    # m <= w + 1: nothing is off-band (ref svd.py:561-564)
+    A = np.random.default_rng(3).standard_normal((5, 5))
+    band, lo, up, it = O.reduce_band_svd(A, 4, 2)
+    assert it == 0 and np.array_equal(band, A) and (lo, up) == (4, 4)
