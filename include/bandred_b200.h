@@ -53,11 +53,21 @@ int br_destroy(br_handle_t h);
  * handle's own. */
 int br_set_streams(br_handle_t h, void* main_stream, void* panel_stream);
 int br_sync(br_handle_t h);
-/* Per-kernel-class CUDA-event timing of subsequent reductions (bench). */
+/* Per-kernel-class CUDA-event timing of subsequent reductions (bench).
+ * enable: 0 off, 1 per-class totals, 2 totals + per-task event trace. */
 int br_set_timing(br_handle_t h, int enable);
 /* Class: 0 = panel, 1 = symm, 2 = syr2k, 3 = gemm (other updates).
- * Accumulated since br_set_timing(h, 1). */
+ * Accumulated since br_set_timing(h, 1 or 2). */
 int br_get_timing(br_handle_t h, int cls, double* ms, double* flops, int64_t* launches);
+/* Event trace of the last reduction run with br_set_timing(h, 2): one record
+ * per task ("qr@k", "lq@k", "left@k", "trail@k", ...; the task ids of the
+ * reference's EventTrace, ref runtime.py:76-104), its stream (0 = main, the
+ * T_P group; 1 = panel, the T_S group) and its device start/end time in
+ * microseconds since the call began. Overlap of the two streams is the
+ * look-ahead. br_trace_count returns the record count (-1 for a NULL h). */
+int64_t br_trace_count(br_handle_t h);
+int br_trace_get(br_handle_t h, int64_t idx, char* id, int64_t idlen, int* stream, double* t0_us,
+                 double* t1_us);
 
 /* Kernel-level calls below run on the main stream (which = 0, default) or the
  * panel stream (which = 1) - the two worker groups of the reference runtime

@@ -11,6 +11,7 @@ There is no CPU fallback: every compute entry point raises if the CUDA
 library or device is missing.
 """
 from .checks import band_check, orth_residual, spectra_match
+from .cli import gen_general, gen_sym, load_matrix, save_matrix
 from .flops import FLOPS, FlopCounter, reset_flops, snapshot_flops, sevp_nominal_flops, svd_nominal_flops
 from .kernels import (
     PanelFactors,
@@ -24,7 +25,7 @@ from .kernels import (
     symm_lower,
     syr2k_lower,
 )
-from .runtime import ExecGroups, WriteOverlapError
+from .runtime import EventTrace, ExecGroups, WriteOverlapError
 from .sevp import SevpConfig, SevpResult, SevpVariant, V2Mapping, reduce_sym_band
 from .svd import SvdConfig, SvdForm, SvdResult, SvdVariant, reduce_band_svd, reduce_tri_band
 from ._dev import set_device, get_device
@@ -45,6 +46,7 @@ __all__ = [
     "syr2k_lower",
     "sym_two_sided_update",
     "ExecGroups",
+    "EventTrace",
     "WriteOverlapError",
     "SevpConfig",
     "SevpResult",
@@ -62,6 +64,10 @@ __all__ = [
     "band_check",
     "orth_residual",
     "spectra_match",
+    "gen_general",
+    "gen_sym",
+    "save_matrix",
+    "load_matrix",
     "set_device",
     "get_device",
 ]

@@ -49,6 +49,34 @@ def call(what: str, fn, *args):
     _lib.check(_lib.load().br_sync(h), what + " (sync)")
 
 
+def run_traced(h, groups, fn):
+    """Run one reduction call `fn() -> rc`. If `groups` carries an EventTrace
+    (ExecGroups does, like the reference's, ref runtime.py:142-160), the
+    library's per-task device trace of this call is appended to it: task id
+    "qr@k" / "left@k" / ..., group "seq" for the panel stream (the T_S role)
+    and "par" for the main stream (T_P), start/end in microseconds."""
+    trace = getattr(groups, "trace", None)
+    lib = _lib.load()
+    if trace is None:
+        return fn()
+    _lib.check(lib.br_set_timing(h, 2), "trace")
+    try:
+        rc = fn()
+        if rc == 0:
+            import ctypes as C
+
+            buf = C.create_string_buffer(64)
+            s, t0, t1 = C.c_int(), C.c_double(), C.c_double()
+            for i in range(lib.br_trace_count(h)):
+                _lib.check(lib.br_trace_get(h, i, buf, 64, C.byref(s), C.byref(t0), C.byref(t1)),
+                           "trace")
+                trace.append(buf.value.decode(), "seq" if s.value == 1 else "par", t0.value,
+                             t1.value)
+    finally:
+        lib.br_set_timing(h, 0)
+    return rc
+
+
 def ld_pad(rows: int) -> int:
     """Device leading dimension: rows rounded up to 32 doubles (256 B)."""
     return max(32, (rows + 31) // 32 * 32)

@@ -61,6 +61,9 @@ SIGNATURES = {
                                           dptr, i64, C.POINTER(BrStats)]),
     "br_reduce_tri_band_host": (C.c_int, [C.c_void_p, i64, i64, i64, i64, C.c_int, dptr, i64, dptr,
                                           i64, C.POINTER(BrStats)]),
+    "br_trace_count": (i64, [C.c_void_p]),
+    "br_trace_get": (C.c_int, [C.c_void_p, i64, C.c_char_p, i64, C.POINTER(C.c_int),
+                               C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "br_reduce_band": (C.c_int, [C.c_void_p, i64, i64, i64, i64, C.c_int, C.c_int, dptr, i64,
                                  C.POINTER(BrStats)]),
     "br_reduce_band_host": (C.c_int, [C.c_void_p, i64, i64, i64, i64, C.c_int, C.c_int, dptr, i64,

@@ -60,7 +60,8 @@ static cudaEvent_t ws_tevent(Workspace& ws) {
   return ws.tevents[ws.tevent_next++];
 }
 
-TimeScope::TimeScope(Workspace& w, cudaStream_t s, int c, double f) : ws(w), st(s), cls(c), flops(f) {
+TimeScope::TimeScope(Workspace& w, cudaStream_t s, int c, double f, const char* tg, int64_t kk)
+    : ws(w), st(s), cls(c), flops(f), tag(tg), k(kk) {
   if (ws.timing) {
     a = ws_tevent(ws);
     cudaEventRecord(a, st);
@@ -70,9 +71,11 @@ TimeScope::~TimeScope() {
   if (ws.timing) {
     cudaEvent_t b = ws_tevent(ws);
     cudaEventRecord(b, st);
-    ws.timed.push_back({cls, a, b, flops});
+    ws.timed.push_back({cls, a, b, flops, tag, k, st == ws.panel ? 1 : 0});
   }
 }
+
+static const char* kClassName[TC_COUNT] = {"panel", "symm", "syr2k", "gemm"};
 
 int ws_collect_timing(Workspace& ws) {
   for (auto& t : ws.timed) {
@@ -81,6 +84,19 @@ int ws_collect_timing(Workspace& ws) {
     ws.t_ms[t.cls] += ms;
     ws.t_flops[t.cls] += t.flops;
     ws.t_launches[t.cls] += 1;
+    if (ws.timing >= 2 && ws.trace_base) {
+      Workspace::TraceRec r{};
+      const char* tg = t.tag ? t.tag : kClassName[t.cls];
+      if (t.k >= 0) snprintf(r.id, sizeof(r.id), "%s@%lld", tg, (long long)t.k);
+      else snprintf(r.id, sizeof(r.id), "%s", tg);
+      r.stream = t.stream;
+      float t0 = 0.f, t1 = 0.f;
+      BR_CUDA(cudaEventElapsedTime(&t0, ws.trace_base, t.a));
+      BR_CUDA(cudaEventElapsedTime(&t1, ws.trace_base, t.b));
+      r.t0_us = 1e3 * t0;
+      r.t1_us = 1e3 * t1;
+      ws.trace.push_back(r);
+    }
   }
   ws.timed.clear();
   ws.tevent_next = 0;
@@ -156,6 +172,48 @@ int zero_fill(cudaStream_t st, MatView V) {
   if (V.rows <= 0 || V.cols <= 0) return 0;
   const int64_t r = V.trans ? V.cols : V.rows, c = V.trans ? V.rows : V.cols;
   BR_CUDA(cudaMemset2DAsync(V.p, V.ld * sizeof(double), 0, r * sizeof(double), c, st));
+  return 0;
+}
+
+// Runs one reduction on the handle's streams, timed by events on `main`
+// around the whole stream program (both streams joined at the end).
+template <class F>
+int timed_reduction(Workspace& ws, br_stats* stats, double nominal, F&& body) {
+  cudaEvent_t e0, e1;
+  BR_CUDA(cudaEventCreate(&e0));
+  BR_CUDA(cudaEventCreate(&e1));
+  const int64_t l0 = launch_count();
+  auto cu = [](cudaError_t e) -> int {
+    if (e == cudaSuccess) return 0;
+    set_error("CUDA: %s", cudaGetErrorString(e));
+    return 1000 + (int)e;
+  };
+  int rc = cu(cudaEventRecord(e0, ws.main));
+  ws.trace_base = e0;
+  if (ws.timing >= 2) ws.trace.clear();
+  int64_t iters = 0;
+  float ms = 0.f;
+  if (!rc) rc = body(&iters);
+  if (!rc) rc = cu(cudaEventRecord(e1, ws.main));
+  if (!rc) rc = cu(cudaEventSynchronize(e1));
+  if (!rc) rc = cu(cudaStreamSynchronize(ws.panel));
+  if (!rc) rc = cu(cudaGetLastError());
+  if (!rc) rc = cu(cudaEventElapsedTime(&ms, e0, e1));
+  if (!rc && ws.timing) rc = ws_collect_timing(ws);
+  ws.trace_base = nullptr;
+  if (rc) {
+    ws.timed.clear();
+    ws.tevent_next = 0;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (rc) return rc;
+  if (stats) {
+    stats->iterations = iters;
+    stats->device_ms = ms;
+    stats->nominal_flops = nominal;
+    stats->launches = launch_count() - l0;
+  }
   return 0;
 }
 
@@ -267,7 +325,9 @@ int br_sync(br_handle_t h) {
 
 int br_set_timing(br_handle_t h, int enable) {
   ARG(h != nullptr, 1);
-  h->ws.timing = enable != 0;
+  ARG(enable >= 0 && enable <= 2, 2);
+  h->ws.timing = enable;
+  h->ws.trace.clear();
   for (int c = 0; c < TC_COUNT; ++c) {
     h->ws.t_ms[c] = 0;
     h->ws.t_flops[c] = 0;
@@ -284,6 +344,20 @@ int br_get_timing(br_handle_t h, int cls, double* ms, double* flops, int64_t* la
   if (ms) *ms = h->ws.t_ms[cls];
   if (flops) *flops = h->ws.t_flops[cls];
   if (launches) *launches = h->ws.t_launches[cls];
+  return 0;
+}
+
+int64_t br_trace_count(br_handle_t h) { return h ? (int64_t)h->ws.trace.size() : -1; }
+
+int br_trace_get(br_handle_t h, int64_t idx, char* id, int64_t idlen, int* stream, double* t0_us,
+                 double* t1_us) {
+  ARG(h != nullptr, 1);
+  ARG(idx >= 0 && idx < (int64_t)h->ws.trace.size(), 2);
+  const auto& r = h->ws.trace[idx];
+  if (id && idlen > 0) snprintf(id, (size_t)idlen, "%s", r.id);
+  if (stream) *stream = r.stream;
+  if (t0_us) *t0_us = r.t0_us;
+  if (t1_us) *t1_us = r.t1_us;
   return 0;
 }
 
@@ -515,35 +589,10 @@ int br_reduce_sym_band(br_handle_t h, int64_t n, int64_t w, int64_t b, int looka
   ARG(A != nullptr && lda >= n, 6);
   ARG(Q == nullptr || ldq >= n, 9);
   DEV(h);
-  Workspace& ws = h->ws;
-  cudaEvent_t e0, e1;
-  BR_CUDA(cudaEventCreate(&e0));
-  BR_CUDA(cudaEventCreate(&e1));
-  const int64_t l0 = launch_count();
-  BR_CUDA(cudaEventRecord(e0, ws.main));
-  int64_t iters = 0;
-  int rc = sevp_reduce(ws, n, w, b, lookahead, A, lda, Q, ldq, &iters);
-  if (rc) {
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    return rc;
-  }
-  BR_CUDA(cudaEventRecord(e1, ws.main));
-  BR_CUDA(cudaEventSynchronize(e1));
-  BR_CUDA(cudaStreamSynchronize(ws.panel));
-  BR_CUDA(cudaGetLastError());
-  float ms = 0;
-  BR_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  if (ws.timing) BR_CHECK(ws_collect_timing(ws));
-  if (stats) {
-    stats->iterations = iters;
-    stats->device_ms = ms;
-    stats->nominal_flops = sevp_nominal(n);
-    stats->launches = launch_count() - l0;
-  }
-  return 0;
+  return timed_reduction(h->ws, stats, sevp_nominal(n),
+                         [&](int64_t* it) {
+                           return sevp_reduce(h->ws, n, w, b, lookahead, A, lda, Q, ldq, it);
+                         });
 }
 
 int br_reduce_tri_band(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b, int lookahead,
@@ -556,35 +605,10 @@ int br_reduce_tri_band(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b
   ARG(lookahead == 0 || lookahead == 1, 6);
   ARG(A != nullptr && lda >= m, 7);
   DEV(h);
-  Workspace& ws = h->ws;
-  cudaEvent_t e0, e1;
-  BR_CUDA(cudaEventCreate(&e0));
-  BR_CUDA(cudaEventCreate(&e1));
-  const int64_t l0 = launch_count();
-  BR_CUDA(cudaEventRecord(e0, ws.main));
-  int64_t iters = 0;
-  int rc = tri_reduce(ws, m, n, w, b, lookahead, A, lda, &iters);
-  if (rc) {
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    return rc;
-  }
-  BR_CUDA(cudaEventRecord(e1, ws.main));
-  BR_CUDA(cudaEventSynchronize(e1));
-  BR_CUDA(cudaStreamSynchronize(ws.panel));
-  BR_CUDA(cudaGetLastError());
-  float ms = 0;
-  BR_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  if (ws.timing) BR_CHECK(ws_collect_timing(ws));
-  if (stats) {
-    stats->iterations = iters;
-    stats->device_ms = ms;
-    stats->nominal_flops = svd_nominal(m, n);
-    stats->launches = launch_count() - l0;
-  }
-  return 0;
+  return timed_reduction(h->ws, stats, svd_nominal(m, n),
+                         [&](int64_t* it) {
+                           return tri_reduce(h->ws, m, n, w, b, lookahead, A, lda, it);
+                         });
 }
 
 int br_reduce_band(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b, int simultaneous,
@@ -598,35 +622,11 @@ int br_reduce_band(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b, in
   ARG(lookahead == 0 || lookahead == 1, 7);
   ARG(A != nullptr && lda >= m, 8);
   DEV(h);
-  Workspace& ws = h->ws;
-  cudaEvent_t e0, e1;
-  BR_CUDA(cudaEventCreate(&e0));
-  BR_CUDA(cudaEventCreate(&e1));
-  const int64_t l0 = launch_count();
-  BR_CUDA(cudaEventRecord(e0, ws.main));
-  int64_t iters = 0;
-  int rc = band_reduce(ws, m, n, w, b, simultaneous, lookahead, A, lda, &iters);
-  if (rc) {
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    return rc;
-  }
-  BR_CUDA(cudaEventRecord(e1, ws.main));
-  BR_CUDA(cudaEventSynchronize(e1));
-  BR_CUDA(cudaStreamSynchronize(ws.panel));
-  BR_CUDA(cudaGetLastError());
-  float ms = 0;
-  BR_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  if (ws.timing) BR_CHECK(ws_collect_timing(ws));
-  if (stats) {
-    stats->iterations = iters;
-    stats->device_ms = ms;
-    stats->nominal_flops = svd_nominal(m, n);
-    stats->launches = launch_count() - l0;
-  }
-  return 0;
+  return timed_reduction(h->ws, stats, svd_nominal(m, n),
+                         [&](int64_t* it) {
+                           return band_reduce(h->ws, m, n, w, b, simultaneous, lookahead, A,
+                                              lda, it);
+                         });
 }
 
 static int host_stage_in(Workspace& ws, int64_t m, int64_t n, const double* A, int64_t lda,

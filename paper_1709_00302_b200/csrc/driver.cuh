@@ -35,13 +35,23 @@ struct Workspace {
   // events
   std::vector<cudaEvent_t> events;
   size_t event_next = 0;
-  // optional per-class timing
-  bool timing = false;
+  // optional per-class timing (timing >= 1) and per-task event trace (2)
+  int timing = 0;
   struct Timed {
     int cls;
     cudaEvent_t a, b;
     double flops;
+    const char* tag;  // task name ("qr", "left", ...) or nullptr
+    int64_t k;        // iteration's leading column
+    int stream;       // 0 main (T_P role), 1 panel (T_S role)
   };
+  struct TraceRec {
+    char id[40];
+    int stream;
+    double t0_us, t1_us;
+  };
+  std::vector<TraceRec> trace;
+  cudaEvent_t trace_base = nullptr;  // start of the current reduction call
   std::vector<Timed> timed;
   std::vector<cudaEvent_t> tevents;
   size_t tevent_next = 0;
@@ -60,13 +70,17 @@ cudaEvent_t ws_event(Workspace& ws);  // recycled sync-only event
 void ws_events_reset(Workspace& ws);
 // Timing scope: records CUDA events around the enclosed launches on `st`
 // (only when ws.timing), attributing `flops` algorithmic flops to `cls`.
+// With ws.timing == 2 the scope is also a trace record "tag@k" on its stream.
 struct TimeScope {
   Workspace& ws;
   cudaStream_t st;
   int cls;
   double flops;
+  const char* tag;
+  int64_t k;
   cudaEvent_t a = nullptr;
-  TimeScope(Workspace& w, cudaStream_t s, int c, double f);
+  TimeScope(Workspace& w, cudaStream_t s, int c, double f, const char* tag = nullptr,
+            int64_t k = -1);
   ~TimeScope();
 };
 int ws_collect_timing(Workspace& ws);  // after a sync: fold events into t_ms

@@ -77,7 +77,7 @@ int sevp_reduce(Workspace& ws, int64_t n, int64_t w, int64_t b, int lookahead, d
     const int64_t bp = std::min(b, n - k - w), j = n - k - w;
     MatView P(Aat(k + w, k), lda, j, bp);
     MatView Y(Yb[par], jmax, j, bp), T(Tb[par], b, bp, bp), W(Wb[par], jmax, j, bp);
-    TimeScope ts(ws, st, TC_PANEL, panel_flops(j, bp));
+    TimeScope ts(ws, st, TC_PANEL, panel_flops(j, bp), "qr", k);
     return panel_qr(st, sk, ws.pscratch, P, Y, taub[par], T, &W);
   };
 
@@ -105,11 +105,11 @@ int sevp_reduce(Workspace& ws, int64_t n, int64_t w, int64_t b, int lookahead, d
                                         MatView(Aat(k + w, k + bp), lda, j, w - bp), 0.0);
     const int64_t kps_u = gemm_plan_kps(ws.sk_main, MatView(Aat(k + w, k + bp), lda, j, w - bp), Y,
                                         MatView(Zm, b, bp, w - bp), 1.0);
-    auto mid = [&](int64_t c0, int64_t c1) -> int {
+    auto mid = [&](int64_t c0, int64_t c1, const char* tag) -> int {
       if (c0 >= c1) return 0;
       MatView M(Aat(k + w, c0), lda, j, c1 - c0);
       MatView Z(Zm + (c0 - k - bp) * b, b, bp, c1 - c0);
-      TimeScope ts(ws, ws.main, TC_GEMM, 2 * gemm_flops(bp, c1 - c0, j));
+      TimeScope ts(ws, ws.main, TC_GEMM, 2 * gemm_flops(bp, c1 - c0, j), tag, k);
       BR_CHECK(gemm(ws.main, ws.sk_main, Z, W.T(), M, 1.0, 0.0, nullptr, 0, kps_z));
       return gemm(ws.main, ws.sk_main, M, Y, Z, 1.0, 1.0, nullptr, 0, kps_u);
     };
@@ -117,17 +117,17 @@ int sevp_reduce(Workspace& ws, int64_t n, int64_t w, int64_t b, int lookahead, d
     auto xprods = [&]() -> int {
       MatView X1(X1b, jmax, j, bp), X3(X3b, jmax, j, bp), X2(X2b, b, bp, bp);
       {
-        TimeScope ts(ws, ws.main, TC_SYMM, gemm_flops(j, bp, j));
+        TimeScope ts(ws, ws.main, TC_SYMM, gemm_flops(j, bp, j), "xprod1", k);
         BR_CHECK(symm_lower(ws.main, ws.sk_main, X1, A2, W));
       }
-      TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(bp, bp, j) + gemm_flops(j, bp, bp));
+      TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(bp, bp, j) + gemm_flops(j, bp, bp), "xprod3", k);
       BR_CHECK(gemm(ws.main, ws.sk_main, X2, X1.T(), W, 0.5, 0.0));
       return gemm(ws.main, ws.sk_main, X3, Y, X2, 1.0, 1.0, &X1);
     };
-    auto trail = [&](int64_t c0, int64_t c1) -> int {
+    auto trail = [&](int64_t c0, int64_t c1, const char* tag) -> int {
       if (c0 >= c1) return 0;
       MatView X3(X3b, jmax, j, bp);
-      TimeScope ts(ws, ws.main, TC_SYR2K, syr2k_flops(j, bp, c0, c1));
+      TimeScope ts(ws, ws.main, TC_SYR2K, syr2k_flops(j, bp, c0, c1), tag, k);
       return syr2k_lower(ws.main, A2, X3, Y, c0, c1);
     };
     // Q[:, k+w:n] := Q[:, k+w:n] (I + W Y^T) (ref sevp.py:138-144)
@@ -135,7 +135,7 @@ int sevp_reduce(Workspace& ws, int64_t n, int64_t w, int64_t b, int lookahead, d
       if (!Q) return 0;
       MatView Qs(Q + (k + w) * ldq, ldq, n, j);
       MatView Z(ZQ, n, n, bp);
-      TimeScope ts(ws, ws.main, TC_GEMM, 2 * gemm_flops(n, bp, j));
+      TimeScope ts(ws, ws.main, TC_GEMM, 2 * gemm_flops(n, bp, j), "accq", k);
       BR_CHECK(gemm(ws.main, ws.sk_main, Z, Qs, W, 1.0, 0.0));
       return gemm(ws.main, ws.sk_main, Qs, Z, Y.T(), 1.0, 1.0);
     };
@@ -152,24 +152,24 @@ int sevp_reduce(Workspace& ws, int64_t n, int64_t w, int64_t b, int lookahead, d
     if (la && split == 0) {
       // V1 regime (2b <= w): next panel lies inside the mid block
       const int64_t h1 = std::min(k + bp + bpn, k + w);
-      BR_CHECK(mid(k + bp, h1));
+      BR_CHECK(mid(k + bp, h1, "mid-head"));
       BR_CHECK(launch_next_panel());
-      BR_CHECK(mid(h1, k + w));
+      BR_CHECK(mid(h1, k + w, "mid-rest"));
       BR_CHECK(xprods());
-      BR_CHECK(trail(0, j));
+      BR_CHECK(trail(0, j, "trail"));
       BR_CHECK(accq());
     } else if (la) {
       // V2 regime (2b > w): next panel spills `split` columns into A2
-      BR_CHECK(mid(k + bp, k + w));
+      BR_CHECK(mid(k + bp, k + w, "mid"));
       BR_CHECK(xprods());
-      BR_CHECK(trail(0, split));
+      BR_CHECK(trail(0, split, "trail-lead"));
       BR_CHECK(launch_next_panel());
-      BR_CHECK(trail(split, j));
+      BR_CHECK(trail(split, j, "trail-rest"));
       BR_CHECK(accq());
     } else {
-      BR_CHECK(mid(k + bp, k + w));
+      BR_CHECK(mid(k + bp, k + w, "mid"));
       BR_CHECK(xprods());
-      BR_CHECK(trail(0, j));
+      BR_CHECK(trail(0, j, "trail"));
       BR_CHECK(accq());
       if (has_next) BR_CHECK(do_panel(ws.main, ws.sk_main, kn, par ^ 1));
     }
@@ -227,14 +227,14 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
     const int64_t i = m - k;
     MatView P(Aat(k, k), lda, i, bp);
     MatView Y(Yu[par], m, i, bp), T(Tu[par], b, bp, bp), W(Wu[par], m, i, bp);
-    TimeScope ts(ws, st, TC_PANEL, panel_flops(i, bp));
+    TimeScope ts(ws, st, TC_PANEL, panel_flops(i, bp), "qr", k);
     return panel_qr(st, sk, ws.pscratch, P, Y, tauu[par], T, &W);
   };
   auto lq = [&](cudaStream_t st, Scratch& sk, int64_t k, int64_t bq) -> int {
     const int64_t jr = n - k - w;
     MatView P(Aat(k, k + w), lda, jr, bq, true);  // transposed view of the bq x jr rows
     MatView Y(Yv, n, jr, bq), T(Tv, b, bq, bq), W(Wv, n, jr, bq);
-    TimeScope ts(ws, st, TC_PANEL, panel_flops(jr, bq));
+    TimeScope ts(ws, st, TC_PANEL, panel_flops(jr, bq), "lq", k);
     return panel_qr(st, sk, ws.pscratch, P, Y, tauv, T, &W);
   };
   auto handoff = [&]() -> int {  // main -> panel ordering point
@@ -284,12 +284,12 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
       MatView E(Aat(k, k + bp), lda, i, ncE);
       MatView Z(ZL, b, bp, ncE);
       {
-        TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(bp, ncE, i));
+        TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(bp, ncE, i), "zleft", k);
         BR_CHECK(gemm(ws.main, ws.sk_main, Z, Wuv.T(), E, 1.0, 0.0));
       }
       if (bq > 0) {
         {  // rows of the LQ panel first
-          TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(bq, ncE, bp));
+          TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(bq, ncE, bp), "left-lq-rows", k);
           BR_CHECK(gemm(ws.main, ws.sk_main, E.sub(0, 0, bq, ncE), Yuv.sub(0, 0, bq, bp), Z, 1.0,
                         1.0));
         }
@@ -300,7 +300,7 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
           ev_lq = mark_panel();
         }
         {
-          TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, ncE, bp));
+          TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, ncE, bp), "left", k);
           BR_CHECK(gemm(ws.main, ws.sk_main, E.sub(bq, 0, i - bq, ncE), Yuv.sub(bq, 0, i - bq, bp),
                         Z, 1.0, 1.0));
         }
@@ -314,30 +314,30 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
         MatView Zr(ZR, m, i - bq, bq);
         if (i - bq > 0) {
           {
-            TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, bq, jr));
+            TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, bq, jr), "zright", k);
             BR_CHECK(gemm(ws.main, ws.sk_main, Zr, D, Wvv, 1.0, 0.0));
           }
           if (la && !next_issued && splitc > 0) {
             const int64_t sc = std::min(splitc, jr);
             const int64_t kps = gemm_plan_kps(ws.sk_main, D, Zr, Yvv.T(), 1.0);
             {
-              TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, sc, bq));
+              TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, sc, bq), "right-head", k);
               BR_CHECK(gemm(ws.main, ws.sk_main, D.sub(0, 0, i - bq, sc), Zr,
                             Yvv.sub(0, 0, sc, bq).T(), 1.0, 1.0, nullptr, 0, kps));
             }
             BR_CHECK(next_qr_on_panel());
             if (sc < jr) {
-              TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, jr - sc, bq));
+              TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, jr - sc, bq), "right", k);
               BR_CHECK(gemm(ws.main, ws.sk_main, D.sub(0, sc, i - bq, jr - sc), Zr,
                             Yvv.sub(sc, 0, jr - sc, bq).T(), 1.0, 1.0, nullptr, 0, kps));
             }
           } else {
-            TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, jr, bq));
+            TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, jr, bq), "right", k);
             BR_CHECK(gemm(ws.main, ws.sk_main, D, Zr, Yvv.T(), 1.0, 1.0));
           }
         }
       } else {
-        TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i, ncE, bp));
+        TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i, ncE, bp), "left", k);
         BR_CHECK(gemm(ws.main, ws.sk_main, E, Yuv, Z, 1.0, 1.0));
       }
     }
@@ -415,13 +415,13 @@ int band_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int f
     const int64_t i = m - t.k - w;
     MatView P(Aat(t.k + w, t.k), lda, i, t.bp);
     MatView Y(Yu[par], m, i, t.bp), T(Tu[par], b, t.bp, t.bp), W(Wu[par], m, i, t.bp);
-    TimeScope ts(ws, st, TC_PANEL, panel_flops(i, t.bp));
+    TimeScope ts(ws, st, TC_PANEL, panel_flops(i, t.bp), "qr", t.k);
     return panel_qr(st, sk, ws.pscratch, P, Y, tauu[par], T, &W);
   };
   auto lq = [&](cudaStream_t st, Scratch& sk, const It& t, int par) -> int {
     MatView P(Aat(t.k, t.k + w), lda, t.jr, t.bq, true);  // transposed view of the bq x jr rows
     MatView Y(Yv[par], n, t.jr, t.bq), T(Tv[par], b, t.bq, t.bq), W(Wv[par], n, t.jr, t.bq);
-    TimeScope ts(ws, st, TC_PANEL, panel_flops(t.jr, t.bq));
+    TimeScope ts(ws, st, TC_PANEL, panel_flops(t.jr, t.bq), "lq", t.k);
     return panel_qr(st, sk, ws.pscratch, P, Y, tauv[par], T, &W);
   };
   auto panels = [&](cudaStream_t st, Scratch& sk, const It& t, int par) -> int {
@@ -466,28 +466,28 @@ int band_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int f
     // ZL[:, c0:c1] = W_U^T ML[:, c0:c1]
     auto zl = [&](int64_t c0, int64_t c1) -> int {
       if (c0 >= c1) return 0;
-      TimeScope ts(ws, st, TC_GEMM, gemm_flops(t.bp, c1 - c0, i));
+      TimeScope ts(ws, st, TC_GEMM, gemm_flops(t.bp, c1 - c0, i), "zleft", t.k);
       return gemm(st, sk, ZL.sub(0, c0, t.bp, c1 - c0), Wuv.T(), ML.sub(0, c0, i, c1 - c0), 1.0,
                   0.0, nullptr, 0, kz_l);
     };
     // ML[r0:r1, c0:c1] += Y_U[r0:r1] ZL[:, c0:c1]
     auto ul = [&](int64_t r0, int64_t r1, int64_t c0, int64_t c1) -> int {
       if (c0 >= c1 || r0 >= r1) return 0;
-      TimeScope ts(ws, st, TC_GEMM, gemm_flops(r1 - r0, c1 - c0, t.bp));
+      TimeScope ts(ws, st, TC_GEMM, gemm_flops(r1 - r0, c1 - c0, t.bp), "left", t.k);
       return gemm(st, sk, ML.sub(r0, c0, r1 - r0, c1 - c0), Yuv.sub(r0, 0, r1 - r0, t.bp),
                   ZL.sub(0, c0, t.bp, c1 - c0), 1.0, 1.0, nullptr, 0, ku_l);
     };
     // ZR[r0:r1] = MR[r0:r1] W_V
     auto zr = [&](int64_t r0, int64_t r1) -> int {
       if (r0 >= r1 || !jr) return 0;
-      TimeScope ts(ws, st, TC_GEMM, gemm_flops(r1 - r0, bq, jr));
+      TimeScope ts(ws, st, TC_GEMM, gemm_flops(r1 - r0, bq, jr), "zright", t.k);
       return gemm(st, sk, ZR.sub(r0, 0, r1 - r0, bq), MR.sub(r0, 0, r1 - r0, jr), Wvv, 1.0, 0.0,
                   nullptr, 0, kz_r);
     };
     // MR[r0:r1, c0:c1] += ZR[r0:r1] Y_V[c0:c1]^T
     auto ur = [&](int64_t r0, int64_t r1, int64_t c0, int64_t c1) -> int {
       if (r0 >= r1 || c0 >= c1) return 0;
-      TimeScope ts(ws, st, TC_GEMM, gemm_flops(r1 - r0, c1 - c0, bq));
+      TimeScope ts(ws, st, TC_GEMM, gemm_flops(r1 - r0, c1 - c0, bq), "right", t.k);
       return gemm(st, sk, MR.sub(r0, c0, r1 - r0, c1 - c0), ZR.sub(r0, 0, r1 - r0, bq),
                   Yvv.sub(c0, 0, c1 - c0, bq).T(), 1.0, 1.0, nullptr, 0, ku_r);
     };
@@ -495,7 +495,7 @@ int band_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int f
     auto dsim = [&](int64_t r0, int64_t r1, int64_t c0, int64_t c1) -> int {
       if (r0 >= r1 || c0 >= c1) return 0;
       {
-        TimeScope ts(ws, st, TC_GEMM, gemm_flops(r1 - r0, c1 - c0, bq));
+        TimeScope ts(ws, st, TC_GEMM, gemm_flops(r1 - r0, c1 - c0, bq), "dsub", t.k);
         BR_CHECK(gemm(st, sk, MR.sub(c1r + r0, c0, r1 - r0, c1 - c0), X.sub(r0, 0, r1 - r0, bq),
                       Yvv.sub(c0, 0, c1 - c0, bq).T(), 1.0, 1.0, nullptr, 0, ku_x));
       }
@@ -554,7 +554,7 @@ int band_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int f
       // Simultaneous: ZL, ZR from the old D; X = ZR_D + Y_U (ZL_D W_V)
       BR_CHECK(zr(0, nrR));
       {
-        TimeScope ts(ws, st, TC_GEMM, gemm_flops(t.bp, bq, jr) + gemm_flops(i, bq, t.bp));
+        TimeScope ts(ws, st, TC_GEMM, gemm_flops(t.bp, bq, jr) + gemm_flops(i, bq, t.bp), "xprod", t.k);
         BR_CHECK(gemm(st, sk, Tm, ZL.sub(0, b1w, t.bp, jr), Wvv, 1.0, 0.0));
         MatView ZRD = ZR.sub(c1r, 0, i, bq);
         BR_CHECK(gemm(st, sk, X, Yuv, Tm, 1.0, 1.0, &ZRD));

@@ -109,9 +109,9 @@ def reduce_sym_band(A, cfg, groups=None, *, lookahead=None, device=None, stats=N
     band = np.empty((n, n), order="F")
     Q = np.empty((n, n), order="F") if cfg.accumulate_q else None
     st = _lib.BrStats()
-    rc = lib.br_reduce_sym_band_host(
+    rc = _dev.run_traced(h, groups, lambda: lib.br_reduce_sym_band_host(
         h, n, cfg.w, cfg.b, depth, A.ctypes.data, n, band.ctypes.data, n,
-        Q.ctypes.data if Q is not None else None, n, st)
+        Q.ctypes.data if Q is not None else None, n, st))
     _lib.check(rc, "reduce_sym_band")
     variant = {SevpVariant.REFERENCE: "reference", SevpVariant.V1: "v1", SevpVariant.V2: "v2"}[cfg.variant]
     flops, iters = sevp_counted_flops(n, cfg.w, cfg.b, variant, cfg.accumulate_q, cfg.inner_b)

@@ -119,7 +119,8 @@ def reduce_tri_band(A, w, b, groups=None, range_log=None, inner_b=16, *, lookahe
                          iterations=inner.iterations)
     band = np.empty((m, n), order="F")
     st = _lib.BrStats()
-    rc = lib.br_reduce_tri_band_host(h, m, n, w, b, depth, A.ctypes.data, m, band.ctypes.data, m, st)
+    rc = _dev.run_traced(h, groups, lambda: lib.br_reduce_tri_band_host(
+        h, m, n, w, b, depth, A.ctypes.data, m, band.ctypes.data, m, st))
     _lib.check(rc, "reduce_tri_band")
     flops, _ = tri_counted_flops(m, n, w, b, inner_b)
     for key, val in flops.items():
@@ -172,8 +173,8 @@ def reduce_band_svd(A, cfg, groups=None, range_log=None, *, lookahead=None, devi
     h, _ = _dev.ctx(device)
     band = np.empty((m, n), order="F")
     st = _lib.BrStats()
-    rc = lib.br_reduce_band_host(h, m, n, w, b, int(simultaneous), depth, A.ctypes.data, m,
-                                 band.ctypes.data, m, st)
+    rc = _dev.run_traced(h, groups, lambda: lib.br_reduce_band_host(
+        h, m, n, w, b, int(simultaneous), depth, A.ctypes.data, m, band.ctypes.data, m, st))
     _lib.check(rc, "reduce_band_svd")
     if st.iterations == 0:
         flops = {"total": 0}

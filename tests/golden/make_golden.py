@@ -203,7 +203,23 @@ def band_golden():
     print("band.npz", len(d), "arrays")
 
 
+def cli_golden():
+    """SplitMix64 inputs and the text matrix format of the reference CLI."""
+    from bandred import cli
+
+    d = {"gen_general_7_5_9": cli.gen_general(7, 5, 9), "gen_sym_6_3": cli.gen_sym(6, 3),
+         "gen_general_33_17_123456789": cli.gen_general(33, 17, 123456789)}
+    np.savez_compressed(os.path.join(OUT, "cli.npz"), **d)
+    A = cli.gen_general(4, 3, 2) * 1e6 - 5e5
+    A[1, 1] = -0.0
+    A[2, 0] = 1e-300
+    d2 = os.path.join(OUT, "matrix_4x3.txt")
+    cli.save_matrix(d2, A)
+    print("cli.npz", len(d), "arrays; matrix_4x3.txt")
+
+
 if __name__ == "__main__":
     kernels_golden()
     reductions_golden()
     band_golden()
+    cli_golden()
