@@ -44,6 +44,8 @@ CONFIGS = {
     "c3": ("sevp", 8192, 128, 128, "SEVP n=8192 w=b=128, graded spectrum 1e-8, seeds 2/3"),
     "c4": ("tri", 16384, 256, 256, "SVD triband m=n=16384 w=b=256, U(-1,1) seed 4"),
     "c5": ("sevp", 32768, 256, 256, "SEVP n=32768 w=b=256, A=(G+G^T)/2 N(0,1) seed 5"),
+    # not a BASELINE config: the equal-bandwidth band form on c4's matrix
+    "b4": ("band", 16384, 256, 256, "SVD band form m=n=16384 w=b=256 (Simultaneous/V2), c4 input"),
 }
 
 
@@ -108,7 +110,7 @@ class ClockSampler:
 def make_input(cfg):
     import oracle as O  # input generators only (same seeds/distributions as the survey)
 
-    return O.gen_config(cfg)
+    return O.gen_config({"b4": "c4"}.get(cfg, cfg))
 
 
 def cpu_sample(cfg, A, seconds_hint=20.0):
@@ -245,6 +247,8 @@ def run_ours(args, rank, world, local_rank):
         A.copy_(A0)
         if kind == "sevp":
             rc = lib.br_reduce_sym_band(h, n, w, b, la, A.data_ptr(), ld, None, 0, st)
+        elif kind == "band":
+            rc = lib.br_reduce_band(h, n, n, w, b, 1, la, A.data_ptr(), ld, st)
         else:
             rc = lib.br_reduce_tri_band(h, n, n, w, b, la, A.data_ptr(), ld, st)
         _lib.check(rc, "reduce")
@@ -296,6 +300,9 @@ def run_ours(args, rank, world, local_rank):
         if kind == "sevp":
             rc = lib.br_reduce_sym_band_host(h, n, w, b, la, Ah.data_ptr(), n, Bh.data_ptr(), n,
                                              None, 0, st)
+        elif kind == "band":
+            rc = lib.br_reduce_band_host(h, n, n, w, b, 1, la, Ah.data_ptr(), n, Bh.data_ptr(), n,
+                                         st)
         else:
             rc = lib.br_reduce_tri_band_host(h, n, n, w, b, la, Ah.data_ptr(), n, Bh.data_ptr(), n, st)
         _lib.check(rc, "reduce_host")
@@ -321,7 +328,7 @@ def run_ours(args, rank, world, local_rank):
     traffic = load_traffic(args.config)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and kind != "band":
         gf, iters, dt, cores = cpu_sample(args.config, A_host, args.cpu_seconds)
         cpu = {"value": gf, "unit": "GFLOP/s", "cores": cores, "kind": "port",
                "sample": f"first {iters} iterations of the same {n}x{n} reduction "
@@ -468,6 +475,8 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if CONFIGS[args.config][0] == "band" and (world > 1 or args.impl == "reference"):
+        sys.exit("the band-form workload is single-GPU, ours only")
     if args.impl == "reference":
         run_reference(args, rank, world)
     elif world > 1:

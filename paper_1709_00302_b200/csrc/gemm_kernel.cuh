@@ -43,6 +43,70 @@ __device__ __forceinline__ void load_tile(double* dst, const double* src, int64_
   }
 }
 
+// Per-thread cp.async plan for one operand tile, set up once per CTA
+// (CUTLASS-style iterator): each thread owns IT 16-byte chunks at a fixed
+// shared-memory offset whose global pointers advance by a constant per
+// k-tile, so the main loop issues cp.async with no per-chunk index math.
+// The tile is TX (contiguous, 2 doubles per chunk) x TY (stride ld); KX says
+// whether K runs along x (A^T, B) or along y (A, B^T). Bounds of the fixed
+// dimension are folded into per-chunk byte counts once; the K bound is only
+// checked on a partial last k-tile. A second K source (src2 from ksplit on,
+// the [X3 | Y] operand of SYR2K) is switched to at its k-tile boundary.
+template <int TX, int TY, int LD, int NT, bool KX>
+struct TileIter {
+  static constexpr int CX = TX / 2;     // chunks per y line
+  static constexpr int YS = NT / CX;    // y distance between a thread's chunks
+  static constexpr int IT = CX * TY / NT;
+  static_assert(NT % CX == 0 && (CX * TY) % NT == 0, "tile / thread count mismatch");
+  const double* p[IT];
+  uint32_t bytes;  // 2 bits per chunk: 0, 1 (8 B) or 2 (16 B) for the fixed dimension
+  int xt, yt;      // this thread's first chunk (x, y) in the tile
+  int64_t step;    // pointer advance per k-tile
+
+  __device__ __forceinline__ void init(const double* src, int64_t ld, int64_t x0, int64_t xmax,
+                                       int64_t y0, int64_t ymax, int tid) {
+    xt = (tid % CX) * 2;
+    yt = tid / CX;
+    bytes = 0;
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int64_t gx = x0 + xt, gy = y0 + yt + it * YS;
+      p[it] = src + gx + gy * ld;
+      uint32_t bc;
+      if (KX) bc = gy < ymax ? 2u : 0u;  // K (x) bound checked per k-tile
+      else bc = gx < xmax ? (gx + 1 < xmax ? 2u : 1u) : 0u;
+      bytes |= bc << (2 * it);
+    }
+    step = KX ? (int64_t)TX : (int64_t)TY * ld;
+  }
+  // Re-base on a second K source (y-K only): y coordinate k0 of the tile is
+  // row k0 - ksplit of src2.
+  __device__ __forceinline__ void rebase(const double* src2, int64_t ld2, int64_t x0,
+                                         int64_t krow) {
+#pragma unroll
+    for (int it = 0; it < IT; ++it) p[it] = src2 + (x0 + xt) + (krow + yt + it * YS) * ld2;
+    step = (int64_t)TY * ld2;
+  }
+  // Issue the tile at K offset k0 (the pointers are already there) into
+  // shared memory at dst; `kend` bounds K when the tile is partial.
+  __device__ __forceinline__ void load(uint32_t dst, int64_t k0, int64_t kend, bool full) {
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      int nb = (int)((bytes >> (2 * it)) & 3u) * 8;
+      if (!full) {
+        if (KX) {
+          const int64_t kx = k0 + xt;
+          nb = kx >= kend ? 0 : (kx + 1 >= kend ? min(nb, 8) : nb);
+        } else {
+          if (k0 + yt + it * YS >= kend) nb = 0;
+        }
+      }
+      cp_async16_u32(dst + (uint32_t)(((yt + it * YS) * LD + xt) * 8), p[it], nb);
+      p[it] += step;
+    }
+  }
+};
+
 // Which layout a SYMM K-tile uses: 0 = strictly lower (direct, [k][m]),
 // 1 = strictly upper (transposed read of the lower triangle, [m][k]),
 // 2 = straddles the diagonal (element-wise select, [k][m]).
@@ -115,10 +179,41 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB) dgemm_kernel(const GemmArgs
   }
 
   const bool vA = g.vecA != 0, vB = g.vecB != 0;
+  // fast iterators (16-byte aligned operands; a second K source only at a
+  // k-tile boundary)
+  using ItA = TileIter<(AM == A_T ? BK : BM), (AM == A_T ? BM : BK),
+                       (AM == A_T ? LDA_MK : LDA_KM), NT, AM == A_T>;
+  using ItB = TileIter<(BMD == B_N ? BK : BN), (BMD == B_N ? BN : BK),
+                       (BMD == B_N ? LDB_NK : LDB_KN), NT, BMD == B_N>;
+  const bool fastA = AM != A_SYM && vA && (g.ksplitA == INT64_MAX || (g.ksplitA - kbeg) % BK == 0);
+  const bool fastB = vB && (g.ksplitB == INT64_MAX || (g.ksplitB - kbeg) % BK == 0);
+  ItA ia;
+  ItB ib;
+  if (AM != A_SYM && fastA) {
+    if (AM == A_T) ia.init(g.A, g.lda, kbeg, kend, m0, g.M, tid);
+    else if (kbeg >= g.ksplitA) {
+      ia.init(g.A2, g.lda2, m0, g.M, kbeg - g.ksplitA, INT64_MAX, tid);
+    } else {
+      ia.init(g.A, g.lda, m0, g.M, kbeg, INT64_MAX, tid);
+    }
+  }
+  if (fastB) {
+    if (BMD == B_N) ib.init(g.B, g.ldb, kbeg, kend, n0, g.N, tid);
+    else if (kbeg >= g.ksplitB) {
+      ib.init(g.B2, g.ldb2, n0, g.N, kbeg - g.ksplitB, INT64_MAX, tid);
+    } else {
+      ib.init(g.B, g.ldb, n0, g.N, kbeg, INT64_MAX, tid);
+    }
+  }
+  const uint32_t as_u32 = smem_u32(As), bs_u32 = smem_u32(Bs);
   auto load_stage = [&](int s, int64_t k0) {
     double* as = As + s * A_STAGE;
     double* bs = Bs + s * B_STAGE;
-    if (AM == A_N) {
+    const bool full = k0 + BK <= kend;
+    if (AM != A_SYM && fastA) {
+      if (AM == A_N && k0 == g.ksplitA && k0 != kbeg) ia.rebase(g.A2, g.lda2, m0, 0);
+      ia.load(as_u32 + (uint32_t)(s * A_STAGE * 8), k0, kend, full);
+    } else if (AM == A_N) {
       load_tile<BM, BK, LDA_KM, NT>(as, g.A, g.lda, g.A2, g.lda2, g.ksplitA, m0, g.M, k0, kend, vA,
                                     tid);
     } else if (AM == A_T) {
@@ -142,7 +237,10 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB) dgemm_kernel(const GemmArgs
         }
       }
     }
-    if (BMD == B_N) {
+    if (fastB) {
+      if (BMD == B_T && k0 == g.ksplitB && k0 != kbeg) ib.rebase(g.B2, g.ldb2, n0, 0);
+      ib.load(bs_u32 + (uint32_t)(s * B_STAGE * 8), k0, kend, full);
+    } else if (BMD == B_N) {
       load_tile<BK, BN, LDB_NK, NT>(bs, g.B, g.ldb, g.B, g.ldb, INT64_MAX, k0, kend, n0, g.N, vB,
                                     tid);
     } else {
