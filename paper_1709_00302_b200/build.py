@@ -54,6 +54,12 @@ def build(verbose: bool = False, force: bool = False) -> str:
     nvcc = _nvcc()
     os.makedirs(OBJ, exist_ok=True)
     os.makedirs(LIBDIR, exist_ok=True)
+    flags = NVFLAGS + (["-DBR_LEAF_PROF"] if os.environ.get("BR_BUILD_PROF") else [])
+    stamp = os.path.join(OBJ, "flags.txt")  # a flag change rebuilds everything
+    if not os.path.exists(stamp) or open(stamp).read() != " ".join(flags):
+        force = True
+        with open(stamp, "w") as f:
+            f.write(" ".join(flags))
     sources = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     headers = sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + glob.glob(os.path.join(INCLUDE, "*.h"))
     jobs = []
@@ -64,7 +70,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
     def compile_one(job):
         src, obj = job
-        cmd = [nvcc, *NVFLAGS, "-c", src, "-o", obj]
+        cmd = [nvcc, *flags, "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)
         r = subprocess.run(cmd, capture_output=True, text=True)

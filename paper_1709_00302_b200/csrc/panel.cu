@@ -123,8 +123,8 @@ static int launch_leaf(cudaStream_t st, MatView P, MatView Y, double* tau, doubl
   static const bool prof_on = std::getenv("BR_LEAF_PROF") != nullptr;
   if (prof_on) {
     if (!g_leaf_prof) {
-      BR_CUDA(cudaMalloc(&g_leaf_prof, 8 * sizeof(long long)));
-      BR_CUDA(cudaMemset(g_leaf_prof, 0, 8 * sizeof(long long)));
+      BR_CUDA(cudaMalloc(&g_leaf_prof, 16 * sizeof(long long)));
+      BR_CUDA(cudaMemset(g_leaf_prof, 0, 16 * sizeof(long long)));
     }
     a.prof = g_leaf_prof;
   }
@@ -149,12 +149,14 @@ static int launch_leaf(cudaStream_t st, MatView P, MatView Y, double* tau, doubl
 // development aid, not part of include/bandred_b200.h).
 extern "C" int br_leaf_prof_dump() {
   if (!br::g_leaf_prof) return 0;
-  long long h[8];
+  long long h[16];
   if (cudaMemcpy(h, br::g_leaf_prof, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) return 1;
-  const double st = h[7] ? (double)h[7] : 1.0;
+  const double st = h[11] ? (double)h[11] : 1.0, nl = h[12] ? (double)h[12] : 1.0;
   printf("leaf phases (cycles/step over %lld steps): reduce %.0f sync1 %.0f push %.0f cbar %.0f "
-         "scalars %.0f sync2 %.0f update %.0f\n",
-         h[7], h[0] / st, h[1] / st, h[2] / st, h[3] / st, h[4] / st, h[5] / st, h[6] / st);
+         "scalars %.0f sync2 %.0f update %.0f | per leaf (%lld): prologue %.0f tail %.0f "
+         "cbar-exit+Y/R %.0f W %.0f\n",
+         h[11], h[0] / st, h[1] / st, h[2] / st, h[3] / st, h[4] / st, h[5] / st, h[6] / st,
+         h[12], h[7] / nl, h[8] / nl, h[9] / nl, h[10] / nl);
   cudaMemset(br::g_leaf_prof, 0, sizeof(h));
   return 0;
 }

@@ -66,9 +66,12 @@ __device__ __forceinline__ void warp_transpose_reduce(double (&v)[RC], int lane)
 // and p[k][NB-i..NB) are Y_0..Y_{i-1} (explicit unit diagonal, zeros above).
 // The rank-1 update writes p[k][c] from p[k][c+1] and appends the new Y
 // column at NB-1, so the rotation is free and no element ever needs a mask.
-// Slots of the per-step reduced vector:
+// Slots of the per-step reduced vector S_c = x^T p[.][c] (x = current
+// column masked to rows >= i, one multiplier for every slot):
 //   c <  NB - i : x^T P_{i+c}                  (c = 0 gives ||x||^2)
-//   c >= NB - i : Y_{c-NB+i}^T v_{i-1}          (Gram column i-1, for T)
+//   c >= NB - i : x^T Y_y, y = c-NB+i          -> Gram column i for T:
+//       Y_y^T v_i = Y_y[i] + (x^T Y_y - Y_y[i] x0) / (x0 - beta)
+//     (v_i = e_i + (x - x0 e_i)/(x0 - beta); Y_y[i] arrives with row i).
 // Per step: FMAs on registers, a warp transpose-reduction (shuffles), the
 // per-warp partials through shared memory, then warp w pushes its slots with
 // st.async into every CTA of the cluster, completing bytes on that CTA's
@@ -106,6 +109,19 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
   const int64_t base = (int64_t)rank * ROWS;
   const bool owner_cta = (base == 0);  // row i < nb <= 32 always lives in CTA 0
 
+#ifdef BR_LEAF_PROF  // phase counters: build with BR_BUILD_PROF=1, run with BR_LEAF_PROF=1
+  const bool pr = a.prof != nullptr && rank == 0 && tid == 0;
+  long long tp[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long tc = pr ? clock64() : 0;
+#define BR_PHASE(k)                 \
+  if (pr) {                         \
+    const long long t_ = clock64(); \
+    tp[k] += t_ - tc;               \
+    tc = t_;                        \
+  }
+#else
+#define BR_PHASE(k)
+#endif
   int64_t gr[R];
   double p[R][NB];
 #pragma unroll
@@ -121,24 +137,14 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   cluster_sync_all();  // mbarriers initialized cluster-wide before any st.async
-
-  const bool pr = a.prof != nullptr && rank == 0 && tid == 0;
-  long long tp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  long long tc = pr ? clock64() : 0;
-#define BR_PHASE(k)                 \
-  if (pr) {                         \
-    const long long t_ = clock64(); \
-    tp[k] += t_ - tc;               \
-    tc = t_;                        \
-  }
-  for (int i = 0; i <= nb; ++i) {
-    const bool hh = i < nb;  // i == nb: final round, Gram column nb-1 only
+  BR_PHASE(7);
+  for (int i = 0; i < nb; ++i) {
     const int buf = i & 1;
     const int g0 = NB - i;  // first Gram slot
-    if (tid == 0) mbar_arrive_expect_tx(&mbar[buf], ncta * NB * 8 + (hh ? NB * 8 : 0));
+    if (tid == 0) mbar_arrive_expect_tx(&mbar[buf], ncta * NB * 8 + NB * 8);
 #pragma unroll
     for (int k = 0; k < R; ++k)
-      if (hh && gr[k] == i) {
+      if (gr[k] == i) {
 #pragma unroll
         for (int c = 0; c < NB; c += 2)
           *reinterpret_cast<double2*>(&rowi[c]) = make_double2(p[k][c], p[k][c + 1]);
@@ -149,7 +155,7 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
 #pragma unroll
     for (int k = 0; k < R; ++k) {
       xk[k] = (gr[k] >= i) ? p[k][0] : 0.0;
-      if (hh && gr[k] < i) Rrow[gr[k]][i] = p[k][0];
+      if (gr[k] < i) Rrow[gr[k]][i] = p[k][0];
     }
     // ---- per-thread partials, transpose-reduced per warp ----
 #pragma unroll
@@ -160,7 +166,7 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
         const int c = ch * RC + cc;
         double s = 0.0;
 #pragma unroll
-        for (int k = 0; k < R; ++k) s = fma((c < g0) ? xk[k] : p[k][NB - 1], p[k][c], s);
+        for (int k = 0; k < R; ++k) s = fma(xk[k], p[k][c], s);
         v[cc] = s;
       }
       warp_transpose_reduce<RC>(v, lane);
@@ -173,19 +179,27 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
     if (warp < NPW) {
       constexpr int NP = SPW / 2;  // slot pairs per warp
       const int ntask = NP * (int)ncta;
-      const bool push_row = hh && owner_cta;
+      const bool push_row = owner_cta;
       for (int t0 = 0; t0 < ntask; t0 += 32) {
         const int t = t0 + lane;
         if (t < ntask) {
           const int pp = t / (int)ncta;
           const uint32_t q = (uint32_t)(t % (int)ncta);
           const int c = warp * SPW + 2 * pp;
-          double s0 = 0.0, s1 = 0.0;
+          double u0[LW], u1[LW];  // fixed pairwise tree over the warps
 #pragma unroll
           for (int w = 0; w < LW; ++w) {
-            s0 += wred[w][c];
-            s1 += wred[w][c + 1];
+            u0[w] = wred[w][c];
+            u1[w] = wred[w][c + 1];
           }
+#pragma unroll
+          for (int h = LW / 2; h >= 1; h >>= 1)
+#pragma unroll
+            for (int w = 0; w < h; ++w) {
+              u0[w] += u0[w + h];
+              u1[w] += u1[w + h];
+            }
+          const double s0 = u0[0], s1 = u1[0];
           const uint32_t rm = map_cluster(&mbar[buf], q);
           st_async_v2(map_cluster(&recv[buf][rank][c], q), s0, s1, rm);
           if (push_row) st_async_v2(map_cluster(&recv_row[buf][c], q), rowi[c], rowi[c + 1], rm);
@@ -199,26 +213,24 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
     // ---- every warp: the same scalars from the same received vectors ----
     double rinv = 0.0;
     {
-      double g0s = 0.0, g1s = 0.0;
       const double pic = (lane < NB) ? recv_row[buf][lane] : 0.0;
-      if (lane < NB) {
-        uint32_t q = 0;
-        for (; q + 1 < ncta; q += 2) {
-          g0s += recv[buf][q][lane];
-          g1s += recv[buf][q + 1][lane];
-        }
-        if (q < ncta) g0s += recv[buf][q][lane];
-      }
-      const double g = g0s + g1s;
-      if (warp == 0 && i > 0 && lane >= g0 && lane < NB - 1) G[lane - g0][i - 1] = g;
-      if (hh) {
+      double gq[LEAF_MAXC];  // fixed pairwise tree over the (power-of-two) CTAs
+#pragma unroll
+      for (int q = 0; q < LEAF_MAXC; ++q)
+        gq[q] = (lane < NB && q < (int)ncta) ? recv[buf][q][lane] : 0.0;
+#pragma unroll
+      for (int h = LEAF_MAXC / 2; h >= 1; h >>= 1)
+#pragma unroll
+        for (int q = 0; q < h; ++q) gq[q] += gq[q + h];
+      const double g = gq[0];
+      {
         const double nrm2 = __shfl_sync(0xffffffffu, g, 0);
         const double x0 = __shfl_sync(0xffffffffu, pic, 0);
-        // beta from the correctly rounded sqrt (it is the R diagonal); the
-        // two reciprocals on the critical path use rsqrt / rcp (~1 ulp)
+        // ||x|| and 1/||x|| from one rsqrt; 1/(x0 - beta) by rcp (~1 ulp
+        // each, far inside the parity tolerance) to keep the chain short
         double beta = 0.0, rb = 0.0;
         if (nrm2 != 0.0) {
-          const double nrm = sqrt(nrm2), rs = rsqrt(nrm2);
+          const double rs = rsqrt(nrm2), nrm = nrm2 * rs;
           beta = (x0 < 0.0) ? nrm : -nrm;
           rb = (x0 < 0.0) ? rs : -rs;
           rinv = __drcp_rn(x0 - beta);
@@ -230,11 +242,12 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
           scal[i][1] = beta;
           scal[i][2] = rinv;
         }
+        if (warp == 0 && lane >= g0 && lane < NB) G[lane - g0][i] = fma(fma(-pic, x0, g), rinv, pic);
         __syncwarp();
       }
     }
     BR_PHASE(4);
-    if (hh) {
+    {
       double al[NB];
 #pragma unroll
       for (int c = 0; c < NB; c += 2) {
@@ -252,18 +265,19 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
     }
     BR_PHASE(6);
   }
-#undef BR_PHASE
-  if (pr) {
-    for (int k = 0; k < 7; ++k) atomicAdd((unsigned long long*)&a.prof[k], (unsigned long long)tp[k]);
-    atomicAdd((unsigned long long*)&a.prof[7], (unsigned long long)(nb + 1));
-  }
 
-  // ---- Y from the register tail: column c at p[k][NB - nb + c] ----
+  // ---- Y from the register tail (column c at p[k][NB - nb + c]): to shared
+  // memory for W and straight to global ----
   if (nb == NB) {
 #pragma unroll
-    for (int k = 0; k < R; ++k)
+    for (int k = 0; k < R; ++k) {
+      const bool ok = gr[k] < a.L;
 #pragma unroll
-      for (int c = 0; c < NB; ++c) Ys[c * ROWS + tid + k * LT] = p[k][c];
+      for (int c = 0; c < NB; ++c) {
+        Ys[c * ROWS + tid + k * LT] = p[k][c];
+        if (ok) a.Y[gr[k] + (int64_t)c * a.ldy] = p[k][c];
+      }
+    }
   } else {
 #pragma unroll
     for (int k = 0; k < R; ++k) {
@@ -274,8 +288,18 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
 #pragma unroll
         for (int m = 0; m < NB; ++m)
           if (m == src) y = p[k][m];
-        Ys[c * ROWS + tid + k * LT] = (c < nb) ? y : 0.0;
+        y = (c < nb) ? y : 0.0;
+        Ys[c * ROWS + tid + k * LT] = y;
+        if (c < nb && gr[k] < a.L) a.Y[gr[k] + (int64_t)c * a.ldy] = y;
       }
+    }
+  }
+  // ---- R rows (owner CTA) ----
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    if (gr[k] < nb) {
+      const int r = (int)gr[k];
+      for (int c = r; c < nb; ++c) *a.P.at(r, c) = (c == r) ? scal[r][1] : Rrow[r][c];
     }
   }
   // ---- tau = (beta - x0) / beta (ref kernels.py:109) ----
@@ -284,66 +308,82 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
     scal[tid][0] = (be != 0.0) ? (be - scal[tid][0]) / be : 0.0;
   }
   __syncthreads();
-  // ---- T by the reference recurrence (ref kernels.py:152-162), one row per lane ----
+  // ---- T by the reference recurrence (ref kernels.py:152-162): lane r owns
+  // row r in registers, T[r][i] = -tau_i sum_{c<i} T[r][c] G[c][i]
+  // (T[r][c] = 0 for c < r) ----
   if (warp == 0 && lane < NB) {
     const int r = lane;
-    for (int c = 0; c < NB; ++c) Ts[r][c] = 0.0;
-    if (r < nb) {
-      Ts[r][r] = -scal[r][0];
-      for (int i = r + 1; i < nb; ++i) {
-        double s0 = 0.0, s1 = 0.0;
-        int c = r;
-        for (; c + 1 < i; c += 2) {
-          s0 = fma(Ts[r][c], G[c][i], s0);
-          s1 = fma(Ts[r][c + 1], G[c + 1][i], s1);
-        }
-        if (c < i) s0 = fma(Ts[r][c], G[c][i], s0);
-        Ts[r][i] = -scal[i][0] * (s0 + s1);
+    double tr[NB];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) tr[c] = (c == r && r < nb) ? -scal[c][0] : 0.0;
+#pragma unroll
+    for (int i = 1; i < NB; ++i) {
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int c = 0; c + 1 < i; c += 2) {
+        s0 = fma(tr[c], G[c][i], s0);
+        s1 = fma(tr[c + 1], G[c + 1][i], s1);
       }
+      if (i & 1) s0 = fma(tr[i - 1], G[i - 1][i], s0);
+      if (i > r && i < nb) tr[i] = -scal[i][0] * (s0 + s1);
     }
+#pragma unroll
+    for (int c = 0; c < NB; ++c) Ts[r][c] = tr[c];
   }
   __syncthreads();
-  cluster_sync_all();  // no remote traffic is in flight when any CTA exits
-
-  // ---- outputs: Y, R ----
-#pragma unroll
-  for (int k = 0; k < R; ++k) {
-    if (gr[k] >= a.L) continue;
-    const int lr = tid + k * LT;
-    for (int c = 0; c < nb; ++c) a.Y[gr[k] + (int64_t)c * a.ldy] = Ys[c * ROWS + lr];
-    if (gr[k] < nb) {
-      const int r = (int)gr[k];
-      for (int c = r; c < nb; ++c) *a.P.at(r, c) = (c == r) ? scal[r][1] : Rrow[r][c];
-    }
-  }
-  // ---- W = Y T on the tensor cores: each warp 8-row slabs x NB columns ----
+  BR_PHASE(8);
+  BR_PHASE(9);
+  // ---- W = Y T on the tensor cores: each warp 4 independent 8-row slabs
+  // at a time x NB columns ----
   if (a.W) {
-    for (int r0 = warp * 8; r0 < ROWS; r0 += LW * 8) {
-      if (base + r0 >= a.L) break;
-      double acc[NB / 8][2];
+    const int gq = lane >> 2, tq = lane & 3;
+    constexpr int U = 4;
+    for (int rb = warp * 8; rb < ROWS; rb += LW * 8 * U) {
+      if (base + rb >= a.L) break;
+      double acc[U][NB / 8][2];
 #pragma unroll
-      for (int n = 0; n < NB / 8; ++n) acc[n][0] = acc[n][1] = 0.0;
-      const int gq = lane >> 2, tq = lane & 3;
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int n = 0; n < NB / 8; ++n) acc[u][n][0] = acc[u][n][1] = 0.0;
 #pragma unroll
       for (int k0 = 0; k0 < NB; k0 += 4) {
-        const double av = Ys[(k0 + tq) * ROWS + r0 + gq];  // A = Y (8 x 4)
+        double bt[NB / 8];
 #pragma unroll
         for (int n = 0; n < NB / 8; ++n)  // B = T, or T^T for the block-reflector form Y T^T
-          dmma884(acc[n][0], acc[n][1], av,
-                  a.wt ? Ts[n * 8 + gq][k0 + tq] : Ts[k0 + tq][n * 8 + gq]);
+          bt[n] = a.wt ? Ts[n * 8 + gq][k0 + tq] : Ts[k0 + tq][n * 8 + gq];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int r0 = rb + u * LW * 8;
+          const double av = (r0 < ROWS) ? Ys[(k0 + tq) * ROWS + r0 + gq] : 0.0;  // A = Y (8 x 4)
+#pragma unroll
+          for (int n = 0; n < NB / 8; ++n) dmma884(acc[u][n][0], acc[u][n][1], av, bt[n]);
+        }
       }
-      const int64_t row = base + r0 + gq;
-      if (row < a.L) {
 #pragma unroll
-        for (int n = 0; n < NB / 8; ++n)
+      for (int u = 0; u < U; ++u) {
+        const int r0 = rb + u * LW * 8;
+        const int64_t row = base + r0 + gq;
+        if (r0 < ROWS && row < a.L) {
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int c = n * 8 + 2 * tq + h;
-            if (c < nb) a.W[row + (int64_t)c * a.ldw] = acc[n][h];
-          }
+          for (int n = 0; n < NB / 8; ++n)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int c = n * 8 + 2 * tq + h;
+              if (c < nb) a.W[row + (int64_t)c * a.ldw] = acc[u][n][h];
+            }
+        }
       }
     }
   }
+  BR_PHASE(10);
+#undef BR_PHASE
+#ifdef BR_LEAF_PROF
+  if (pr) {
+    for (int k = 0; k < 11; ++k) atomicAdd((unsigned long long*)&a.prof[k], (unsigned long long)tp[k]);
+    atomicAdd((unsigned long long*)&a.prof[11], (unsigned long long)(nb + 1));
+    atomicAdd((unsigned long long*)&a.prof[12], 1ull);
+  }
+#endif
   if (rank == 0) {
     if (tid < nb) a.tau[tid] = scal[tid][0];
     if (a.T)
@@ -352,6 +392,7 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
         a.T[r + (int64_t)c * a.ldt] = Ts[r][c];
       }
   }
+  cluster_sync_all();  // no remote traffic is in flight when any CTA exits
 }
 
 }  // namespace br
