@@ -1,6 +1,7 @@
 // Context, workspace, elementwise kernels and the C ABI (include/bandred_b200.h).
 #include <algorithm>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 #include <atomic>
 #include <new>
@@ -281,7 +282,10 @@ int br_create(int device, br_handle_t* out) {
   int lo = 0, hi = 0;
   BR_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   BR_CUDA(cudaStreamCreateWithPriority(&h->ws.own_main, cudaStreamNonBlocking, lo));
-  BR_CUDA(cudaStreamCreateWithPriority(&h->ws.own_panel, cudaStreamNonBlocking, hi));
+  // BR_PANEL_PRIO=lo (tuning aid): panel stream at the main stream's priority
+  const char* pp = std::getenv("BR_PANEL_PRIO");
+  BR_CUDA(cudaStreamCreateWithPriority(&h->ws.own_panel, cudaStreamNonBlocking,
+                                       (pp && pp[0] == 'l') ? lo : hi));
   h->ws.main = h->ws.own_main;
   h->ws.panel = h->ws.own_panel;
   *out = h;

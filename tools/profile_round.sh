@@ -1,6 +1,6 @@
 #!/bin/bash
 # Round profiling pass (run under gpurun). Each ncu command follows a plain run
-# of the same command that exited 0.
+# of the same command that exited 0. Outputs land in gpurun_out/.
 set -x
 mkdir -p gpurun_out
 CMD="python bench.py --config c4 --steps 1 --warmup 1 --no-cpu --e2e-steps 1"
@@ -11,6 +11,8 @@ CMD1="python bench.py --config c1 --steps 1 --warmup 1 --no-cpu --e2e-steps 1"
 $CMD1 > gpurun_out/prof_plain1.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv \
     --log-file gpurun_out/launches_c1.csv $CMD1 > gpurun_out/ncu_launch1.log 2>&1
+# dominant kernels at c4 iteration-0 shapes: rank-b update (E += Y_U Z_L) and
+# the split-K reduction (Z_L = W_U^T E)
 CMD2="python tools/gemm_bench.py left 16384 16128 256 1"
 $CMD2 > /dev/null 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:dgemm -c 2 \
