@@ -163,54 +163,142 @@ extern "C" int br_leaf_prof_dump() {
 
 namespace br {
 
-// T from the Gram matrix, blocked: diagonal 32x32 blocks by the reference
-// recurrence, then T[0:s, s:e] = T[0:s,0:s] * G[0:s, s:e] * T[s:e, s:e].
-__global__ void t_diag_kernel(const double* G, int64_t ldg, const double* tau, int64_t b,
-                              double* T, int64_t ldt) {
-  // one CTA (one warp) per 32-column diagonal block, staged in shared memory;
-  // lane r computes row r of the block (rows are independent in the
-  // recurrence T[r][i] = -tau_i sum_{c=r}^{i-1} T[r][c] G[c][i])
-  __shared__ double Gs[32][33];
-  __shared__ double Tr[32][33];
-  __shared__ double ts[32];
-  const int lane = threadIdx.x;
-  const int64_t s = (int64_t)blockIdx.x * 32;
-  const int nb = (int)std::min<int64_t>(32, b - s);
-  for (int c = 0; c < nb; ++c)
-    if (lane < nb) Gs[lane][c] = G[(s + lane) + (s + c) * ldg];
-  if (lane < nb) ts[lane] = tau[s + lane];
-  __syncwarp();
-  if (lane < nb) {
-    const int r = lane;
-    for (int c = 0; c < 32; ++c) Tr[r][c] = 0.0;
-    Tr[r][r] = -ts[r];
-    for (int i = r + 1; i < nb; ++i) {
-      double s0 = 0.0, s1 = 0.0;
-      int c = r;
-      for (; c + 1 < i; c += 2) {
-        s0 = fma(Tr[r][c], Gs[c][i], s0);
-        s1 = fma(Tr[r][c + 1], Gs[c + 1][i], s1);
-      }
-      if (c < i) s0 = fma(Tr[r][c], Gs[c][i], s0);
-      Tr[r][i] = -ts[i] * (s0 + s1);
+// T (b x b, upper triangular, T = -T_larft) from the Gram matrix G = Y^T Y and
+// tau, by the reference recurrence T[r][i] = -tau_i sum_{c<i} T[r][c] G[c][i]
+// (ref kernels.py:152-162), blocked by 32 columns:
+//   T[q, e] = T[q, q:e] G[q:e, e] T_ee            (block rows q < e),
+// the blocked form of the same recurrence. CTA q owns row block q of T, so a
+// CTA only ever reads its own earlier results: its warps first form the
+// diagonal blocks T_ee (e >= q) in parallel (lane r = row r, registers),
+// then it walks the later block columns e in order. One launch replaces the
+// diagonal kernel and the 2 (nblk-1) small GEMMs of the GEMM formulation.
+constexpr int TAB = 32;      // block size
+constexpr int TAB_MAXB = 256;  // widest panel handled (smem: row block + diagonal blocks + G stage)
+static size_t t_assemble_smem(int b) {
+  const int nblk = (b + TAB - 1) / TAB;
+  return sizeof(double) * ((size_t)TAB * b + (size_t)nblk * TAB * (TAB + 1) + (size_t)b * TAB +
+                           TAB * (TAB + 1));
+}
+
+__global__ void __launch_bounds__(256) t_assemble_kernel(const double* __restrict__ G, int64_t ldg,
+                                                         const double* __restrict__ tau, int b,
+                                                         double* __restrict__ T, int64_t ldt) {
+  extern __shared__ double sm[];
+  const int nblk = (b + TAB - 1) / TAB;
+  const int q = blockIdx.x, q0 = q * TAB;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* Trow = sm;                       // [TAB][b]   row block q of T
+  double* Td = Trow + TAB * b;             // [nblk][TAB][TAB+1] diagonal blocks
+  double* Gs = Td + nblk * TAB * (TAB + 1);  // [b][TAB]  G[q0:s, e-block]
+  double* Xs = Gs + b * TAB;               // [TAB][TAB+1]
+  for (int i = tid; i < TAB * b; i += 256) Trow[i] = 0.0;
+  // diagonal G blocks e >= q into Td (overwritten in place by T_ee below)
+  for (int e = q; e < nblk; ++e) {
+    const int e0 = e * TAB;
+    for (int i = tid; i < TAB * TAB; i += 256) {
+      const int r = i % TAB, c = i / TAB;
+      Td[(e * TAB + r) * (TAB + 1) + c] =
+          (e0 + r < b && e0 + c < b) ? G[(e0 + r) + (int64_t)(e0 + c) * ldg] : 0.0;
     }
   }
-  __syncwarp();
-  for (int c = 0; c < nb; ++c)
-    if (lane < nb) T[(s + lane) + (s + c) * ldt] = Tr[lane][c];
+  __syncthreads();
+  for (int e = q + warp; e < nblk; e += 8) {  // T_ee: lane r = row r
+    const int e0 = e * TAB, r = lane;
+    double* D = Td + e * TAB * (TAB + 1);
+    double tr[TAB];
+#pragma unroll
+    for (int c = 0; c < TAB; ++c) tr[c] = (c == r && e0 + r < b) ? -tau[e0 + r] : 0.0;
+#pragma unroll
+    for (int i = 1; i < TAB; ++i) {
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int c = 0; c + 1 < i; c += 2) {
+        s0 = fma(tr[c], D[c * (TAB + 1) + i], s0);
+        s1 = fma(tr[c + 1], D[(c + 1) * (TAB + 1) + i], s1);
+      }
+      if (i & 1) s0 = fma(tr[i - 1], D[(i - 1) * (TAB + 1) + i], s0);
+      if (i > r && e0 + i < b) tr[i] = -tau[e0 + i] * (s0 + s1);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < TAB; ++c) D[r * (TAB + 1) + c] = tr[c];
+  }
+  __syncthreads();
+  for (int i = tid; i < TAB * TAB; i += 256) {
+    const int r = i / TAB, c = i % TAB;
+    if (q0 + c < b) Trow[r * b + q0 + c] = Td[(q * TAB + r) * (TAB + 1) + c];
+  }
+  __syncthreads();
+  const int cc = tid % TAB, r0 = (tid / TAB) * 4;  // 4 rows x 1 column per thread
+  for (int e = q + 1; e < nblk; ++e) {
+    const int e0 = e * TAB, kk = e0 - q0;  // K range [q0, e0)
+    for (int i = tid; i < kk * TAB; i += 256) {
+      const int k = i / TAB, c = i % TAB;
+      Gs[k * TAB + c] = (e0 + c < b) ? G[(q0 + k) + (int64_t)(e0 + c) * ldg] : 0.0;
+    }
+    __syncthreads();
+    double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;
+    for (int k = 0; k < kk; ++k) {
+      const double gv = Gs[k * TAB + cc];
+      x0 = fma(Trow[(r0 + 0) * b + q0 + k], gv, x0);
+      x1 = fma(Trow[(r0 + 1) * b + q0 + k], gv, x1);
+      x2 = fma(Trow[(r0 + 2) * b + q0 + k], gv, x2);
+      x3 = fma(Trow[(r0 + 3) * b + q0 + k], gv, x3);
+    }
+    Xs[(r0 + 0) * (TAB + 1) + cc] = x0;
+    Xs[(r0 + 1) * (TAB + 1) + cc] = x1;
+    Xs[(r0 + 2) * (TAB + 1) + cc] = x2;
+    Xs[(r0 + 3) * (TAB + 1) + cc] = x3;
+    __syncthreads();
+    const double* D = Td + e * TAB * (TAB + 1);
+    double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
+#pragma unroll 8
+    for (int k = 0; k < TAB; ++k) {
+      const double dv = D[k * (TAB + 1) + cc];
+      y0 = fma(Xs[(r0 + 0) * (TAB + 1) + k], dv, y0);
+      y1 = fma(Xs[(r0 + 1) * (TAB + 1) + k], dv, y1);
+      y2 = fma(Xs[(r0 + 2) * (TAB + 1) + k], dv, y2);
+      y3 = fma(Xs[(r0 + 3) * (TAB + 1) + k], dv, y3);
+    }
+    if (e0 + cc < b) {
+      Trow[(r0 + 0) * b + e0 + cc] = y0;
+      Trow[(r0 + 1) * b + e0 + cc] = y1;
+      Trow[(r0 + 2) * b + e0 + cc] = y2;
+      Trow[(r0 + 3) * b + e0 + cc] = y3;
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < TAB * b; i += 256) {
+    const int r = i % TAB, c = i / TAB;
+    if (q0 + r < b) T[(q0 + r) + (int64_t)c * ldt] = Trow[r * b + c];
+  }
 }
 
 int t_from_gram(cudaStream_t st, const double* G, int64_t ldg, const double* tau, int64_t b,
                 double* T, int64_t ldt) {
-  // caller zero-fills T (the blocks above the diagonal are filled later)
-  const int nblk = (int)cdiv(b, 32);
+  if (b < 1 || b > TAB_MAXB) {
+    set_error("t_from_gram: b = %lld outside [1, %d]", (long long)b, TAB_MAXB);
+    return -1;
+  }
+  const int nblk = (int)cdiv(b, TAB);
+  const size_t smem = t_assemble_smem((int)b);
+  static int attr_dev_mask = 0;
+  int dev = 0;
+  BR_CUDA(cudaGetDevice(&dev));
+  if (!(attr_dev_mask & (1 << dev))) {
+    BR_CUDA(cudaFuncSetAttribute(t_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)t_assemble_smem(TAB_MAXB)));
+    attr_dev_mask |= 1 << dev;
+  }
   count_launch();
-  t_diag_kernel<<<nblk, 32, 0, st>>>(G, ldg, tau, b, T, ldt);
+  t_assemble_kernel<<<nblk, 256, smem, st>>>(G, ldg, tau, (int)b, T, ldt);
   BR_CUDA(cudaGetLastError());
   return 0;
 }
 
-int64_t panel_scratch_doubles(int64_t b) { return b * b + LEAF_NB * LEAF_NB + 2 * LEAF_NB * b; }
+int64_t panel_scratch_doubles(int64_t b) {
+  return b * b + LEAF_NB * LEAF_NB + 2 * LEAF_NB * b + (b > TAB_MAXB ? b * TAB_MAXB : 0);
+}
 
 int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView Y, double* tau,
              MatView T, MatView* W) {
@@ -268,15 +356,23 @@ int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView 
       BR_CHECK(gemm(st, ws, rest, leafY, Z2s, 1.0, 1.0));
     }
   }
-  // full T: Gram, blocked recurrence
+  // full T: Gram, then the blocked recurrence in one kernel (T is written whole,
+  // zeros below the diagonal)
   BR_CHECK(gemm(st, ws, G, Y.T(), Y, 1.0, 0.0));
-  BR_CHECK(t_from_gram(st, G.p, G.ld, tau, b, T.p, T.ld));
-  for (int64_t s = 32; s < b; s += 32) {
-    const int64_t e = std::min<int64_t>(s + 32, b);
-    // T[0:s, s:e] = T[0:s,0:s] * (G[0:s, s:e] * T[s:e, s:e])
-    MatView tmp(Z.p, s, s, e - s);  // s x (e-s) scratch (fits: 32*b >= s*32)
-    BR_CHECK(gemm(st, ws, tmp, G.sub(0, s, s, e - s), T.sub(s, s, e - s, e - s), 1.0, 0.0));
-    BR_CHECK(gemm(st, ws, T.sub(0, s, s, e - s), T.sub(0, 0, s, s), tmp, 1.0, 0.0));
+  if (b <= TAB_MAXB) {
+    BR_CHECK(t_from_gram(st, G.p, G.ld, tau, b, T.p, T.ld));
+  } else {
+    // wider than one assembly kernel: diagonal super-blocks by the kernel,
+    // T[0:s, s:e] = T[0:s,0:s] (G[0:s,s:e] T[s:e,s:e]) by GEMMs
+    double* tmpp = scratch + b * b + LEAF_NB * LEAF_NB + 2 * LEAF_NB * b;
+    for (int64_t s = 0; s < b; s += TAB_MAXB) {
+      const int64_t e = std::min<int64_t>(s + TAB_MAXB, b);
+      BR_CHECK(t_from_gram(st, G.p + s + s * G.ld, G.ld, tau + s, e - s, T.p + s + s * T.ld, T.ld));
+      if (s == 0) continue;
+      MatView tmp(tmpp, s, s, e - s);
+      BR_CHECK(gemm(st, ws, tmp, G.sub(0, s, s, e - s), T.sub(s, s, e - s, e - s), 1.0, 0.0));
+      BR_CHECK(gemm(st, ws, T.sub(0, s, s, e - s), T.sub(0, 0, s, s), tmp, 1.0, 0.0));
+    }
   }
   if (W) BR_CHECK(gemm(st, ws, *W, Y, T, 1.0, 0.0));
   return 0;
