@@ -42,6 +42,14 @@ void devbuf_free(DevBuf& b) {
   b.cap = 0;
 }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("BR_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 cudaEvent_t ws_event(Workspace& ws) {
   if (ws.event_next == ws.events.size()) {
     cudaEvent_t e;

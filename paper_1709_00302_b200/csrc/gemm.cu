@@ -15,6 +15,8 @@ __global__ void splitk_reduce_kernel(int64_t M, int64_t N, int S, const double* 
                                      double alpha, double beta, const double* Cin, int64_t ldcin,
                                      double* C, int64_t ldc) {
   const int64_t total = M * N;
+  pdl_wait();
+  pdl_trigger();
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = idx % M, c = idx / M;
@@ -112,9 +114,8 @@ static int run_gemm(int am, cudaStream_t st, Scratch& ws, GemmArgs g, bool btran
     const int64_t total = g.M * g.N;
     int blocks = (int)std::min<int64_t>(cdiv(total, 256), 4096);
     count_launch();
-    splitk_reduce_kernel<<<blocks, 256, 0, st>>>(g.M, g.N, 0, nullptr, g.alpha, g.beta, g.Cin,
-                                                 g.ldcin, g.C, g.ldc);
-    BR_CUDA(cudaGetLastError());
+    BR_CUDA(launch_pdl(splitk_reduce_kernel, dim3(blocks), dim3(256), 0, st, g.M, g.N, 0,
+                       (const double*)nullptr, g.alpha, g.beta, g.Cin, g.ldcin, g.C, g.ldc));
     return 0;
   }
   const int cfg = pick_cfg(am, g);
@@ -138,9 +139,8 @@ static int run_gemm(int am, cudaStream_t st, Scratch& ws, GemmArgs g, bool btran
     const int64_t total = g.M * g.N;
     int blocks = (int)std::min<int64_t>(cdiv(total, 256), (int64_t)sms * 8);
     count_launch();
-    splitk_reduce_kernel<<<blocks, 256, 0, st>>>(g.M, g.N, (int)S, ws.p, g.alpha, g.beta, g.Cin,
-                                                 g.ldcin, g.C, g.ldc);
-    BR_CUDA(cudaGetLastError());
+    BR_CUDA(launch_pdl(splitk_reduce_kernel, dim3(blocks), dim3(256), 0, st, g.M, g.N, (int)S,
+                       (const double*)ws.p, g.alpha, g.beta, g.Cin, g.ldcin, g.C, g.ldc));
   }
   return 0;
 }

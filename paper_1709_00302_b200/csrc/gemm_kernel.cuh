@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB) dgemm_kernel(const GemmArgs
     kend = min(g.K, kbeg + g.k_per_split);
   }
   const int64_t nmax = (EPI == EPI_LOWER) ? g.c1 : g.N;
+  pdl_wait();  // inputs written by the previous kernel in the stream
 
   // Accumulators start from beta*C when alpha == 1 (every rank-b update and
   // the SYR2K): the C tile is fetched in one batch before the main loop
@@ -298,6 +299,7 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB) dgemm_kernel(const GemmArgs
     }
   }
   cp_async_wait<0>();
+  pdl_trigger();  // the next kernel may start launching during the epilogue
 
   // ---- epilogue ----
 #pragma unroll
@@ -352,8 +354,7 @@ static int launch(cudaStream_t st, const GemmArgs& g, dim3 grid) {
     attr_dev_mask |= 1 << dev;
   }
   count_launch();
-  kern<<<grid, WM * WN * 32, smem, st>>>(g);
-  BR_CUDA(cudaGetLastError());
+  BR_CUDA(launch_pdl(kern, grid, dim3(WM * WN * 32), smem, st, g));
   return 0;
 }
 

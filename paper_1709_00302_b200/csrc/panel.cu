@@ -83,7 +83,7 @@ static int launch_leaf_t(cudaStream_t st, const LeafArgs& a) {
     attr_dev_mask |= (1 << dev);
   }
   cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   cfg.gridDim = dim3(C);
   cfg.blockDim = dim3(LT);
   cfg.dynamicSmemBytes = smem;
@@ -92,8 +92,10 @@ static int launch_leaf_t(cudaStream_t st, const LeafArgs& a) {
   at[0].val.clusterDim.x = C;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   count_launch();
   BR_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   return 0;
@@ -184,6 +186,8 @@ __global__ void __launch_bounds__(256) t_assemble_kernel(const double* __restric
                                                          const double* __restrict__ tau, int b,
                                                          double* __restrict__ T, int64_t ldt) {
   extern __shared__ double sm[];
+  pdl_wait();
+  pdl_trigger();
   const int nblk = (b + TAB - 1) / TAB;
   const int q = blockIdx.x, q0 = q * TAB;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -291,8 +295,8 @@ int t_from_gram(cudaStream_t st, const double* G, int64_t ldg, const double* tau
     attr_dev_mask |= 1 << dev;
   }
   count_launch();
-  t_assemble_kernel<<<nblk, 256, smem, st>>>(G, ldg, tau, (int)b, T, ldt);
-  BR_CUDA(cudaGetLastError());
+  BR_CUDA(launch_pdl(t_assemble_kernel, dim3(nblk), dim3(256), smem, st, G, ldg, tau, (int)b, T,
+                     ldt));
   return 0;
 }
 

@@ -124,6 +124,7 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
 #endif
   int64_t gr[R];
   double p[R][NB];
+  pdl_wait();  // the panel columns were written by the previous kernel
 #pragma unroll
   for (int k = 0; k < R; ++k) {
     gr[k] = base + tid + (int64_t)k * LT;
@@ -266,6 +267,7 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
     BR_PHASE(6);
   }
 
+  pdl_trigger();
   // ---- Y from the register tail (column c at p[k][NB - nb + c]): to shared
   // memory for W and straight to global ----
   if (nb == NB) {
