@@ -132,6 +132,11 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Host: when set, the kernel launchers only load their kernel (lazy module
+// loading would otherwise load it at first launch, which blocks while a
+// persistent panel kernel waits for that very launch) and return.
+extern thread_local bool g_preload_only;
+
 // Host: launch `kern` with programmatic stream serialization (BR_PDL=0
 // disables it). Every kernel of the library starts with pdl_wait().
 bool pdl_enabled();
@@ -148,6 +153,10 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  if (g_preload_only) {
+    cudaFuncAttributes fa;
+    return cudaFuncGetAttributes(&fa, kern);
+  }
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 

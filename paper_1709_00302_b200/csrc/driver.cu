@@ -42,6 +42,8 @@ void devbuf_free(DevBuf& b) {
   b.cap = 0;
 }
 
+thread_local bool g_preload_only = false;
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("BR_PDL");
@@ -259,12 +261,15 @@ static int ensure_scratch(Workspace& ws, int64_t main_doubles, int64_t panel_dou
   const int64_t both = std::max(main_doubles, panel_doubles);
   BR_CHECK(devbuf_reserve(ws.skbuf_main, both));
   BR_CHECK(devbuf_reserve(ws.skbuf_panel, both));
+  BR_CHECK(devbuf_reserve(ws.skbuf_aux, both));
   BR_CHECK(devbuf_reserve(ws.pscratch, pscr));
   ws.sk_main.p = ws.skbuf_main.p;
   ws.sk_main.cap = ws.skbuf_main.cap;
   ws.sk_panel.p = ws.skbuf_panel.p;
   ws.sk_panel.cap = ws.skbuf_panel.cap;
-  ws.sk_main.num_sms = ws.sk_panel.num_sms = ws.num_sms;
+  ws.sk_aux.p = ws.skbuf_aux.p;
+  ws.sk_aux.cap = ws.skbuf_aux.cap;
+  ws.sk_main.num_sms = ws.sk_panel.num_sms = ws.sk_aux.num_sms = ws.num_sms;
   return 0;
 }
 
@@ -296,6 +301,24 @@ int br_create(int device, br_handle_t* out) {
                                        (pp && pp[0] == 'l') ? lo : hi));
   h->ws.main = h->ws.own_main;
   h->ws.panel = h->ws.own_panel;
+  BR_CUDA(cudaStreamCreateWithPriority(&h->ws.aux, cudaStreamNonBlocking, hi));
+  BR_CUDA(cudaMalloc(&h->ws.flags, 128 * sizeof(unsigned)));
+  BR_CUDA(cudaMemset(h->ws.flags, 0, 128 * sizeof(unsigned)));
+  BR_CUDA(cudaEventCreateWithFlags(&h->ws.ev_aux0, cudaEventDisableTiming));
+  BR_CUDA(cudaEventCreateWithFlags(&h->ws.ev_aux1, cudaEventDisableTiming));
+  // load every kernel now: under lazy loading a first launch inside the
+  // persistent panel's handshake would wait for the spinning panel kernel
+  g_preload_only = true;
+  int prc = preload_gemm_kernels();
+  if (!prc) prc = preload_panel_kernels();
+  g_preload_only = false;
+  if (prc) return prc;
+  {
+    cudaFuncAttributes fa;
+    BR_CUDA(cudaFuncGetAttributes(&fa, finalize_sym_kernel));
+    BR_CUDA(cudaFuncGetAttributes(&fa, mask_band_kernel));
+    BR_CUDA(cudaFuncGetAttributes(&fa, identity_kernel));
+  }
   *out = h;
   return 0;
 }
@@ -312,6 +335,11 @@ int br_destroy(br_handle_t h) {
   devbuf_free(ws.tmp);
   devbuf_free(ws.stageA);
   devbuf_free(ws.stageQ);
+  devbuf_free(ws.skbuf_aux);
+  if (ws.flags) cudaFree(ws.flags);
+  if (ws.ev_aux0) cudaEventDestroy(ws.ev_aux0);
+  if (ws.ev_aux1) cudaEventDestroy(ws.ev_aux1);
+  if (ws.aux) cudaStreamDestroy(ws.aux);
   for (auto e : ws.events) cudaEventDestroy(e);
   for (auto e : ws.tevents) cudaEventDestroy(e);
   if (ws.own_main) cudaStreamDestroy(ws.own_main);
@@ -388,7 +416,8 @@ static int qr_common(br_handle_t h, MatView P, double* Y, int64_t ldy, double* T
   BR_CHECK(ensure_scratch(ws, 4 * std::max<int64_t>(j, 1) * b + (1 << 20), (1 << 20) + 4 * j * b,
                           panel_scratch_doubles(b)));
   MatView Yv(Y, ldy, j, b), Tv(T, ldt, b, b), Wv(W, ldw, j, b);
-  return panel_qr(cur_stream(ws), cur_sk(ws), ws.pscratch, P, Yv, tau, Tv, W ? &Wv : nullptr);
+  return panel_qr(cur_stream(ws), cur_sk(ws), ws.pscratch, P, Yv, tau, Tv, W ? &Wv : nullptr, 0,
+                  &ws);
 }
 
 int br_qr_panel(br_handle_t h, int64_t j, int64_t b, double* P, int64_t ldp, double* Y,

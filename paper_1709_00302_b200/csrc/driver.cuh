@@ -32,6 +32,14 @@ struct Workspace {
   DevBuf factors;   // reduction buffers
   DevBuf tmp;       // kernel-level API temporaries
   DevBuf stageA, stageQ;  // host-buffer entry points
+  // auxiliary stream of the persistent panel: the block updates between
+  // leaves run there while the leaf cluster stays resident
+  cudaStream_t aux = nullptr;
+  Scratch sk_aux;
+  DevBuf skbuf_aux;
+  unsigned* flags = nullptr;  // 128 leaf handshake words
+  unsigned epoch = 0;
+  cudaEvent_t ev_aux0 = nullptr, ev_aux1 = nullptr;
   // events
   std::vector<cudaEvent_t> events;
   size_t event_next = 0;
@@ -92,11 +100,15 @@ int ws_collect_timing(Workspace& ws);  // after a sync: fold events into t_ms
 // b x b triangle; the strictly-lower part of P is left unspecified (the
 // reductions zero it in their final band mask).
 int panel_qr(cudaStream_t st, Scratch& sk, DevBuf& pscratch, MatView P, MatView Y, double* tau,
-             MatView T, MatView* W);
+             MatView T, MatView* W, int max_ctas = 0, Workspace* pws = nullptr);
 int64_t panel_scratch_doubles(int64_t b);
 int t_from_gram(cudaStream_t st, const double* G, int64_t ldg, const double* tau, int64_t b,
                 double* T, int64_t ldt);
 int house_gen_dev(cudaStream_t st, int64_t L, const double* x, double* v, double* tau_beta);
+
+// Force-load every kernel of the library (gemm.cu, panel.cu, driver.cu).
+int preload_gemm_kernels();
+int preload_panel_kernels();
 
 // Elementwise helpers (driver.cu)
 int finalize_sym(cudaStream_t st, double* A, int64_t lda, int64_t n, int64_t w);

@@ -46,8 +46,8 @@ static int env_cfg(const char* var, int dflt) {
 static int big_cfg(int am, bool rank_update) {
   static int gen = -1, sym = -1, rku = -1;
   if (gen < 0) {
-    gen = env_cfg("BR_GEMM_BIG", CFG_C);
-    sym = env_cfg("BR_GEMM_SYMM", CFG_A);
+    gen = env_cfg("BR_GEMM_BIG", CFG_G);
+    sym = env_cfg("BR_GEMM_SYMM", CFG_G);
     rku = env_cfg("BR_GEMM_RANKB", CFG_D);
   }
   if (am == A_SYM) return sym;
@@ -283,6 +283,24 @@ int syr2k_lower(cudaStream_t st, MatView A2, MatView X3, MatView Y, int64_t c0, 
   const int cfg = lower_cfg(j);
   dim3 grid((unsigned)cdiv(j - c0, kTiles[cfg].bm), (unsigned)cdiv(c1 - c0, kTiles[cfg].bn), 1);
   return launch_tile(cfg, A_N, B_T, EPI_LOWER, st, g, grid);
+}
+
+// Load every GEMM instantiation and the split-K reduction (see g_preload_only).
+int preload_gemm_kernels() {
+  GemmArgs g{};
+  const dim3 grid(1, 1, 1);
+  for (int cfg = 0; cfg < CFG_COUNT; ++cfg) {
+    for (int am : {A_N, A_T, A_SYM})
+      for (int bmd : {B_N, B_T})
+        for (int epi : {EPI_GEN, EPI_SPLIT}) {
+          if (am == A_SYM && bmd == B_T) continue;
+          BR_CHECK(launch_tile(cfg, am, bmd, epi, 0, g, grid));
+        }
+    if (kTiles[cfg].bm == kTiles[cfg].bn) BR_CHECK(launch_tile(cfg, A_N, B_T, EPI_LOWER, 0, g, grid));
+  }
+  cudaFuncAttributes fa;
+  BR_CUDA(cudaFuncGetAttributes(&fa, splitk_reduce_kernel));
+  return 0;
 }
 
 }  // namespace br

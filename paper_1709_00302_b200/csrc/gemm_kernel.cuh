@@ -353,6 +353,7 @@ static int launch(cudaStream_t st, const GemmArgs& g, dim3 grid) {
     BR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_dev_mask |= 1 << dev;
   }
+  if (g_preload_only) return (int)launch_pdl(kern, grid, dim3(WM * WN * 32), smem, st, g);
   count_launch();
   BR_CUDA(launch_pdl(kern, grid, dim3(WM * WN * 32), smem, st, g));
   return 0;

@@ -7,7 +7,8 @@
 
 namespace br {
 
-enum TileCfg { CFG_L = 0, CFG_NS, CFG_MS, CFG_A, CFG_B, CFG_C, CFG_D, CFG_E, CFG_F, CFG_COUNT };
+enum TileCfg { CFG_L = 0, CFG_NS, CFG_MS, CFG_A, CFG_B, CFG_C, CFG_D, CFG_E, CFG_F, CFG_G, CFG_H,
+               CFG_COUNT };
 
 struct TileInfo {
   const char* name;
@@ -26,9 +27,11 @@ constexpr TileInfo kTiles[CFG_COUNT] = {
     {"D", 64, 64, 3},    // 4 warps 2x2, warp 32x32, 4 stages
     {"E", 64, 128, 2},   // 8 warps 2x4, warp 32x32, BK=32, 2 stages
     {"F", 128, 64, 2},   // 8 warps 4x2, warp 32x32, BK=32, 2 stages
+    {"G", 64, 128, 2},   // 4 warps 2x2, warp 32x64, 3 stages
+    {"H", 128, 64, 2},   // 4 warps 2x2, warp 64x32, 3 stages
 };
 // K depth of one pipeline stage per configuration (split-K granularity)
-constexpr int kTileBK[CFG_COUNT] = {16, 16, 16, 16, 16, 16, 16, 32, 32};
+constexpr int kTileBK[CFG_COUNT] = {16, 16, 16, 16, 16, 16, 16, 32, 32, 16, 16};
 
 int launch_tile_L(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
 int launch_tile_NS(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
@@ -39,6 +42,8 @@ int launch_tile_C(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, 
 int launch_tile_D(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
 int launch_tile_E(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
 int launch_tile_F(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
+int launch_tile_G(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
+int launch_tile_H(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
 
 inline int launch_tile(int cfg, int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g,
                        dim3 grid) {
@@ -51,7 +56,9 @@ inline int launch_tile(int cfg, int am, int bmd, int epi, cudaStream_t st, const
     case CFG_C: return launch_tile_C(am, bmd, epi, st, g, grid);
     case CFG_D: return launch_tile_D(am, bmd, epi, st, g, grid);
     case CFG_E: return launch_tile_E(am, bmd, epi, st, g, grid);
-    default: return launch_tile_F(am, bmd, epi, st, g, grid);
+    case CFG_F: return launch_tile_F(am, bmd, epi, st, g, grid);
+    case CFG_G: return launch_tile_G(am, bmd, epi, st, g, grid);
+    default: return launch_tile_H(am, bmd, epi, st, g, grid);
   }
 }
 

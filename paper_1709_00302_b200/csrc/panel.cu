@@ -23,6 +23,8 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cuda.h>
+
 #include "driver.cuh"
 #include "gemm.cuh"
 
@@ -45,6 +47,10 @@ struct LeafArgs {
   int nb;
   int wt;           // W output: 0 -> Y T, 1 -> Y T^T (block reflector Q^T = I + Y T^T Y^T)
   long long* prof;  // optional per-phase cycle counters (BR_LEAF_PROF=1)
+  // persistent mode: nleaves leaves of width lw over a btot-wide panel P
+  int nleaves, lw, btot;
+  unsigned* flags;  // [0, 64): leaf done, [64, 128): next leaf's columns ready
+  unsigned epoch;
 };
 
 }  // namespace br
@@ -54,7 +60,18 @@ namespace br {
 // Rows one cluster holds at leaf width nb: 16 CTAs x 256 threads x R rows
 // with R * NB = 64 register doubles per thread.
 static int leaf_rows_per_thread(int nb) { return nb > 16 ? 2 : (nb > 8 ? 4 : 8); }
-static int64_t leaf_capacity(int nb) { return (int64_t)LEAF_MAXC * 256 * leaf_rows_per_thread(nb); }
+// Threads per leaf CTA at most (BR_LEAF_LT=128: half-SM CTAs only; tuning aid).
+static int leaf_max_lt() {
+  static int lt = 0;
+  if (!lt) {
+    const char* e = std::getenv("BR_LEAF_LT");
+    lt = (e && std::atoi(e) == 128) ? 128 : 256;
+  }
+  return lt;
+}
+static int64_t leaf_capacity(int nb) {
+  return (int64_t)LEAF_MAXC * leaf_max_lt() * leaf_rows_per_thread(nb);
+}
 
 // Leaf width for a j x b panel: the widest of {32, 16, 8} (or b if narrower)
 // whose L rows fit one cluster.
@@ -96,15 +113,21 @@ static int launch_leaf_t(cudaStream_t st, const LeafArgs& a) {
   at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 2;
+  if (g_preload_only) {
+    cudaFuncAttributes fa;
+    BR_CUDA(cudaFuncGetAttributes(&fa, kern));
+    return 0;
+  }
   count_launch();
   BR_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   return 0;
 }
 
 static int launch_leaf(cudaStream_t st, MatView P, MatView Y, double* tau, double* T, int64_t ldt,
-                       MatView* W, int wt = 0) {
+                       MatView* W, int wt = 0, int nleaves = 1, int lw = 0,
+                       unsigned* flags = nullptr, unsigned epoch = 0) {
   const int64_t L = P.rows;
-  const int nb = (int)P.cols;
+  const int nb = nleaves > 1 ? lw : (int)P.cols;
   if (nb < 1 || nb > LEAF_NB || L > leaf_capacity(nb)) {
     set_error("panel leaf %lld x %d does not fit one cluster", (long long)L, nb);
     return -1;
@@ -122,6 +145,11 @@ static int launch_leaf(cudaStream_t st, MatView P, MatView Y, double* tau, doubl
   a.nb = nb;
   a.wt = wt;
   a.prof = nullptr;
+  a.nleaves = nleaves;
+  a.lw = nb;
+  a.btot = (int)P.cols;
+  a.flags = flags;
+  a.epoch = epoch;
   static const bool prof_on = std::getenv("BR_LEAF_PROF") != nullptr;
   if (prof_on) {
     if (!g_leaf_prof) {
@@ -300,12 +328,68 @@ int t_from_gram(cudaStream_t st, const double* G, int64_t ldg, const double* tau
   return 0;
 }
 
+// Persistent panels for panels of at most this many rows (BR_PERSIST_ROWS,
+// default 0 = off). One cluster launch per panel instead of one per leaf:
+// under a concurrent rank-b update it cuts the panel's time 3x in isolation
+// (tools/overlap_bench.py), but it holds the cluster's SMs for the whole
+// panel, and on c3-c5 the net effect measured flat to -2 %, so it is off.
+static bool persistent_panel_enabled(int64_t rows) {
+  static const int64_t lim = [] {
+    const char* e = std::getenv("BR_PERSIST_ROWS");
+    return e ? (int64_t)std::atoll(e) : (int64_t)0;  // measured: no gain on c3-c5
+  }();
+  return rows <= lim;
+}
+
+// Stream-ordered 32-bit flag wait / release write (driver stream memory
+// operations: no SM is held while waiting). Resolved through the runtime's
+// driver entry point so the library does not link libcuda directly.
+typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static PFN_waitValue32 g_wait32 = nullptr;
+static PFN_writeValue32 g_write32 = nullptr;
+static int stream_ops_init() {
+  if (g_wait32 && g_write32) return 0;
+  cudaDriverEntryPointQueryResult q1, q2;
+  void* f1 = nullptr;
+  void* f2 = nullptr;
+  // the CUDA 12 (_v2) entry points; the unversioned lookup can return the
+  // legacy ABI, whose calls succeed without taking effect
+  BR_CUDA(cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", &f1, 12000, cudaEnableDefault, &q1));
+  BR_CUDA(cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", &f2, 12000, cudaEnableDefault, &q2));
+  if (!f1 || !f2 || q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess) {
+    set_error("driver stream memory operations unavailable");
+    return 1;
+  }
+  g_wait32 = (PFN_waitValue32)f1;
+  g_write32 = (PFN_writeValue32)f2;
+  return 0;
+}
+static int stream_wait_flag(cudaStream_t st, unsigned* f, unsigned v) {
+  BR_CHECK(stream_ops_init());
+  const CUresult r = g_wait32((CUstream)st, (CUdeviceptr)f, v, CU_STREAM_WAIT_VALUE_EQ);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuStreamWaitValue32 failed (CUresult %d)", (int)r);
+    return 1000 + (int)r;
+  }
+  return 0;
+}
+static int stream_set_flag(cudaStream_t st, unsigned* f, unsigned v) {
+  BR_CHECK(stream_ops_init());
+  const CUresult r = g_write32((CUstream)st, (CUdeviceptr)f, v, CU_STREAM_WRITE_VALUE_DEFAULT);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuStreamWriteValue32 failed (CUresult %d)", (int)r);
+    return 1000 + (int)r;
+  }
+  return 0;
+}
+
 int64_t panel_scratch_doubles(int64_t b) {
   return b * b + LEAF_NB * LEAF_NB + 2 * LEAF_NB * b + (b > TAB_MAXB ? b * TAB_MAXB : 0);
 }
 
 int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView Y, double* tau,
-             MatView T, MatView* W) {
+             MatView T, MatView* W, int max_ctas, Workspace* pws) {
   const int64_t j = P.rows, b = P.cols;
   if (j < b || b < 1) {
     set_error("panel_qr needs j >= b >= 1, got %lld x %lld", (long long)j, (long long)b);
@@ -333,7 +417,38 @@ int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView 
   double* tblk = scratch + b * b;
   MatView Z(tblk + LEAF_NB * LEAF_NB, LEAF_NB, LEAF_NB, b);
   MatView Z2(Z.p + LEAF_NB * b, LEAF_NB, LEAF_NB, b);
-  for (int64_t s = 0; s < b; s += nbl) {
+  const int nleaves = (int)cdiv(b, nbl);
+  const bool persist = pws && W && nleaves <= 64 && persistent_panel_enabled(j);
+  if (persist) {
+    // Persistent panel: one cluster launch factors every leaf; the block
+    // update of leaf s is applied on the aux stream, first to the next
+    // leaf's columns (then the leaf may proceed), then to the rest of the
+    // panel while the next leaf runs.
+    Workspace& w = *pws;
+    if (++w.epoch == 0) ++w.epoch;
+    const unsigned ep = w.epoch;
+    BR_CUDA(cudaEventRecord(w.ev_aux0, st));
+    BR_CUDA(cudaStreamWaitEvent(w.aux, w.ev_aux0, 0));
+    BR_CHECK(launch_leaf(st, P, Y, tau, nullptr, 0, W, 1, nleaves, nbl, w.flags, ep));
+    for (int s = 0; s + 1 < nleaves; ++s) {
+      const int64_t c0 = (int64_t)s * nbl, e = std::min<int64_t>(c0 + nbl, b), wc = e - c0;
+      const int64_t h1 = std::min<int64_t>(e + nbl, b);
+      BR_CHECK(stream_wait_flag(w.aux, &w.flags[s], ep));
+      MatView leafY = Y.sub(c0, c0, j - c0, wc), What = W->sub(c0, c0, j - c0, wc);
+      MatView head = P.sub(c0, e, j - c0, h1 - e), Zh = Z.sub(0, 0, wc, h1 - e);
+      BR_CHECK(gemm(w.aux, w.sk_aux, Zh, leafY.T(), head, 1.0, 0.0, nullptr, max_ctas));
+      BR_CHECK(gemm(w.aux, w.sk_aux, head, What, Zh, 1.0, 1.0, nullptr, max_ctas));
+      BR_CHECK(stream_set_flag(w.aux, &w.flags[64 + s + 1], ep));
+      if (h1 < b) {
+        MatView rest = P.sub(c0, h1, j - c0, b - h1), Zr = Z.sub(0, h1 - e, wc, b - h1);
+        BR_CHECK(gemm(w.aux, w.sk_aux, Zr, leafY.T(), rest, 1.0, 0.0, nullptr, max_ctas));
+        BR_CHECK(gemm(w.aux, w.sk_aux, rest, What, Zr, 1.0, 1.0, nullptr, max_ctas));
+      }
+    }
+    BR_CUDA(cudaEventRecord(w.ev_aux1, w.aux));
+    BR_CUDA(cudaStreamWaitEvent(st, w.ev_aux1, 0));
+  }
+  for (int64_t s = 0; s < b && !persist; s += nbl) {
     const int64_t e = std::min<int64_t>(s + nbl, b);
     const int64_t w = e - s;
     MatView leafP = P.sub(s, s, j - s, w);
@@ -345,8 +460,8 @@ int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView 
       BR_CHECK(launch_leaf(st, leafP, leafY, tau + s, tblk, LEAF_NB, &What, 1));
       MatView rest = P.sub(s, e, j - s, b - e);
       MatView Zs = Z.sub(0, 0, w, b - e);
-      BR_CHECK(gemm(st, ws, Zs, leafY.T(), rest, 1.0, 0.0));
-      BR_CHECK(gemm(st, ws, rest, What, Zs, 1.0, 1.0));
+      BR_CHECK(gemm(st, ws, Zs, leafY.T(), rest, 1.0, 0.0, nullptr, max_ctas));
+      BR_CHECK(gemm(st, ws, rest, What, Zs, 1.0, 1.0, nullptr, max_ctas));
       continue;
     }
     BR_CHECK(launch_leaf(st, leafP, leafY, tau + s, tblk, LEAF_NB, nullptr));
@@ -355,14 +470,14 @@ int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView 
       MatView rest = P.sub(s, e, j - s, b - e);
       MatView Zs = Z.sub(0, 0, w, b - e), Z2s = Z2.sub(0, 0, w, b - e);
       MatView Tb(tblk, LEAF_NB, w, w);
-      BR_CHECK(gemm(st, ws, Zs, leafY.T(), rest, 1.0, 0.0));
-      BR_CHECK(gemm(st, ws, Z2s, Tb.T(), Zs, 1.0, 0.0));
-      BR_CHECK(gemm(st, ws, rest, leafY, Z2s, 1.0, 1.0));
+      BR_CHECK(gemm(st, ws, Zs, leafY.T(), rest, 1.0, 0.0, nullptr, max_ctas));
+      BR_CHECK(gemm(st, ws, Z2s, Tb.T(), Zs, 1.0, 0.0, nullptr, max_ctas));
+      BR_CHECK(gemm(st, ws, rest, leafY, Z2s, 1.0, 1.0, nullptr, max_ctas));
     }
   }
   // full T: Gram, then the blocked recurrence in one kernel (T is written whole,
   // zeros below the diagonal)
-  BR_CHECK(gemm(st, ws, G, Y.T(), Y, 1.0, 0.0));
+  BR_CHECK(gemm(st, ws, G, Y.T(), Y, 1.0, 0.0, nullptr, max_ctas));
   if (b <= TAB_MAXB) {
     BR_CHECK(t_from_gram(st, G.p, G.ld, tau, b, T.p, T.ld));
   } else {
@@ -374,11 +489,11 @@ int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView 
       BR_CHECK(t_from_gram(st, G.p + s + s * G.ld, G.ld, tau + s, e - s, T.p + s + s * T.ld, T.ld));
       if (s == 0) continue;
       MatView tmp(tmpp, s, s, e - s);
-      BR_CHECK(gemm(st, ws, tmp, G.sub(0, s, s, e - s), T.sub(s, s, e - s, e - s), 1.0, 0.0));
-      BR_CHECK(gemm(st, ws, T.sub(0, s, s, e - s), T.sub(0, 0, s, s), tmp, 1.0, 0.0));
+      BR_CHECK(gemm(st, ws, tmp, G.sub(0, s, s, e - s), T.sub(s, s, e - s, e - s), 1.0, 0.0, nullptr, max_ctas));
+      BR_CHECK(gemm(st, ws, T.sub(0, s, s, e - s), T.sub(0, 0, s, s), tmp, 1.0, 0.0, nullptr, max_ctas));
     }
   }
-  if (W) BR_CHECK(gemm(st, ws, *W, Y, T, 1.0, 0.0));
+  if (W) BR_CHECK(gemm(st, ws, *W, Y, T, 1.0, 0.0, nullptr, max_ctas));
   return 0;
 }
 
@@ -410,6 +525,22 @@ int house_gen_dev(cudaStream_t st, int64_t L, const double* x, double* v, double
   count_launch();
   house_gen_kernel<<<1, 256, 0, st>>>(L, x, v, tb);
   BR_CUDA(cudaGetLastError());
+  return 0;
+}
+
+// Load every panel kernel (see g_preload_only).
+int preload_panel_kernels() {
+  LeafArgs a{};
+  a.nleaves = 1;
+  BR_CHECK((launch_leaf_t<32, 2, 128>(0, a)));
+  BR_CHECK((launch_leaf_t<32, 2, 256>(0, a)));
+  BR_CHECK((launch_leaf_t<16, 4, 128>(0, a)));
+  BR_CHECK((launch_leaf_t<16, 4, 256>(0, a)));
+  BR_CHECK((launch_leaf_t<8, 8, 128>(0, a)));
+  BR_CHECK((launch_leaf_t<8, 8, 256>(0, a)));
+  cudaFuncAttributes fa;
+  BR_CUDA(cudaFuncGetAttributes(&fa, t_assemble_kernel));
+  BR_CUDA(cudaFuncGetAttributes(&fa, house_gen_kernel));
   return 0;
 }
 

@@ -33,6 +33,20 @@ __device__ __forceinline__ void st_async_v2(uint32_t raddr, double a, double b, 
       : "memory");
 }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // Transpose-reduce RC values across a warp: afterwards v[0] of lane l holds
 // the warp total of slot (l / (32/RC)). Fixed summation tree (deterministic).
 template <int RC>
@@ -105,7 +119,6 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
 
   const uint32_t rank = cluster_ctarank(), ncta = cluster_nctarank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nb = a.nb;
   const int64_t base = (int64_t)rank * ROWS;
   const bool owner_cta = (base == 0);  // row i < nb <= 32 always lives in CTA 0
 
@@ -122,278 +135,311 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
 #else
 #define BR_PHASE(k)
 #endif
-  int64_t gr[R];
-  double p[R][NB];
   pdl_wait();  // the panel columns were written by the previous kernel
-#pragma unroll
-  for (int k = 0; k < R; ++k) {
-    gr[k] = base + tid + (int64_t)k * LT;
-    const bool valid = gr[k] < a.L;
-#pragma unroll
-    for (int c = 0; c < NB; ++c) p[k][c] = (valid && c < nb) ? *a.P.at(gr[k], c) : 0.0;
-  }
   if (tid == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  cluster_sync_all();  // mbarriers initialized cluster-wide before any st.async
-  BR_PHASE(7);
-  for (int i = 0; i < nb; ++i) {
-    const int buf = i & 1;
-    const int g0 = NB - i;  // first Gram slot
-    if (tid == 0) mbar_arrive_expect_tx(&mbar[buf], ncta * NB * 8 + NB * 8);
-#pragma unroll
-    for (int k = 0; k < R; ++k)
-      if (gr[k] == i) {
-#pragma unroll
-        for (int c = 0; c < NB; c += 2)
-          *reinterpret_cast<double2*>(&rowi[c]) = make_double2(p[k][c], p[k][c + 1]);
+  unsigned gstep = 0;  // exchange rounds so far (mbarrier buffer / phase)
+  // Persistent mode (a.nleaves > 1): the cluster factors the panel's leaves
+  // one after another; between leaves the block update of the next leaf's
+  // columns runs on the auxiliary stream (flags: done[s] -> aux, aux ->
+  // ready[s+1]), so the cluster is launched (and its SMs drained) once per panel.
+  for (int leaf = 0; leaf < a.nleaves; ++leaf) {
+    const int64_t off = (int64_t)leaf * a.lw;
+    const int nb = (a.nleaves == 1) ? a.nb : (int)min((int64_t)a.lw, (int64_t)a.btot - off);
+    const int64_t Lr = a.L - off;  // rows of this leaf
+    const MatView P = a.P.sub(off, off, Lr, nb);
+    double* const Yo = a.Y + off + off * a.ldy;
+    double* const Wo = a.W ? a.W + off + off * a.ldw : nullptr;
+    double* const tauo = a.tau + off;
+    if (leaf > 0) {
+      if (tid == 0) {
+        const unsigned long long t0 = globaltimer_ns();
+        while (ld_acquire_u32(&a.flags[64 + leaf]) != a.epoch) {
+          __nanosleep(64);
+          if (globaltimer_ns() - t0 > 10000000000ull) __trap();  // 10 s: fail loudly, never hang
+        }
       }
-    // rows above i keep their final R entries in the registers (captured into
-    // Rrow when they reach column 0); masking x removes them from every sum
-    double xk[R];
+      __syncthreads();
+    }
+    int64_t gr[R];
+    double p[R][NB];
 #pragma unroll
     for (int k = 0; k < R; ++k) {
-      xk[k] = (gr[k] >= i) ? p[k][0] : 0.0;
-      if (gr[k] < i) Rrow[gr[k]][i] = p[k][0];
+      gr[k] = base + tid + (int64_t)k * LT;
+      const bool valid = gr[k] < Lr;
+#pragma unroll
+      for (int c = 0; c < NB; ++c) p[k][c] = (valid && c < nb) ? __ldcg(P.at(gr[k], c)) : 0.0;
     }
-    // ---- per-thread partials, transpose-reduced per warp ----
+    if (leaf == 0) cluster_sync_all();  // mbarriers initialized cluster-wide before any st.async
+    BR_PHASE(7);
+    for (int i = 0; i < nb; ++i, ++gstep) {
+      const int buf = gstep & 1;
+      const int g0 = NB - i;  // first Gram slot
+      if (tid == 0) mbar_arrive_expect_tx(&mbar[buf], ncta * NB * 8 + NB * 8);
 #pragma unroll
-    for (int ch = 0; ch < NCH; ++ch) {
-      double v[RC];
+      for (int k = 0; k < R; ++k)
+        if (gr[k] == i) {
 #pragma unroll
-      for (int cc = 0; cc < RC; ++cc) {
-        const int c = ch * RC + cc;
-        double s = 0.0;
-#pragma unroll
-        for (int k = 0; k < R; ++k) s = fma(xk[k], p[k][c], s);
-        v[cc] = s;
-      }
-      warp_transpose_reduce<RC>(v, lane);
-      if ((lane & (SH - 1)) == 0) wred[warp][ch * RC + lane / SH] = v[0];
-    }
-    BR_PHASE(0);
-    __syncthreads();
-    BR_PHASE(1);
-    // ---- warp w sums and pushes slots [w*SPW, (w+1)*SPW) to every CTA ----
-    if (warp < NPW) {
-      constexpr int NP = SPW / 2;  // slot pairs per warp
-      const int ntask = NP * (int)ncta;
-      const bool push_row = owner_cta;
-      for (int t0 = 0; t0 < ntask; t0 += 32) {
-        const int t = t0 + lane;
-        if (t < ntask) {
-          const int pp = t / (int)ncta;
-          const uint32_t q = (uint32_t)(t % (int)ncta);
-          const int c = warp * SPW + 2 * pp;
-          double u0[LW], u1[LW];  // fixed pairwise tree over the warps
-#pragma unroll
-          for (int w = 0; w < LW; ++w) {
-            u0[w] = wred[w][c];
-            u1[w] = wred[w][c + 1];
-          }
-#pragma unroll
-          for (int h = LW / 2; h >= 1; h >>= 1)
-#pragma unroll
-            for (int w = 0; w < h; ++w) {
-              u0[w] += u0[w + h];
-              u1[w] += u1[w + h];
-            }
-          const double s0 = u0[0], s1 = u1[0];
-          const uint32_t rm = map_cluster(&mbar[buf], q);
-          st_async_v2(map_cluster(&recv[buf][rank][c], q), s0, s1, rm);
-          if (push_row) st_async_v2(map_cluster(&recv_row[buf][c], q), rowi[c], rowi[c + 1], rm);
+          for (int c = 0; c < NB; c += 2)
+            *reinterpret_cast<double2*>(&rowi[c]) = make_double2(p[k][c], p[k][c + 1]);
         }
-      }
-    }
-    BR_PHASE(2);
-    while (!mbar_try_wait(&mbar[buf], (i >> 1) & 1)) {
-    }
-    BR_PHASE(3);
-    // ---- every warp: the same scalars from the same received vectors ----
-    double rinv = 0.0;
-    {
-      const double pic = (lane < NB) ? recv_row[buf][lane] : 0.0;
-      double gq[LEAF_MAXC];  // fixed pairwise tree over the (power-of-two) CTAs
-#pragma unroll
-      for (int q = 0; q < LEAF_MAXC; ++q)
-        gq[q] = (lane < NB && q < (int)ncta) ? recv[buf][q][lane] : 0.0;
-#pragma unroll
-      for (int h = LEAF_MAXC / 2; h >= 1; h >>= 1)
-#pragma unroll
-        for (int q = 0; q < h; ++q) gq[q] += gq[q + h];
-      const double g = gq[0];
-      {
-        const double nrm2 = __shfl_sync(0xffffffffu, g, 0);
-        const double x0 = __shfl_sync(0xffffffffu, pic, 0);
-        // ||x|| and 1/||x|| from one rsqrt; 1/(x0 - beta) by rcp (~1 ulp
-        // each, far inside the parity tolerance) to keep the chain short
-        double beta = 0.0, rb = 0.0;
-        if (nrm2 != 0.0) {
-          const double rs = rsqrt(nrm2), nrm = nrm2 * rs;
-          beta = (x0 < 0.0) ? nrm : -nrm;
-          rb = (x0 < 0.0) ? rs : -rs;
-          rinv = __drcp_rn(x0 - beta);
-        }
-        if (lane < NB)  // tau == 0 (zero column): identity reflector, no update
-          alw[warp][lane] = (nrm2 != 0.0 && lane >= 1 && lane < nb - i) ? fma(-g, rb, pic) : 0.0;
-        if (warp == 0 && lane == 0) {  // tau = (beta - x0) / beta later, off the critical path
-          scal[i][0] = x0;
-          scal[i][1] = beta;
-          scal[i][2] = rinv;
-        }
-        if (warp == 0 && lane >= g0 && lane < NB) G[lane - g0][i] = fma(fma(-pic, x0, g), rinv, pic);
-        __syncwarp();
-      }
-    }
-    BR_PHASE(4);
-    {
-      double al[NB];
-#pragma unroll
-      for (int c = 0; c < NB; c += 2) {
-        const double2 t2 = *reinterpret_cast<const double2*>(&alw[warp][c]);
-        al[c] = t2.x;
-        al[c + 1] = t2.y;
-      }
+      // rows above i keep their final R entries in the registers (captured into
+      // Rrow when they reach column 0); masking x removes them from every sum
+      double xk[R];
 #pragma unroll
       for (int k = 0; k < R; ++k) {
-        const double vk = (gr[k] == i) ? 1.0 : xk[k] * rinv;  // 0 above row i
-#pragma unroll
-        for (int c = 0; c < NB - 1; ++c) p[k][c] = fma(-vk, al[c + 1], p[k][c + 1]);
-        p[k][NB - 1] = vk;  // Y column i (unit diagonal, zeros above)
+        xk[k] = (gr[k] >= i) ? p[k][0] : 0.0;
+        if (gr[k] < i) Rrow[gr[k]][i] = p[k][0];
       }
+      // ---- per-thread partials, transpose-reduced per warp ----
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        double v[RC];
+#pragma unroll
+        for (int cc = 0; cc < RC; ++cc) {
+          const int c = ch * RC + cc;
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < R; ++k) s = fma(xk[k], p[k][c], s);
+          v[cc] = s;
+        }
+        warp_transpose_reduce<RC>(v, lane);
+        if ((lane & (SH - 1)) == 0) wred[warp][ch * RC + lane / SH] = v[0];
+      }
+      BR_PHASE(0);
+      __syncthreads();
+      BR_PHASE(1);
+      // ---- warp w sums and pushes slots [w*SPW, (w+1)*SPW) to every CTA ----
+      if (warp < NPW) {
+        constexpr int NP = SPW / 2;  // slot pairs per warp
+        const int ntask = NP * (int)ncta;
+        const bool push_row = owner_cta;
+        for (int t0 = 0; t0 < ntask; t0 += 32) {
+          const int t = t0 + lane;
+          if (t < ntask) {
+            const int pp = t / (int)ncta;
+            const uint32_t q = (uint32_t)(t % (int)ncta);
+            const int c = warp * SPW + 2 * pp;
+            double u0[LW], u1[LW];  // fixed pairwise tree over the warps
+#pragma unroll
+            for (int w = 0; w < LW; ++w) {
+              u0[w] = wred[w][c];
+              u1[w] = wred[w][c + 1];
+            }
+#pragma unroll
+            for (int h = LW / 2; h >= 1; h >>= 1)
+#pragma unroll
+              for (int w = 0; w < h; ++w) {
+                u0[w] += u0[w + h];
+                u1[w] += u1[w + h];
+              }
+            const double s0 = u0[0], s1 = u1[0];
+            const uint32_t rm = map_cluster(&mbar[buf], q);
+            st_async_v2(map_cluster(&recv[buf][rank][c], q), s0, s1, rm);
+            if (push_row) st_async_v2(map_cluster(&recv_row[buf][c], q), rowi[c], rowi[c + 1], rm);
+          }
+        }
+      }
+      BR_PHASE(2);
+      while (!mbar_try_wait(&mbar[buf], (gstep >> 1) & 1)) {
+      }
+      BR_PHASE(3);
+      // ---- every warp: the same scalars from the same received vectors ----
+      double rinv = 0.0;
+      {
+        const double pic = (lane < NB) ? recv_row[buf][lane] : 0.0;
+        double gq[LEAF_MAXC];  // fixed pairwise tree over the (power-of-two) CTAs
+#pragma unroll
+        for (int q = 0; q < LEAF_MAXC; ++q)
+          gq[q] = (lane < NB && q < (int)ncta) ? recv[buf][q][lane] : 0.0;
+#pragma unroll
+        for (int h = LEAF_MAXC / 2; h >= 1; h >>= 1)
+#pragma unroll
+          for (int q = 0; q < h; ++q) gq[q] += gq[q + h];
+        const double g = gq[0];
+        {
+          const double nrm2 = __shfl_sync(0xffffffffu, g, 0);
+          const double x0 = __shfl_sync(0xffffffffu, pic, 0);
+          // ||x|| and 1/||x|| from one rsqrt; 1/(x0 - beta) by rcp (~1 ulp
+          // each, far inside the parity tolerance) to keep the chain short
+          double beta = 0.0, rb = 0.0;
+          if (nrm2 != 0.0) {
+            const double rs = rsqrt(nrm2), nrm = nrm2 * rs;
+            beta = (x0 < 0.0) ? nrm : -nrm;
+            rb = (x0 < 0.0) ? rs : -rs;
+            rinv = __drcp_rn(x0 - beta);
+          }
+          if (lane < NB)  // tau == 0 (zero column): identity reflector, no update
+            alw[warp][lane] = (nrm2 != 0.0 && lane >= 1 && lane < nb - i) ? fma(-g, rb, pic) : 0.0;
+          if (warp == 0 && lane == 0) {  // tau = (beta - x0) / beta later, off the critical path
+            scal[i][0] = x0;
+            scal[i][1] = beta;
+            scal[i][2] = rinv;
+          }
+          if (warp == 0 && lane >= g0 && lane < NB) G[lane - g0][i] = fma(fma(-pic, x0, g), rinv, pic);
+          __syncwarp();
+        }
+      }
+      BR_PHASE(4);
+      {
+        double al[NB];
+#pragma unroll
+        for (int c = 0; c < NB; c += 2) {
+          const double2 t2 = *reinterpret_cast<const double2*>(&alw[warp][c]);
+          al[c] = t2.x;
+          al[c + 1] = t2.y;
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          const double vk = (gr[k] == i) ? 1.0 : xk[k] * rinv;  // 0 above row i
+#pragma unroll
+          for (int c = 0; c < NB - 1; ++c) p[k][c] = fma(-vk, al[c + 1], p[k][c + 1]);
+          p[k][NB - 1] = vk;  // Y column i (unit diagonal, zeros above)
+        }
+      }
+      BR_PHASE(6);
     }
-    BR_PHASE(6);
-  }
 
-  pdl_trigger();
-  // ---- Y from the register tail (column c at p[k][NB - nb + c]): to shared
-  // memory for W and straight to global ----
-  if (nb == NB) {
+    // dependents may start launching once the last leaf's steps are done (an
+    // earlier trigger could park them on SMs the aux-stream updates need)
+    if (leaf == a.nleaves - 1) pdl_trigger();
+    // ---- Y from the register tail (column c at p[k][NB - nb + c]): to shared
+    // memory for W and straight to global ----
+    if (nb == NB) {
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const bool ok = gr[k] < Lr;
+#pragma unroll
+        for (int c = 0; c < NB; ++c) {
+          Ys[c * ROWS + tid + k * LT] = p[k][c];
+          if (ok) Yo[gr[k] + (int64_t)c * a.ldy] = p[k][c];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+#pragma unroll
+        for (int c = 0; c < NB; ++c) {
+          const int src = NB - nb + c;  // runtime-dependent: select from the array
+          double y = 0.0;
+#pragma unroll
+          for (int m = 0; m < NB; ++m)
+            if (m == src) y = p[k][m];
+          y = (c < nb) ? y : 0.0;
+          Ys[c * ROWS + tid + k * LT] = y;
+          if (c < nb && gr[k] < Lr) Yo[gr[k] + (int64_t)c * a.ldy] = y;
+        }
+      }
+    }
+    // ---- R rows (owner CTA) ----
 #pragma unroll
     for (int k = 0; k < R; ++k) {
-      const bool ok = gr[k] < a.L;
-#pragma unroll
-      for (int c = 0; c < NB; ++c) {
-        Ys[c * ROWS + tid + k * LT] = p[k][c];
-        if (ok) a.Y[gr[k] + (int64_t)c * a.ldy] = p[k][c];
+      if (gr[k] < nb) {
+        const int r = (int)gr[k];
+        for (int c = r; c < nb; ++c) *P.at(r, c) = (c == r) ? scal[r][1] : Rrow[r][c];
       }
     }
-  } else {
+    // ---- tau = (beta - x0) / beta (ref kernels.py:109) ----
+    if (tid < nb) {
+      const double be = scal[tid][1];
+      scal[tid][0] = (be != 0.0) ? (be - scal[tid][0]) / be : 0.0;
+    }
+    __syncthreads();
+    // ---- T by the reference recurrence (ref kernels.py:152-162): lane r owns
+    // row r in registers, T[r][i] = -tau_i sum_{c<i} T[r][c] G[c][i]
+    // (T[r][c] = 0 for c < r) ----
+    if (warp == 0 && lane < NB) {
+      const int r = lane;
+      double tr[NB];
 #pragma unroll
-    for (int k = 0; k < R; ++k) {
+      for (int c = 0; c < NB; ++c) tr[c] = (c == r && r < nb) ? -scal[c][0] : 0.0;
 #pragma unroll
-      for (int c = 0; c < NB; ++c) {
-        const int src = NB - nb + c;  // runtime-dependent: select from the array
-        double y = 0.0;
+      for (int i = 1; i < NB; ++i) {
+        double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-        for (int m = 0; m < NB; ++m)
-          if (m == src) y = p[k][m];
-        y = (c < nb) ? y : 0.0;
-        Ys[c * ROWS + tid + k * LT] = y;
-        if (c < nb && gr[k] < a.L) a.Y[gr[k] + (int64_t)c * a.ldy] = y;
+        for (int c = 0; c + 1 < i; c += 2) {
+          s0 = fma(tr[c], G[c][i], s0);
+          s1 = fma(tr[c + 1], G[c + 1][i], s1);
+        }
+        if (i & 1) s0 = fma(tr[i - 1], G[i - 1][i], s0);
+        if (i > r && i < nb) tr[i] = -scal[i][0] * (s0 + s1);
       }
+#pragma unroll
+      for (int c = 0; c < NB; ++c) Ts[r][c] = tr[c];
     }
-  }
-  // ---- R rows (owner CTA) ----
+    __syncthreads();
+    BR_PHASE(8);
+    BR_PHASE(9);
+    // ---- W = Y T on the tensor cores: each warp 4 independent 8-row slabs
+    // at a time x NB columns ----
+    if (Wo) {
+      const int gq = lane >> 2, tq = lane & 3;
+      constexpr int U = 4;
+      for (int rb = warp * 8; rb < ROWS; rb += LW * 8 * U) {
+        if (base + rb >= Lr) break;
+        double acc[U][NB / 8][2];
 #pragma unroll
-  for (int k = 0; k < R; ++k) {
-    if (gr[k] < nb) {
-      const int r = (int)gr[k];
-      for (int c = r; c < nb; ++c) *a.P.at(r, c) = (c == r) ? scal[r][1] : Rrow[r][c];
-    }
-  }
-  // ---- tau = (beta - x0) / beta (ref kernels.py:109) ----
-  if (tid < nb) {
-    const double be = scal[tid][1];
-    scal[tid][0] = (be != 0.0) ? (be - scal[tid][0]) / be : 0.0;
-  }
-  __syncthreads();
-  // ---- T by the reference recurrence (ref kernels.py:152-162): lane r owns
-  // row r in registers, T[r][i] = -tau_i sum_{c<i} T[r][c] G[c][i]
-  // (T[r][c] = 0 for c < r) ----
-  if (warp == 0 && lane < NB) {
-    const int r = lane;
-    double tr[NB];
+        for (int u = 0; u < U; ++u)
 #pragma unroll
-    for (int c = 0; c < NB; ++c) tr[c] = (c == r && r < nb) ? -scal[c][0] : 0.0;
+          for (int n = 0; n < NB / 8; ++n) acc[u][n][0] = acc[u][n][1] = 0.0;
 #pragma unroll
-    for (int i = 1; i < NB; ++i) {
-      double s0 = 0.0, s1 = 0.0;
+        for (int k0 = 0; k0 < NB; k0 += 4) {
+          double bt[NB / 8];
 #pragma unroll
-      for (int c = 0; c + 1 < i; c += 2) {
-        s0 = fma(tr[c], G[c][i], s0);
-        s1 = fma(tr[c + 1], G[c + 1][i], s1);
-      }
-      if (i & 1) s0 = fma(tr[i - 1], G[i - 1][i], s0);
-      if (i > r && i < nb) tr[i] = -scal[i][0] * (s0 + s1);
-    }
+          for (int n = 0; n < NB / 8; ++n)  // B = T, or T^T for the block-reflector form Y T^T
+            bt[n] = a.wt ? Ts[n * 8 + gq][k0 + tq] : Ts[k0 + tq][n * 8 + gq];
 #pragma unroll
-    for (int c = 0; c < NB; ++c) Ts[r][c] = tr[c];
-  }
-  __syncthreads();
-  BR_PHASE(8);
-  BR_PHASE(9);
-  // ---- W = Y T on the tensor cores: each warp 4 independent 8-row slabs
-  // at a time x NB columns ----
-  if (a.W) {
-    const int gq = lane >> 2, tq = lane & 3;
-    constexpr int U = 4;
-    for (int rb = warp * 8; rb < ROWS; rb += LW * 8 * U) {
-      if (base + rb >= a.L) break;
-      double acc[U][NB / 8][2];
+          for (int u = 0; u < U; ++u) {
+            const int r0 = rb + u * LW * 8;
+            const double av = (r0 < ROWS) ? Ys[(k0 + tq) * ROWS + r0 + gq] : 0.0;  // A = Y (8 x 4)
 #pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int n = 0; n < NB / 8; ++n) acc[u][n][0] = acc[u][n][1] = 0.0;
-#pragma unroll
-      for (int k0 = 0; k0 < NB; k0 += 4) {
-        double bt[NB / 8];
-#pragma unroll
-        for (int n = 0; n < NB / 8; ++n)  // B = T, or T^T for the block-reflector form Y T^T
-          bt[n] = a.wt ? Ts[n * 8 + gq][k0 + tq] : Ts[k0 + tq][n * 8 + gq];
+            for (int n = 0; n < NB / 8; ++n) dmma884(acc[u][n][0], acc[u][n][1], av, bt[n]);
+          }
+        }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int r0 = rb + u * LW * 8;
-          const double av = (r0 < ROWS) ? Ys[(k0 + tq) * ROWS + r0 + gq] : 0.0;  // A = Y (8 x 4)
+          const int64_t row = base + r0 + gq;
+          if (r0 < ROWS && row < Lr) {
 #pragma unroll
-          for (int n = 0; n < NB / 8; ++n) dmma884(acc[u][n][0], acc[u][n][1], av, bt[n]);
-        }
-      }
+            for (int n = 0; n < NB / 8; ++n)
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int r0 = rb + u * LW * 8;
-        const int64_t row = base + r0 + gq;
-        if (r0 < ROWS && row < a.L) {
-#pragma unroll
-          for (int n = 0; n < NB / 8; ++n)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int c = n * 8 + 2 * tq + h;
-              if (c < nb) a.W[row + (int64_t)c * a.ldw] = acc[u][n][h];
-            }
+              for (int h = 0; h < 2; ++h) {
+                const int c = n * 8 + 2 * tq + h;
+                if (c < nb) Wo[row + (int64_t)c * a.ldw] = acc[u][n][h];
+              }
+          }
         }
       }
     }
-  }
-  BR_PHASE(10);
+    BR_PHASE(10);
 #undef BR_PHASE
 #ifdef BR_LEAF_PROF
-  if (pr) {
-    for (int k = 0; k < 11; ++k) atomicAdd((unsigned long long*)&a.prof[k], (unsigned long long)tp[k]);
-    atomicAdd((unsigned long long*)&a.prof[11], (unsigned long long)(nb + 1));
-    atomicAdd((unsigned long long*)&a.prof[12], 1ull);
-  }
+    if (pr) {
+      for (int k = 0; k < 11; ++k) atomicAdd((unsigned long long*)&a.prof[k], (unsigned long long)tp[k]);
+      atomicAdd((unsigned long long*)&a.prof[11], (unsigned long long)(nb + 1));
+      atomicAdd((unsigned long long*)&a.prof[12], 1ull);
+    }
 #endif
-  if (rank == 0) {
-    if (tid < nb) a.tau[tid] = scal[tid][0];
-    if (a.T)
-      for (int q = tid; q < nb * nb; q += LT) {
-        const int r = q % nb, c = q / nb;
-        a.T[r + (int64_t)c * a.ldt] = Ts[r][c];
-      }
-  }
+    if (rank == 0) {
+      if (tid < nb) tauo[tid] = scal[tid][0];
+      if (a.T && a.nleaves == 1)
+        for (int q = tid; q < nb * nb; q += LT) {
+          const int r = q % nb, c = q / nb;
+          a.T[r + (int64_t)c * a.ldt] = Ts[r][c];
+        }
+    }
+    if (a.nleaves > 1) {
+      // leaf outputs (Y, W, R, tau) visible, then hand the block update to the
+      // aux stream; the cluster barrier also protects the smem reused next leaf
+      __threadfence();
+      cluster_sync_all();
+      if (rank == 0 && tid == 0) st_release_u32(&a.flags[leaf], a.epoch);
+    }
+  }  // leaf
   cluster_sync_all();  // no remote traffic is in flight when any CTA exits
 }
 

@@ -13,6 +13,7 @@
 // split-invariant (fixed K order, no atomics), so look-ahead depth 1 is
 // bitwise identical to depth 0 on the same GPU.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "driver.cuh"
@@ -27,6 +28,22 @@ static double syr2k_flops(int64_t j, int64_t bp, int64_t c0, int64_t c1) {
   s = (double)(c1 - c0) * (double)j - 0.5 * ((double)c1 * (c1 - 1) - (double)c0 * (c0 - 1));
   return 4.0 * (double)bp * s;
 }
+// CTA cap for the split-K GEMMs inside a panel factorization (0 = none):
+// while the trailing update is large, the panel stream's GEMMs run on few
+// CTAs so they steal fewer SM slots from the update (tuning: BR_PANEL_CAP,
+// BR_PANEL_CAP_ROWS). Depends only on the panel height, so the schedule with
+// and without look-ahead makes the same choice (bitwise equality).
+static int panel_cap(int64_t rows) {
+  static int cap = -1;
+  static int64_t min_rows = 6144;
+  if (cap < 0) {
+    const char* e = std::getenv("BR_PANEL_CAP");
+    cap = e ? std::atoi(e) : 0;
+    if (const char* r = std::getenv("BR_PANEL_CAP_ROWS")) min_rows = std::atoll(r);
+  }
+  return rows >= min_rows ? cap : 0;
+}
+
 static double panel_flops(int64_t j, int64_t b) {
   return 2.0 * j * b * b - 2.0 * b * b * b / 3.0 + (double)j * b * b;  // QR + T/W
 }
@@ -49,9 +66,11 @@ int sevp_reduce(Workspace& ws, int64_t n, int64_t w, int64_t b, int lookahead, d
   BR_CHECK(devbuf_reserve(ws.factors, total));
   BR_CHECK(devbuf_reserve(ws.skbuf_main, 4 * n * b + (1 << 20)));
   BR_CHECK(devbuf_reserve(ws.skbuf_panel, 4 * jmax * b + (1 << 20)));
+  BR_CHECK(devbuf_reserve(ws.skbuf_aux, 4 * jmax * b + (1 << 20)));
   BR_CHECK(devbuf_reserve(ws.pscratch, panel_scratch_doubles(b)));
   ws.sk_main = Scratch{ws.skbuf_main.p, ws.skbuf_main.cap, ws.num_sms};
   ws.sk_panel = Scratch{ws.skbuf_panel.p, ws.skbuf_panel.cap, ws.num_sms};
+  ws.sk_aux = Scratch{ws.skbuf_aux.p, ws.skbuf_aux.cap, ws.num_sms};
   double* f = ws.factors.p;
   double *Yb[2], *Wb[2], *Tb[2], *taub[2];
   for (int p = 0; p < 2; ++p) {
@@ -78,7 +97,7 @@ int sevp_reduce(Workspace& ws, int64_t n, int64_t w, int64_t b, int lookahead, d
     MatView P(Aat(k + w, k), lda, j, bp);
     MatView Y(Yb[par], jmax, j, bp), T(Tb[par], b, bp, bp), W(Wb[par], jmax, j, bp);
     TimeScope ts(ws, st, TC_PANEL, panel_flops(j, bp), "qr", k);
-    return panel_qr(st, sk, ws.pscratch, P, Y, taub[par], T, &W);
+    return panel_qr(st, sk, ws.pscratch, P, Y, taub[par], T, &W, panel_cap(j), &ws);
   };
 
   cudaEvent_t ev_panel = nullptr;
@@ -200,9 +219,11 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
   BR_CHECK(devbuf_reserve(ws.factors, total));
   BR_CHECK(devbuf_reserve(ws.skbuf_main, 4 * std::max(m, n) * b + (1 << 20)));
   BR_CHECK(devbuf_reserve(ws.skbuf_panel, 4 * std::max(m, n) * b + (1 << 20)));
+  BR_CHECK(devbuf_reserve(ws.skbuf_aux, 4 * std::max(m, n) * b + (1 << 20)));
   BR_CHECK(devbuf_reserve(ws.pscratch, panel_scratch_doubles(b)));
   ws.sk_main = Scratch{ws.skbuf_main.p, ws.skbuf_main.cap, ws.num_sms};
   ws.sk_panel = Scratch{ws.skbuf_panel.p, ws.skbuf_panel.cap, ws.num_sms};
+  ws.sk_aux = Scratch{ws.skbuf_aux.p, ws.skbuf_aux.cap, ws.num_sms};
   double* f = ws.factors.p;
   double *Yu[2], *Wu[2], *Tu[2], *tauu[2];
   for (int p = 0; p < 2; ++p) {
@@ -228,14 +249,14 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
     MatView P(Aat(k, k), lda, i, bp);
     MatView Y(Yu[par], m, i, bp), T(Tu[par], b, bp, bp), W(Wu[par], m, i, bp);
     TimeScope ts(ws, st, TC_PANEL, panel_flops(i, bp), "qr", k);
-    return panel_qr(st, sk, ws.pscratch, P, Y, tauu[par], T, &W);
+    return panel_qr(st, sk, ws.pscratch, P, Y, tauu[par], T, &W, panel_cap(i), &ws);
   };
   auto lq = [&](cudaStream_t st, Scratch& sk, int64_t k, int64_t bq) -> int {
     const int64_t jr = n - k - w;
     MatView P(Aat(k, k + w), lda, jr, bq, true);  // transposed view of the bq x jr rows
     MatView Y(Yv, n, jr, bq), T(Tv, b, bq, bq), W(Wv, n, jr, bq);
     TimeScope ts(ws, st, TC_PANEL, panel_flops(jr, bq), "lq", k);
-    return panel_qr(st, sk, ws.pscratch, P, Y, tauv, T, &W);
+    return panel_qr(st, sk, ws.pscratch, P, Y, tauv, T, &W, panel_cap(jr), &ws);
   };
   auto handoff = [&]() -> int {  // main -> panel ordering point
     cudaEvent_t ev = ws_event(ws);
@@ -390,9 +411,11 @@ int band_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int f
   BR_CHECK(devbuf_reserve(ws.factors, total));
   BR_CHECK(devbuf_reserve(ws.skbuf_main, 4 * std::max(m, n) * b + (1 << 20)));
   BR_CHECK(devbuf_reserve(ws.skbuf_panel, 4 * std::max(m, n) * b + (1 << 20)));
+  BR_CHECK(devbuf_reserve(ws.skbuf_aux, 4 * std::max(m, n) * b + (1 << 20)));
   BR_CHECK(devbuf_reserve(ws.pscratch, panel_scratch_doubles(b)));
   ws.sk_main = Scratch{ws.skbuf_main.p, ws.skbuf_main.cap, ws.num_sms};
   ws.sk_panel = Scratch{ws.skbuf_panel.p, ws.skbuf_panel.cap, ws.num_sms};
+  ws.sk_aux = Scratch{ws.skbuf_aux.p, ws.skbuf_aux.cap, ws.num_sms};
   double* f = ws.factors.p;
   double *Yu[2], *Wu[2], *Tu[2], *tauu[2], *Yv[2], *Wv[2], *Tv[2], *tauv[2];
   for (int p = 0; p < 2; ++p) {
@@ -416,13 +439,13 @@ int band_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int f
     MatView P(Aat(t.k + w, t.k), lda, i, t.bp);
     MatView Y(Yu[par], m, i, t.bp), T(Tu[par], b, t.bp, t.bp), W(Wu[par], m, i, t.bp);
     TimeScope ts(ws, st, TC_PANEL, panel_flops(i, t.bp), "qr", t.k);
-    return panel_qr(st, sk, ws.pscratch, P, Y, tauu[par], T, &W);
+    return panel_qr(st, sk, ws.pscratch, P, Y, tauu[par], T, &W, panel_cap(i), &ws);
   };
   auto lq = [&](cudaStream_t st, Scratch& sk, const It& t, int par) -> int {
     MatView P(Aat(t.k, t.k + w), lda, t.jr, t.bq, true);  // transposed view of the bq x jr rows
     MatView Y(Yv[par], n, t.jr, t.bq), T(Tv[par], b, t.bq, t.bq), W(Wv[par], n, t.jr, t.bq);
     TimeScope ts(ws, st, TC_PANEL, panel_flops(t.jr, t.bq), "lq", t.k);
-    return panel_qr(st, sk, ws.pscratch, P, Y, tauv[par], T, &W);
+    return panel_qr(st, sk, ws.pscratch, P, Y, tauv[par], T, &W, panel_cap(t.jr), &ws);
   };
   auto panels = [&](cudaStream_t st, Scratch& sk, const It& t, int par) -> int {
     BR_CHECK(qr(st, sk, t, par));
