@@ -140,6 +140,9 @@ extern thread_local bool g_preload_only;
 // Host: launch `kern` with programmatic stream serialization (BR_PDL=0
 // disables it). Every kernel of the library starts with pdl_wait().
 bool pdl_enabled();
+// The stream's priority, attached to every launch as a launch attribute so it
+// survives CUDA-graph capture (graph kernel nodes do not inherit it).
+int stream_priority(cudaStream_t st);
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                               cudaStream_t st, Args... args) {
@@ -148,11 +151,13 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  at[1].id = cudaLaunchAttributePriority;
+  at[1].val.priority = stream_priority(st);
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   if (g_preload_only) {
     cudaFuncAttributes fa;
     return cudaFuncGetAttributes(&fa, kern);

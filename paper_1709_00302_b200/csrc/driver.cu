@@ -16,6 +16,7 @@ static thread_local char g_err[1024] = "";
 static std::atomic<int64_t> g_launches{0};
 int64_t launch_count() { return g_launches.load(); }
 void count_launch(int64_t n) { g_launches += n; }
+void g_launches_adjust(int64_t d) { g_launches += d; }
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -24,8 +25,12 @@ void set_error(const char* fmt, ...) {
   va_end(ap);
 }
 
+static std::atomic<int64_t> g_alloc_gen{0};
+int64_t alloc_generation() { return g_alloc_gen.load(); }
+
 int devbuf_reserve(DevBuf& b, int64_t n) {
   if (n <= b.cap) return 0;
+  ++g_alloc_gen;
   if (b.p) {
     BR_CUDA(cudaDeviceSynchronize());
     BR_CUDA(cudaFree(b.p));
@@ -43,6 +48,21 @@ void devbuf_free(DevBuf& b) {
 }
 
 thread_local bool g_preload_only = false;
+
+int stream_priority(cudaStream_t st) {
+  thread_local cudaStream_t last = nullptr;
+  thread_local int prio = 0;
+  if (st != last || st == nullptr) {
+    int p = 0;
+    if (cudaStreamGetPriority(st, &p) != cudaSuccess) {
+      cudaGetLastError();
+      p = 0;
+    }
+    last = st;
+    prio = p;
+  }
+  return prio;
+}
 
 bool pdl_enabled() {
   static const bool on = [] {
@@ -186,10 +206,32 @@ int zero_fill(cudaStream_t st, MatView V) {
   return 0;
 }
 
+// Graph replay pays off while launch latency is a visible share of the run
+// (c1/c2: -6 % / -5 %); for the large reductions the graph's replay of the
+// two-stream program measured 10 % slower than the stream program itself, so
+// only reductions below BR_GRAPH_MAX_FLOPS nominal flops (default 2e11) are
+// graphed; BR_GRAPHS=0 disables graphs.
+static bool graphs_enabled(double nominal) {
+  static const bool on = [] {
+    const char* e = std::getenv("BR_GRAPHS");
+    return !(e && e[0] == '0');
+  }();
+  static const double lim = [] {
+    const char* e = std::getenv("BR_GRAPH_MAX_FLOPS");
+    return e ? std::atof(e) : 2e11;
+  }();
+  return on && nominal <= lim;
+}
+
 // Runs one reduction on the handle's streams, timed by events on `main`
-// around the whole stream program (both streams joined at the end).
+// around the whole stream program (both streams joined at the end). Without
+// timing, the stream program of a reduction that repeats with identical
+// arguments is captured once into a CUDA graph (on its second call; the
+// first call sizes the workspace) and replayed afterwards: one launch per
+// reduction instead of hundreds, with the programmatic (PDL) edges kept.
 template <class F>
-int timed_reduction(Workspace& ws, br_stats* stats, double nominal, F&& body) {
+int timed_reduction(Workspace& ws, br_stats* stats, double nominal, Workspace::GraphKey key,
+                    F&& body) {
   cudaEvent_t e0, e1;
   BR_CUDA(cudaEventCreate(&e0));
   BR_CUDA(cudaEventCreate(&e1));
@@ -199,12 +241,62 @@ int timed_reduction(Workspace& ws, br_stats* stats, double nominal, F&& body) {
     set_error("CUDA: %s", cudaGetErrorString(e));
     return 1000 + (int)e;
   };
-  int rc = cu(cudaEventRecord(e0, ws.main));
-  ws.trace_base = e0;
-  if (ws.timing >= 2) ws.trace.clear();
+  key.gen = alloc_generation();
+  key.main = ws.main;
+  key.panel = ws.panel;
+  key.timing = ws.timing;
+  // events recorded by captured graph nodes cannot be timed, so the timing /
+  // trace modes stay eager
+  const bool graphable = graphs_enabled(nominal) && ws.timing == 0 && ws.main != nullptr;
+  const bool same = graphable && key == ws.gkey;
+  int rc = 0;
   int64_t iters = 0;
   float ms = 0.f;
-  if (!rc) rc = body(&iters);
+  if (same && !ws.gexec && ws.gseen >= 1) {
+    // capture the stream program (workspace already sized by the eager run)
+    const int64_t c0 = launch_count();
+    ws.timed.clear();
+    ws.tevent_next = 0;
+    rc = cu(cudaStreamBeginCapture(ws.main, cudaStreamCaptureModeRelaxed));
+    if (!rc) {
+      const int brc = body(&iters);
+      cudaGraph_t g = nullptr;
+      const cudaError_t ee = cudaStreamEndCapture(ws.main, &g);
+      if (brc == 0 && ee == cudaSuccess && g) {
+        if (cudaGraphInstantiate(&ws.gexec, g, 0) != cudaSuccess) ws.gexec = nullptr;
+      }
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();  // a failed capture leaves no sticky error
+      ws_events_reset(ws);
+      if (brc != 0 && brc < 0) rc = brc;  // argument errors are real
+      ws.g_iters = iters;
+      ws.g_launches = launch_count() - c0;
+      ws.timed.clear();
+      g_launches_adjust(-(launch_count() - c0));  // the capture itself launched nothing
+    }
+    if (!ws.gexec) ws.gseen = -1000000;  // capture failed: stay eager for this key
+  }
+  rc = rc ? rc : cu(cudaEventRecord(e0, ws.main));
+  ws.trace_base = e0;
+  if (ws.timing >= 2) ws.trace.clear();
+  if (!rc) {
+    if (same && ws.gexec) {
+      rc = cu(cudaGraphLaunch(ws.gexec, ws.main));
+      iters = ws.g_iters;
+      count_launch(ws.g_launches);
+    } else {
+      rc = body(&iters);
+      if (graphable) {
+        if (!same) {
+          if (ws.gexec) cudaGraphExecDestroy(ws.gexec);
+          ws.gexec = nullptr;
+          ws.gkey = key;
+          ws.gseen = 0;
+        }
+        ++ws.gseen;
+      }
+    }
+  }
   if (!rc) rc = cu(cudaEventRecord(e1, ws.main));
   if (!rc) rc = cu(cudaEventSynchronize(e1));
   if (!rc) rc = cu(cudaStreamSynchronize(ws.panel));
@@ -342,6 +434,7 @@ int br_destroy(br_handle_t h) {
   if (ws.aux) cudaStreamDestroy(ws.aux);
   for (auto e : ws.events) cudaEventDestroy(e);
   for (auto e : ws.tevents) cudaEventDestroy(e);
+  if (ws.gexec) cudaGraphExecDestroy(ws.gexec);
   if (ws.own_main) cudaStreamDestroy(ws.own_main);
   if (ws.own_panel) cudaStreamDestroy(ws.own_panel);
   delete h;
@@ -630,7 +723,17 @@ int br_reduce_sym_band(br_handle_t h, int64_t n, int64_t w, int64_t b, int looka
   ARG(A != nullptr && lda >= n, 6);
   ARG(Q == nullptr || ldq >= n, 9);
   DEV(h);
-  return timed_reduction(h->ws, stats, sevp_nominal(n),
+  Workspace::GraphKey key;
+  key.kind = 0;
+  key.n = n;
+  key.w = w;
+  key.b = b;
+  key.la = lookahead;
+  key.A = A;
+  key.lda = lda;
+  key.Q = Q;
+  key.ldq = ldq;
+  return timed_reduction(h->ws, stats, sevp_nominal(n), key,
                          [&](int64_t* it) {
                            return sevp_reduce(h->ws, n, w, b, lookahead, A, lda, Q, ldq, it);
                          });
@@ -646,7 +749,16 @@ int br_reduce_tri_band(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b
   ARG(lookahead == 0 || lookahead == 1, 6);
   ARG(A != nullptr && lda >= m, 7);
   DEV(h);
-  return timed_reduction(h->ws, stats, svd_nominal(m, n),
+  Workspace::GraphKey key;
+  key.kind = 1;
+  key.m = m;
+  key.n = n;
+  key.w = w;
+  key.b = b;
+  key.la = lookahead;
+  key.A = A;
+  key.lda = lda;
+  return timed_reduction(h->ws, stats, svd_nominal(m, n), key,
                          [&](int64_t* it) {
                            return tri_reduce(h->ws, m, n, w, b, lookahead, A, lda, it);
                          });
@@ -663,7 +775,17 @@ int br_reduce_band(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b, in
   ARG(lookahead == 0 || lookahead == 1, 7);
   ARG(A != nullptr && lda >= m, 8);
   DEV(h);
-  return timed_reduction(h->ws, stats, svd_nominal(m, n),
+  Workspace::GraphKey key;
+  key.kind = 2;
+  key.m = m;
+  key.n = n;
+  key.w = w;
+  key.b = b;
+  key.fused = simultaneous;
+  key.la = lookahead;
+  key.A = A;
+  key.lda = lda;
+  return timed_reduction(h->ws, stats, svd_nominal(m, n), key,
                          [&](int64_t* it) {
                            return band_reduce(h->ws, m, n, w, b, simultaneous, lookahead, A,
                                               lda, it);

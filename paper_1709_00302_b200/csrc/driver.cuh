@@ -13,6 +13,7 @@ struct DevBuf {
   int64_t cap = 0;  // doubles
 };
 int devbuf_reserve(DevBuf& b, int64_t n);
+int64_t alloc_generation();  // bumped whenever a DevBuf is (re)allocated
 void devbuf_free(DevBuf& b);
 
 enum TimeClass { TC_PANEL = 0, TC_SYMM = 1, TC_SYR2K = 2, TC_GEMM = 3, TC_COUNT = 4 };
@@ -40,6 +41,25 @@ struct Workspace {
   unsigned* flags = nullptr;  // 128 leaf handshake words
   unsigned epoch = 0;
   cudaEvent_t ev_aux0 = nullptr, ev_aux1 = nullptr;
+  // CUDA graph of the last reduction's stream program, replayed when the
+  // same reduction (sizes, pointers, streams, workspace generation) repeats
+  struct GraphKey {
+    int kind = -1, fused = 0, la = 0, timing = 0;
+    int64_t m = 0, n = 0, w = 0, b = 0, lda = 0, ldq = 0, gen = -1;
+    const void* A = nullptr;
+    const void* Q = nullptr;
+    cudaStream_t main = nullptr, panel = nullptr;
+    bool operator==(const GraphKey& o) const {
+      return kind == o.kind && fused == o.fused && la == o.la && timing == o.timing && m == o.m &&
+             n == o.n &&
+             w == o.w && b == o.b && lda == o.lda && ldq == o.ldq && gen == o.gen && A == o.A &&
+             Q == o.Q && main == o.main && panel == o.panel;
+    }
+  };
+  GraphKey gkey;
+  int gseen = 0;  // eager runs of gkey so far
+  cudaGraphExec_t gexec = nullptr;
+  int64_t g_iters = 0, g_launches = 0;
   // events
   std::vector<cudaEvent_t> events;
   size_t event_next = 0;
@@ -73,6 +93,7 @@ struct Workspace {
 // Kernels launched by this library in this process (stats / bench evidence).
 int64_t launch_count();
 void count_launch(int64_t n = 1);
+void g_launches_adjust(int64_t d);
 
 cudaEvent_t ws_event(Workspace& ws);  // recycled sync-only event
 void ws_events_reset(Workspace& ws);

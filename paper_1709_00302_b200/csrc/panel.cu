@@ -100,7 +100,7 @@ static int launch_leaf_t(cudaStream_t st, const LeafArgs& a) {
     attr_dev_mask |= (1 << dev);
   }
   cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[3];
   cfg.gridDim = dim3(C);
   cfg.blockDim = dim3(LT);
   cfg.dynamicSmemBytes = smem;
@@ -111,8 +111,10 @@ static int launch_leaf_t(cudaStream_t st, const LeafArgs& a) {
   at[0].val.clusterDim.z = 1;
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  at[2].id = cudaLaunchAttributePriority;
+  at[2].val.priority = stream_priority(st);
   cfg.attrs = at;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = 3;
   if (g_preload_only) {
     cudaFuncAttributes fa;
     BR_CUDA(cudaFuncGetAttributes(&fa, kern));
