@@ -551,8 +551,10 @@ int br_build_w(br_handle_t h, int64_t j, int64_t b, const double* Y, int64_t ldy
   Workspace& ws = h->ws;
   BR_CHECK(ensure_scratch(ws, 4 * std::max<int64_t>(j, 1) * std::max<int64_t>(b, 1) + (1 << 20),
                           1 << 20, panel_scratch_doubles(1)));
+  // W[:, i] = Y[:, :i+1] T[:i+1, i] (ref kernels.py:139-149): only T's upper
+  // triangle is read
   return gemm(cur_stream(ws), cur_sk(ws), MatView(W, ldw, j, b), MatView((double*)Y, ldy, j, b),
-              MatView((double*)T, ldt, b, b), 1.0, 0.0);
+              MatView((double*)T, ldt, b, b), 1.0, 0.0, nullptr, 0, 0, true);
 }
 
 int br_apply_wy_left(br_handle_t h, int64_t rows, int64_t cols, double* A, int64_t lda,

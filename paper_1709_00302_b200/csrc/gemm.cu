@@ -194,11 +194,16 @@ static int make_args(MatView C, MatView A, MatView B, double alpha, double beta,
 }
 
 int gemm(cudaStream_t st, Scratch& ws, MatView C, MatView A, MatView B, double alpha,
-         double beta, const MatView* Cin, int max_ctas, int64_t kps) {
+         double beta, const MatView* Cin, int max_ctas, int64_t kps, bool b_upper) {
   GemmArgs g;
   int am = 0;
   bool bt = false;
+  if (b_upper && (B.trans || C.trans)) {
+    set_error("gemm: b_upper needs a non-transposed B and C");
+    return -1;
+  }
   BR_CHECK(make_args(C, A, B, alpha, beta, Cin, g, am, bt));
+  g.b_upper = b_upper ? 1 : 0;
   return run_gemm(am, st, ws, g, bt, max_ctas, kps);
 }
 

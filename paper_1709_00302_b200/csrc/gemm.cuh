@@ -50,6 +50,7 @@ struct GemmArgs {
   double* ws;           // EPI_SPLIT: partials [z][N][M]
   int64_t c0, c1;       // EPI_LOWER: rows [c0, M) x cols [c0, c1)
   int vecA, vecB;       // 16-byte cp.async allowed for A / B
+  int b_upper;          // B_N with B upper triangular: K range of a tile ends at its last column
 };
 
 // Host-side launch helpers (gemm.cu). All return 0 or a positive CUDA error.
@@ -57,7 +58,8 @@ struct GemmArgs {
 // transposition; a transposed C is handled by transposing the product.
 // kps > 0 pins the split-K chunk (see gemm_plan_kps).
 int gemm(cudaStream_t st, Scratch& ws, MatView C, MatView A, MatView B, double alpha,
-         double beta, const MatView* Cin = nullptr, int max_ctas = 0, int64_t kps = 0);
+         double beta, const MatView* Cin = nullptr, int max_ctas = 0, int64_t kps = 0,
+         bool b_upper = false);
 // The split-K chunk gemm() would choose for this whole product. Updating the
 // product in row/column pieces with this kps sums every element in the same
 // order as the whole call, so the result is bitwise independent of the pieces.

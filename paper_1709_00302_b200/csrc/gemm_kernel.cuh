@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB) dgemm_kernel(const GemmArgs
     n0 = (int64_t)blockIdx.y * BN;
     kbeg = (int64_t)blockIdx.z * g.k_per_split;
     kend = min(g.K, kbeg + g.k_per_split);
+    if (BMD == B_N && g.b_upper) kend = max(kbeg, min(kend, n0 + BN));  // rows > n of B are 0
   }
   const int64_t nmax = (EPI == EPI_LOWER) ? g.c1 : g.N;
   pdl_wait();  // inputs written by the previous kernel in the stream

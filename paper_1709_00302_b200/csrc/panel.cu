@@ -495,7 +495,7 @@ int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView 
       BR_CHECK(gemm(st, ws, T.sub(0, s, s, e - s), T.sub(0, 0, s, s), tmp, 1.0, 0.0, nullptr, max_ctas));
     }
   }
-  if (W) BR_CHECK(gemm(st, ws, *W, Y, T, 1.0, 0.0, nullptr, max_ctas));
+  if (W) BR_CHECK(gemm(st, ws, *W, Y, T, 1.0, 0.0, nullptr, max_ctas, 0, true));  // T upper
   return 0;
 }
 
