@@ -48,13 +48,13 @@ static int big_cfg(int am, bool rank_update) {
   if (gen < 0) {
     gen = env_cfg("BR_GEMM_BIG", CFG_G);
     sym = env_cfg("BR_GEMM_SYMM", CFG_G);
-    rku = env_cfg("BR_GEMM_RANKB", CFG_D);
+    rku = env_cfg("BR_GEMM_RANKB", CFG_J);
   }
   if (am == A_SYM) return sym;
   return rank_update ? rku : gen;
 }
 static int lower_cfg(int64_t j) {
-  // 64x64 tiles (3 CTAs/SM) for large trailing blocks, 128x128 for small ones
+  // 64x64 tiles with BK=32 (3 CTAs/SM) for large trailing blocks, 128x128 for small ones
   static int cfg = -2;
   if (cfg == -2) {
     cfg = -1;
@@ -62,7 +62,7 @@ static int lower_cfg(int64_t j) {
     if (cfg >= 0 && kTiles[cfg].bm != kTiles[cfg].bn) cfg = CFG_L;
   }
   if (cfg >= 0) return cfg;
-  return j >= 4096 ? CFG_D : CFG_L;
+  return j >= 4096 ? CFG_J : CFG_L;
 }
 
 // Tile configuration of a general/symm GEMM of shape (M, N, K).
