@@ -47,7 +47,7 @@ static int big_cfg(int am, bool rank_update) {
   static int gen = -1, sym = -1, rku = -1;
   if (gen < 0) {
     gen = env_cfg("BR_GEMM_BIG", CFG_G);
-    sym = env_cfg("BR_GEMM_SYMM", CFG_G);
+    sym = env_cfg("BR_GEMM_SYMM", CFG_K);
     rku = env_cfg("BR_GEMM_RANKB", CFG_J);
   }
   if (am == A_SYM) return sym;

@@ -8,7 +8,7 @@
 namespace br {
 
 enum TileCfg { CFG_L = 0, CFG_NS, CFG_MS, CFG_A, CFG_B, CFG_C, CFG_D, CFG_E, CFG_F, CFG_G, CFG_H,
-               CFG_J, CFG_COUNT };
+               CFG_J, CFG_K, CFG_COUNT };
 
 struct TileInfo {
   const char* name;
@@ -30,9 +30,10 @@ constexpr TileInfo kTiles[CFG_COUNT] = {
     {"G", 64, 128, 2},   // 4 warps 2x2, warp 32x64, 3 stages
     {"H", 128, 64, 2},   // 4 warps 2x2, warp 64x32, 3 stages
     {"J", 64, 64, 3},    // 4 warps 2x2, warp 32x32, BK=32, 2 stages
+    {"K", 64, 128, 2},   // 4 warps 2x2, warp 32x64, BK=32, 2 stages
 };
 // K depth of one pipeline stage per configuration (split-K granularity)
-constexpr int kTileBK[CFG_COUNT] = {16, 16, 16, 16, 16, 16, 16, 32, 32, 16, 16, 32};
+constexpr int kTileBK[CFG_COUNT] = {16, 16, 16, 16, 16, 16, 16, 32, 32, 16, 16, 32, 32};
 
 int launch_tile_L(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
 int launch_tile_NS(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
@@ -46,6 +47,7 @@ int launch_tile_F(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, 
 int launch_tile_G(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
 int launch_tile_H(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
 int launch_tile_J(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
+int launch_tile_K(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
 
 inline int launch_tile(int cfg, int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g,
                        dim3 grid) {
@@ -61,7 +63,8 @@ inline int launch_tile(int cfg, int am, int bmd, int epi, cudaStream_t st, const
     case CFG_F: return launch_tile_F(am, bmd, epi, st, g, grid);
     case CFG_G: return launch_tile_G(am, bmd, epi, st, g, grid);
     case CFG_H: return launch_tile_H(am, bmd, epi, st, g, grid);
-    default: return launch_tile_J(am, bmd, epi, st, g, grid);
+    case CFG_J: return launch_tile_J(am, bmd, epi, st, g, grid);
+    default: return launch_tile_K(am, bmd, epi, st, g, grid);
   }
 }
 
