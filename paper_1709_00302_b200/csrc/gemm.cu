@@ -285,7 +285,9 @@ int syr2k_lower(cudaStream_t st, MatView A2, MatView X3, MatView Y, int64_t c0, 
   g.vecA = al16(X3.p, X3.ld) && al16(Y.p, Y.ld) && (c0 % 2 == 0);
   g.vecB = g.vecA;
   (void)max_ctas;
-  const int cfg = lower_cfg(j);
+  // narrow column ranges (the look-ahead's lead strip) on 64x64 tiles: more
+  // CTAs for a latency-bound launch; the per-element K order is the same
+  const int cfg = (c1 - c0 <= 64) ? CFG_J : lower_cfg(j);
   dim3 grid((unsigned)cdiv(j - c0, kTiles[cfg].bm), (unsigned)cdiv(c1 - c0, kTiles[cfg].bn), 1);
   return launch_tile(cfg, A_N, B_T, EPI_LOWER, st, g, grid);
 }
