@@ -87,6 +87,10 @@ struct TileIter {
     for (int it = 0; it < IT; ++it) p[it] = src2 + (x0 + xt) + (krow + yt + it * YS) * ld2;
     step = (int64_t)TY * ld2;
   }
+  __device__ __forceinline__ void advance() {
+#pragma unroll
+    for (int it = 0; it < IT; ++it) p[it] += step;
+  }
   // Issue the tile at K offset k0 (the pointers are already there) into
   // shared memory at dst; `kend` bounds K when the tile is partial.
   __device__ __forceinline__ void load(uint32_t dst, int64_t k0, int64_t kend, bool full) {
@@ -207,6 +211,17 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB) dgemm_kernel(const GemmArgs
       ib.init(g.B, g.ldb, n0, g.N, kbeg, INT64_MAX, tid);
     }
   }
+  // SYMM: a direct iterator for k-tiles below the diagonal block and a
+  // transposed one (reading the stored lower triangle) for k-tiles above it
+  using ItSN = TileIter<BM, BK, LDA_KM, NT, false>;
+  using ItST = TileIter<BK, BM, LDA_MK, NT, true>;
+  const bool fastS = AM == A_SYM && vA;
+  ItSN isn;
+  ItST ist;
+  if (AM == A_SYM && fastS) {
+    isn.init(g.A, g.lda, m0, g.M, kbeg, INT64_MAX, tid);
+    ist.init(g.A, g.lda, kbeg, kend, m0, g.M, tid);
+  }
   const uint32_t as_u32 = smem_u32(As), bs_u32 = smem_u32(Bs);
   auto load_stage = [&](int s, int64_t k0) {
     double* as = As + s * A_STAGE;
@@ -221,7 +236,20 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB) dgemm_kernel(const GemmArgs
     } else if (AM == A_T) {
       load_tile<BK, BM, LDA_MK, NT>(as, g.A, g.lda, g.A, g.lda, INT64_MAX, k0, kend, m0, g.M, vA,
                                     tid);
+    } else if (fastS && sym_case(k0, m0, BK, BM) != 2) {
+      const uint32_t dst = as_u32 + (uint32_t)(s * A_STAGE * 8);
+      if (sym_case(k0, m0, BK, BM) == 0) {
+        isn.load(dst, k0, kend, full);
+        ist.advance();
+      } else {
+        ist.load(dst, k0, kend, full);
+        isn.advance();
+      }
     } else {
+      if (fastS) {
+        isn.advance();
+        ist.advance();
+      }
       const int c = sym_case(k0, m0, BK, BM);
       if (c == 0) {
         load_tile<BM, BK, LDA_KM, NT>(as, g.A, g.lda, g.A, g.lda, INT64_MAX, m0, g.M, k0, kend, vA,
@@ -230,12 +258,23 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB) dgemm_kernel(const GemmArgs
         load_tile<BK, BM, LDA_MK, NT>(as, g.A, g.lda, g.A, g.lda, INT64_MAX, k0, kend, m0, g.M, vA,
                                       tid);
       } else {
-        for (int idx = tid; idx < BK * BM; idx += NT) {
+        // diagonal k-tile: element (m, k) from the stored lower triangle; the
+        // loads are issued in batches (independent) before the shared stores
+        constexpr int PER = BK * BM / NT;
+        double v[PER];
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int idx = tid + u * NT;
           const int k = idx / BM, m = idx % BM;
           const int64_t r = m0 + m, cc = k0 + k;
-          double v = 0.0;
-          if (r < g.M && cc < kend) v = (r >= cc) ? g.A[r + cc * g.lda] : g.A[cc + r * g.lda];
-          as[k * LDA_KM + m] = v;
+          v[u] = (r < g.M && cc < kend) ? __ldg((r >= cc) ? &g.A[r + cc * g.lda]
+                                                          : &g.A[cc + r * g.lda])
+                                        : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int idx = tid + u * NT;
+          as[(idx / BM) * LDA_KM + idx % BM] = v[u];
         }
       }
     }
