@@ -396,7 +396,13 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
             const int r0 = rb + u * LW * 8;
             const double av = (r0 < ROWS) ? Ys[(k0 + tq) * ROWS + r0 + gq] : 0.0;  // A = Y (8 x 4)
 #pragma unroll
-            for (int n = 0; n < NB / 8; ++n) dmma884(acc[u][n][0], acc[u][n][1], av, bt[n]);
+            for (int n = 0; n < NB / 8; ++n) {
+              // T is upper triangular: the 4 x 8 block (k0.., n*8..) is zero when
+              // k0 >= n*8 + 8 (B = T) or k0 + 4 <= n*8 (B = T^T); skip those DMMAs
+              if (!a.wt && k0 >= n * 8 + 8) continue;
+              if (a.wt && k0 + 4 <= n * 8) continue;
+              dmma884(acc[u][n][0], acc[u][n][1], av, bt[n]);
+            }
           }
         }
 #pragma unroll

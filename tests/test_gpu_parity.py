@@ -395,3 +395,45 @@ def test_band_edge_cases(br):
     res = br.reduce_band_svd(A, br.SvdConfig(200, 10, 12, 6))
     ref, _, _, it = O.reduce_band_svd(A, 12, 6)
     assert res.iterations == it and rel(res.band, ref, np.linalg.norm(A)) <= 1e-13
+
+
+# --- execution paths: CUDA-graph replay, persistent panels ---------------------
+
+def test_graph_replay_bitwise(br):
+    """Repeated identical reductions run eager, then captured into a CUDA
+    graph, then replayed: all three results are bitwise equal."""
+    A = sym(300, 21)
+    outs = [br.reduce_sym_band(A, br.SevpConfig(300, 16, 16, br.SevpVariant.V2)).band
+            for _ in range(4)]
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+    B = rand(260, 200, 22)
+    touts = [br.reduce_tri_band(B, 16, 8).band for _ in range(3)]
+    assert np.array_equal(touts[1], touts[0]) and np.array_equal(touts[2], touts[0])
+    bouts = [br.reduce_band_svd(B, br.SvdConfig(260, 200, 12, 6, variant=br.SvdVariant.V1)).band
+             for _ in range(3)]
+    assert np.array_equal(bouts[2], bouts[0])
+
+
+def test_persistent_panel_mode_matches(tmp_path):
+    """BR_PERSIST_ROWS enables the one-launch panel with aux-stream block
+    updates (a tuning mode); its panels agree with the default path."""
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, paper_1709_00302_b200 as br\n"
+        "A = np.asfortranarray(np.random.default_rng(5).standard_normal((3000, 96)))\n"
+        "P = br.qr_panel(A.copy(order='F'))\n"
+        "np.save(r'%s', np.stack([P.y, P.w]))\n")
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for rows in ("0", "100000"):
+        path = tmp_path / f"p{rows}.npy"
+        env = dict(os.environ, BR_PERSIST_ROWS=rows)
+        r = subprocess.run([sys.executable, "-c", code % path], cwd=root, env=env,
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        outs.append(np.load(path))
+    assert np.max(np.abs(outs[0] - outs[1])) <= 1e-12 * np.max(np.abs(outs[0]))
