@@ -142,11 +142,14 @@ int ws_collect_timing(Workspace& ws) {
 // entries kept, upper in-band entries mirrored from the lower triangle,
 // everything with |i-j| > w set to exactly 0. Upper entries are only
 // written, never read, so the input's upper triangle is never observed.
-__global__ void finalize_sym_kernel(double* A, int64_t lda, int64_t n, int64_t w) {
-  const int64_t total = n * n;
+// Columns [c0, c0 + nc) only (the host entry points finalize and stream out
+// finished column blocks while the reduction continues).
+__global__ void finalize_sym_kernel(double* A, int64_t lda, int64_t n, int64_t c0, int64_t nc,
+                                    int64_t w) {
+  const int64_t total = n * nc;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = idx % n, c = idx / n;
+    const int64_t r = idx % n, c = c0 + idx / n;
     const int64_t d = r - c;
     if (d > w || -d > w) A[r + c * lda] = 0.0;
     else if (d < 0) A[r + c * lda] = A[c + r * lda];
@@ -154,12 +157,12 @@ __global__ void finalize_sym_kernel(double* A, int64_t lda, int64_t n, int64_t w
 }
 
 // Exact off-band zeroing (ref svd.py:237-239 / oracles.py band pattern).
-__global__ void mask_band_kernel(double* A, int64_t lda, int64_t m, int64_t n, int64_t lo,
-                                 int64_t up) {
-  const int64_t total = m * n;
+__global__ void mask_band_kernel(double* A, int64_t lda, int64_t m, int64_t c0, int64_t nc,
+                                 int64_t lo, int64_t up) {
+  const int64_t total = m * nc;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = idx % m, c = idx / m;
+    const int64_t r = idx % m, c = c0 + idx / m;
     if (r - c > lo || c - r > up) A[r + c * lda] = 0.0;
   }
 }
@@ -177,18 +180,21 @@ static int grid_for(int64_t total) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 148 * 16));
 }
 
-int finalize_sym(cudaStream_t st, double* A, int64_t lda, int64_t n, int64_t w) {
-  if (n <= 0) return 0;
+int finalize_sym(cudaStream_t st, double* A, int64_t lda, int64_t n, int64_t w, int64_t c0,
+                 int64_t c1) {
+  if (c1 < 0) c1 = n;
+  if (n <= 0 || c1 <= c0) return 0;
   count_launch();
-  finalize_sym_kernel<<<grid_for(n * n), 256, 0, st>>>(A, lda, n, w);
+  finalize_sym_kernel<<<grid_for(n * (c1 - c0)), 256, 0, st>>>(A, lda, n, c0, c1 - c0, w);
   BR_CUDA(cudaGetLastError());
   return 0;
 }
 int mask_tri(cudaStream_t st, double* A, int64_t lda, int64_t m, int64_t n, int64_t lo,
-             int64_t up) {
-  if (m <= 0 || n <= 0) return 0;
+             int64_t up, int64_t c0, int64_t c1) {
+  if (c1 < 0) c1 = n;
+  if (m <= 0 || c1 <= c0) return 0;
   count_launch();
-  mask_band_kernel<<<grid_for(m * n), 256, 0, st>>>(A, lda, m, n, lo, up);
+  mask_band_kernel<<<grid_for(m * (c1 - c0)), 256, 0, st>>>(A, lda, m, c0, c1 - c0, lo, up);
   BR_CUDA(cudaGetLastError());
   return 0;
 }
@@ -197,6 +203,23 @@ int set_identity(cudaStream_t st, double* Q, int64_t ldq, int64_t n) {
   count_launch();
   identity_kernel<<<grid_for(n * n), 256, 0, st>>>(Q, ldq, n);
   BR_CUDA(cudaGetLastError());
+  return 0;
+}
+
+// Finish columns [done, upto) of the band on the copy stream (after the main
+// stream's work so far) and queue their D2H copy into the pinned host buffer.
+int band_out_flush(Workspace& ws, BandOut* bo, int64_t upto) {
+  if (!bo || upto <= bo->done) return 0;
+  cudaEvent_t ev = ws_event(ws);
+  BR_CUDA(cudaEventRecord(ev, ws.main));
+  BR_CUDA(cudaStreamWaitEvent(bo->st, ev, 0));
+  if (bo->sym) BR_CHECK(finalize_sym(bo->st, bo->A, bo->lda, bo->rows, bo->w, bo->done, upto));
+  else BR_CHECK(mask_tri(bo->st, bo->A, bo->lda, bo->rows, upto, bo->lo, bo->up, bo->done, upto));
+  BR_CUDA(cudaMemcpy2DAsync(bo->host + bo->done * bo->ldh, bo->ldh * sizeof(double),
+                            bo->A + bo->done * bo->lda, bo->lda * sizeof(double),
+                            bo->rows * sizeof(double), upto - bo->done, cudaMemcpyDeviceToHost,
+                            bo->st));
+  bo->done = upto;
   return 0;
 }
 int zero_fill(cudaStream_t st, MatView V) {
@@ -247,7 +270,8 @@ int timed_reduction(Workspace& ws, br_stats* stats, double nominal, Workspace::G
   key.timing = ws.timing;
   // events recorded by captured graph nodes cannot be timed, so the timing /
   // trace modes stay eager
-  const bool graphable = graphs_enabled(nominal) && ws.timing == 0 && ws.main != nullptr;
+  const bool graphable =
+      graphs_enabled(nominal) && ws.timing == 0 && ws.main != nullptr && ws.band_out == nullptr;
   const bool same = graphable && key == ws.gkey;
   int rc = 0;
   int64_t iters = 0;
@@ -394,6 +418,7 @@ int br_create(int device, br_handle_t* out) {
   h->ws.main = h->ws.own_main;
   h->ws.panel = h->ws.own_panel;
   BR_CUDA(cudaStreamCreateWithPriority(&h->ws.aux, cudaStreamNonBlocking, hi));
+  BR_CUDA(cudaStreamCreateWithFlags(&h->ws.copy, cudaStreamNonBlocking));
   BR_CUDA(cudaMalloc(&h->ws.flags, 128 * sizeof(unsigned)));
   BR_CUDA(cudaMemset(h->ws.flags, 0, 128 * sizeof(unsigned)));
   BR_CUDA(cudaEventCreateWithFlags(&h->ws.ev_aux0, cudaEventDisableTiming));
@@ -432,6 +457,7 @@ int br_destroy(br_handle_t h) {
   if (ws.ev_aux0) cudaEventDestroy(ws.ev_aux0);
   if (ws.ev_aux1) cudaEventDestroy(ws.ev_aux1);
   if (ws.aux) cudaStreamDestroy(ws.aux);
+  if (ws.copy) cudaStreamDestroy(ws.copy);
   for (auto e : ws.events) cudaEventDestroy(e);
   for (auto e : ws.tevents) cudaEventDestroy(e);
   if (ws.gexec) cudaGraphExecDestroy(ws.gexec);
@@ -737,7 +763,8 @@ int br_reduce_sym_band(br_handle_t h, int64_t n, int64_t w, int64_t b, int looka
   key.ldq = ldq;
   return timed_reduction(h->ws, stats, sevp_nominal(n), key,
                          [&](int64_t* it) {
-                           return sevp_reduce(h->ws, n, w, b, lookahead, A, lda, Q, ldq, it);
+                           return sevp_reduce(h->ws, n, w, b, lookahead, A, lda, Q, ldq, it,
+                                              h->ws.band_out);
                          });
 }
 
@@ -762,7 +789,8 @@ int br_reduce_tri_band(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b
   key.lda = lda;
   return timed_reduction(h->ws, stats, svd_nominal(m, n), key,
                          [&](int64_t* it) {
-                           return tri_reduce(h->ws, m, n, w, b, lookahead, A, lda, it);
+                           return tri_reduce(h->ws, m, n, w, b, lookahead, A, lda, it,
+                                             h->ws.band_out);
                          });
 }
 
@@ -790,8 +818,28 @@ int br_reduce_band(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b, in
   return timed_reduction(h->ws, stats, svd_nominal(m, n), key,
                          [&](int64_t* it) {
                            return band_reduce(h->ws, m, n, w, b, simultaneous, lookahead, A,
-                                              lda, it);
+                                              lda, it, h->ws.band_out);
                          });
+}
+
+// Stream the band out while reducing when the destination is pinned host
+// memory and the matrix is large (pageable D2H copies block the host thread).
+static bool setup_band_out(Workspace& ws, BandOut& bo, double* band, int64_t ldb, double* dA,
+                           int64_t ldd, int64_t m, int64_t n) {
+  cudaPointerAttributes pa;
+  const bool pinned = cudaPointerGetAttributes(&pa, band) == cudaSuccess &&
+                      pa.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  if (!pinned || m * n * (int64_t)sizeof(double) < ((int64_t)64 << 20)) return false;
+  bo.st = ws.copy;
+  bo.host = band;
+  bo.ldh = ldb;
+  bo.A = dA;
+  bo.lda = ldd;
+  bo.rows = m;
+  bo.done = 0;
+  ws.band_out = &bo;
+  return true;
 }
 
 static int host_stage_in(Workspace& ws, int64_t m, int64_t n, const double* A, int64_t lda,
@@ -822,9 +870,17 @@ int br_reduce_sym_band_host(br_handle_t h, int64_t n, int64_t w, int64_t b, int 
     BR_CHECK(devbuf_reserve(dQ, ldd * n));
     qd = dQ.p;
   }
-  BR_CHECK(br_reduce_sym_band(h, n, w, b, lookahead, dA.p, ldd, qd, ldd, stats));
-  BR_CUDA(cudaMemcpy2DAsync(band, ldb * sizeof(double), dA.p, ldd * sizeof(double),
-                            n * sizeof(double), n, cudaMemcpyDeviceToHost, ws.main));
+  BandOut bo;
+  bo.sym = true;
+  bo.w = w;
+  const bool streamed = setup_band_out(ws, bo, band, ldb, dA.p, ldd, n, n);
+  const int rc = br_reduce_sym_band(h, n, w, b, lookahead, dA.p, ldd, qd, ldd, stats);
+  ws.band_out = nullptr;
+  if (streamed) BR_CUDA(cudaStreamSynchronize(ws.copy));
+  BR_CHECK(rc);
+  if (!streamed)
+    BR_CUDA(cudaMemcpy2DAsync(band, ldb * sizeof(double), dA.p, ldd * sizeof(double),
+                              n * sizeof(double), n, cudaMemcpyDeviceToHost, ws.main));
   if (Q)
     BR_CUDA(cudaMemcpy2DAsync(Q, ldq * sizeof(double), dQ.p, ldd * sizeof(double),
                               n * sizeof(double), n, cudaMemcpyDeviceToHost, ws.main));
@@ -845,9 +901,17 @@ int br_reduce_tri_band_host(br_handle_t h, int64_t m, int64_t n, int64_t w, int6
   DevBuf& dA = ws.stageA;
   int64_t ldd = 0;
   BR_CHECK(host_stage_in(ws, m, n, A, lda, dA, ldd));
-  BR_CHECK(br_reduce_tri_band(h, m, n, w, b, lookahead, dA.p, ldd, stats));
-  BR_CUDA(cudaMemcpy2DAsync(band, ldb * sizeof(double), dA.p, ldd * sizeof(double),
-                            m * sizeof(double), n, cudaMemcpyDeviceToHost, ws.main));
+  BandOut bo;
+  bo.lo = 0;
+  bo.up = w;
+  const bool streamed = setup_band_out(ws, bo, band, ldb, dA.p, ldd, m, n);
+  const int rc = br_reduce_tri_band(h, m, n, w, b, lookahead, dA.p, ldd, stats);
+  ws.band_out = nullptr;
+  if (streamed) BR_CUDA(cudaStreamSynchronize(ws.copy));
+  BR_CHECK(rc);
+  if (!streamed)
+    BR_CUDA(cudaMemcpy2DAsync(band, ldb * sizeof(double), dA.p, ldd * sizeof(double),
+                              m * sizeof(double), n, cudaMemcpyDeviceToHost, ws.main));
   BR_CUDA(cudaStreamSynchronize(ws.main));
   return 0;
 }
@@ -865,9 +929,17 @@ int br_reduce_band_host(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t 
   DevBuf& dA = ws.stageA;
   int64_t ldd = 0;
   BR_CHECK(host_stage_in(ws, m, n, A, lda, dA, ldd));
-  BR_CHECK(br_reduce_band(h, m, n, w, b, simultaneous, lookahead, dA.p, ldd, stats));
-  BR_CUDA(cudaMemcpy2DAsync(band, ldb * sizeof(double), dA.p, ldd * sizeof(double),
-                            m * sizeof(double), n, cudaMemcpyDeviceToHost, ws.main));
+  BandOut bo;
+  bo.lo = w;
+  bo.up = w;
+  const bool streamed = setup_band_out(ws, bo, band, ldb, dA.p, ldd, m, n);
+  const int rc = br_reduce_band(h, m, n, w, b, simultaneous, lookahead, dA.p, ldd, stats);
+  ws.band_out = nullptr;
+  if (streamed) BR_CUDA(cudaStreamSynchronize(ws.copy));
+  BR_CHECK(rc);
+  if (!streamed)
+    BR_CUDA(cudaMemcpy2DAsync(band, ldb * sizeof(double), dA.p, ldd * sizeof(double),
+                              m * sizeof(double), n, cudaMemcpyDeviceToHost, ws.main));
   BR_CUDA(cudaStreamSynchronize(ws.main));
   return 0;
 }

@@ -57,6 +57,8 @@ struct Workspace {
     }
   };
   GraphKey gkey;
+  struct BandOut* band_out = nullptr;  // set by the host entry points while streaming out
+  cudaStream_t copy = nullptr;         // D2H stream of the streamed band
   int gseen = 0;  // eager runs of gkey so far
   cudaGraphExec_t gexec = nullptr;
   int64_t g_iters = 0, g_launches = 0;
@@ -132,18 +134,35 @@ int preload_gemm_kernels();
 int preload_panel_kernels();
 
 // Elementwise helpers (driver.cu)
-int finalize_sym(cudaStream_t st, double* A, int64_t lda, int64_t n, int64_t w);
+int finalize_sym(cudaStream_t st, double* A, int64_t lda, int64_t n, int64_t w, int64_t c0 = 0,
+                 int64_t c1 = -1);
 int mask_tri(cudaStream_t st, double* A, int64_t lda, int64_t m, int64_t n, int64_t lower_bw,
-             int64_t upper_bw);
+             int64_t upper_bw, int64_t c0 = 0, int64_t c1 = -1);
+
+// Host entry points with a pinned destination: finished column blocks are
+// finalized and copied out on a copy stream while the reduction continues
+// (after iteration k, columns [0, k + bp) are final in all three reductions).
+struct BandOut {
+  cudaStream_t st = nullptr;
+  double* host = nullptr;
+  int64_t ldh = 0;
+  double* A = nullptr;
+  int64_t lda = 0, rows = 0;
+  bool sym = false;  // SEVP finalize (mirror + zero) instead of the band mask
+  int64_t w = 0, lo = 0, up = 0;
+  int64_t done = 0;  // columns already queued
+};
+int band_out_flush(Workspace& ws, BandOut* bo, int64_t upto);
 int zero_fill(cudaStream_t st, MatView V);
 int set_identity(cudaStream_t st, double* Q, int64_t ldq, int64_t n);
 
 // Reductions (reduce.cu)
 int sevp_reduce(Workspace& ws, int64_t n, int64_t w, int64_t b, int lookahead, double* A,
-                int64_t lda, double* Q, int64_t ldq, int64_t* iterations);
+                int64_t lda, double* Q, int64_t ldq, int64_t* iterations, BandOut* bo = nullptr);
 int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lookahead,
-               double* A, int64_t lda, int64_t* iterations);
+               double* A, int64_t lda, int64_t* iterations, BandOut* bo = nullptr);
 int band_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int fused,
-                int lookahead, double* A, int64_t lda, int64_t* iterations);
+                int lookahead, double* A, int64_t lda, int64_t* iterations,
+                BandOut* bo = nullptr);
 
 }  // namespace br

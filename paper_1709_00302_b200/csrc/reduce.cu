@@ -52,11 +52,18 @@ static double panel_flops(int64_t j, int64_t b) {
 // SEVP
 // ---------------------------------------------------------------------------
 int sevp_reduce(Workspace& ws, int64_t n, int64_t w, int64_t b, int lookahead, double* A,
-                int64_t lda, double* Q, int64_t ldq, int64_t* iterations) {
+                int64_t lda, double* Q, int64_t ldq, int64_t* iterations, BandOut* bo) {
   std::vector<int64_t> ks;
   for (int64_t k = 0; n - k - w >= 2; k += std::min(b, n - k - w)) ks.push_back(k);
   *iterations = (int64_t)ks.size();
-  if (ks.empty()) return 0;  // n <= w + 1: input returned unchanged (sevp.py:302-305)
+  if (ks.empty()) {  // n <= w + 1: input returned unchanged (sevp.py:302-305)
+    if (bo) {
+      BR_CUDA(cudaMemcpy2DAsync(bo->host, bo->ldh * sizeof(double), A, lda * sizeof(double),
+                                n * sizeof(double), n, cudaMemcpyDeviceToHost, ws.main));
+      bo->done = n;
+    }
+    return 0;
+  }
 
   const int64_t jmax = n - w;
   // factor buffers: Y[2], W[2] (jmax x b), T[2] (b x b), tau[2] (b), X1, X3
@@ -192,6 +199,12 @@ int sevp_reduce(Workspace& ws, int64_t n, int64_t w, int64_t b, int lookahead, d
       BR_CHECK(accq());
       if (has_next) BR_CHECK(do_panel(ws.main, ws.sk_main, kn, par ^ 1));
     }
+    BR_CHECK(band_out_flush(ws, bo, k + bp));  // columns [0, k + bp) are final
+  }
+  if (bo) {
+    BR_CHECK(band_out_flush(ws, bo, n));
+    ws_events_reset(ws);
+    return 0;
   }
   ws_events_reset(ws);
   return finalize_sym(ws.main, A, lda, n, w);
@@ -201,7 +214,7 @@ int sevp_reduce(Workspace& ws, int64_t n, int64_t w, int64_t b, int lookahead, d
 // Triangular-band SVD
 // ---------------------------------------------------------------------------
 int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lookahead,
-               double* A, int64_t lda, int64_t* iterations) {
+               double* A, int64_t lda, int64_t* iterations, BandOut* bo) {
   struct It {
     int64_t k, bp;
   };
@@ -212,7 +225,10 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
     k += bp;
   }
   *iterations = (int64_t)its.size();
-  if (its.empty()) return mask_tri(ws.main, A, lda, m, n, 0, w);
+  if (its.empty()) {
+    if (bo) return band_out_flush(ws, bo, n);
+    return mask_tri(ws.main, A, lda, m, n, 0, w);
+  }
 
   const int64_t nYu = m * b, nYv = n * b, nT = b * b;
   const int64_t total = 4 * nYu + 2 * nT + 2 * b + 2 * nYv + nT + b + b * n + m * b;
@@ -366,8 +382,14 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
       if (la) BR_CHECK(next_qr_on_panel());
       else BR_CHECK(qr(ws.main, ws.sk_main, kn, bpn, par ^ 1));
     }
+    BR_CHECK(band_out_flush(ws, bo, k + bp));  // columns [0, k + bp) are final
   }
   if (ev_qr) BR_CHECK(join(ev_qr));
+  if (bo) {
+    BR_CHECK(band_out_flush(ws, bo, n));
+    ws_events_reset(ws);
+    return 0;
+  }
   ws_events_reset(ws);
   return mask_tri(ws.main, A, lda, m, n, 0, w);
 }
@@ -392,7 +414,7 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
 // the split-K chunk planned for its whole product, so depth 1 is bitwise
 // equal to depth 0.
 int band_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int fused,
-                int lookahead, double* A, int64_t lda, int64_t* iterations) {
+                int lookahead, double* A, int64_t lda, int64_t* iterations, BandOut* bo) {
   struct It {
     int64_t k, bp, jr, bq;
   };
@@ -404,7 +426,14 @@ int band_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int f
     k += bp;
   }
   *iterations = (int64_t)its.size();
-  if (its.empty()) return 0;  // m <= w + 1: returned unchanged (ref svd.py:561-564)
+  if (its.empty()) {  // m <= w + 1: returned unchanged (ref svd.py:561-564)
+    if (bo) {
+      BR_CUDA(cudaMemcpy2DAsync(bo->host, bo->ldh * sizeof(double), A, lda * sizeof(double),
+                                m * sizeof(double), n, cudaMemcpyDeviceToHost, ws.main));
+      bo->done = n;
+    }
+    return 0;
+  }
 
   const int64_t nYu = m * b, nYv = n * b, nT = b * b;
   const int64_t total = 4 * nYu + 4 * nYv + 4 * nT + 4 * b + b * n + 2 * m * b + nT;
@@ -601,8 +630,14 @@ int band_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int f
       }
     }
     if (has_next && !issued) BR_CHECK(panels(ws.main, ws.sk_main, tn, par ^ 1));
+    BR_CHECK(band_out_flush(ws, bo, std::min(n, t.k + t.bp)));  // columns [0, k + bp) are final
   }
   if (ev_panels) BR_CUDA(cudaStreamWaitEvent(ws.main, ev_panels, 0));
+  if (bo) {
+    BR_CHECK(band_out_flush(ws, bo, n));
+    ws_events_reset(ws);
+    return 0;
+  }
   ws_events_reset(ws);
   return mask_tri(ws.main, A, lda, m, n, w, w);
 }

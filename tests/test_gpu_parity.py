@@ -437,3 +437,39 @@ def test_persistent_panel_mode_matches(tmp_path):
         assert r.returncode == 0, r.stderr
         outs.append(np.load(path))
     assert np.max(np.abs(outs[0] - outs[1])) <= 1e-12 * np.max(np.abs(outs[0]))
+
+
+@pytest.mark.parametrize("kind", ["sevp", "tri", "band"])
+def test_streamed_band_output_matches(br, kind):
+    """Host entry points with a pinned destination finalize and copy finished
+    column blocks out while the reduction runs; the result is bitwise the one
+    of the pageable (single final copy) path."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1709_00302_b200 import _lib
+
+    lib = _lib.load()
+    h = _lib.handle(0)
+    n, w, b = 3000, 48, 48  # 72 MB: above the streaming threshold
+    A = sym(n, 31) if kind == "sevp" else rand(n, n, 31)
+    Ah = torch.from_numpy(np.asfortranarray(A).T.copy()).pin_memory()
+    outs = []
+    for pinned in (True, False):
+        Bt = torch.empty((n, n), dtype=torch.float64)
+        if pinned:
+            Bt = Bt.pin_memory()
+        st = _lib.BrStats()
+        if kind == "sevp":
+            rc = lib.br_reduce_sym_band_host(h, n, w, b, 1, Ah.data_ptr(), n, Bt.data_ptr(), n,
+                                             None, 0, st)
+        elif kind == "tri":
+            rc = lib.br_reduce_tri_band_host(h, n, n, w, b, 1, Ah.data_ptr(), n, Bt.data_ptr(), n, st)
+        else:
+            rc = lib.br_reduce_band_host(h, n, n, w, b, 1, 1, Ah.data_ptr(), n, Bt.data_ptr(), n, st)
+        _lib.check(rc, kind)
+        outs.append(Bt.numpy().T.copy())
+    assert np.array_equal(outs[0], outs[1])
+    lo, up = {"sevp": (w, w), "tri": (0, w), "band": (w, w)}[kind]
+    assert br.band_check(outs[0], lo, up) == 0.0
