@@ -142,6 +142,29 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   unsigned gstep = 0;  // exchange rounds so far (mbarrier buffer / phase)
+  // this lane's push targets (slot pair c of this CTA -> CTA q), mapped once
+  // (only for the 32-wide leaves: for the narrow ones the extra registers
+  // cost more than the per-step index math they save, measured)
+  constexpr bool PRE = NB >= 32;
+  constexpr int NPP = SPW / 2;  // slot pairs per pushing warp
+  constexpr int MAXT = PRE ? (NPP * LEAF_MAXC + 31) / 32 : 1;
+  uint32_t ra_recv[MAXT], ra_row[MAXT], ra_mbar[MAXT];
+  int tc_[MAXT];
+#pragma unroll
+  for (int tt = 0; tt < MAXT && PRE; ++tt) {
+    const int t = tt * 32 + lane;
+    tc_[tt] = -1;
+    ra_recv[tt] = ra_row[tt] = ra_mbar[tt] = 0;
+    if (warp < NPW && t < NPP * (int)ncta) {
+      const int pp = t / (int)ncta;
+      const uint32_t q = (uint32_t)(t % (int)ncta);
+      const int c = warp * SPW + 2 * pp;
+      tc_[tt] = c;
+      ra_recv[tt] = map_cluster(&recv[0][rank][c], q);
+      ra_row[tt] = map_cluster(&recv_row[0][c], q);
+      ra_mbar[tt] = map_cluster(&mbar[0], q);
+    }
+  }
   // Persistent mode (a.nleaves > 1): the cluster factors the panel's leaves
   // one after another; between leaves the block update of the next leaf's
   // columns runs on the auxiliary stream (flags: done[s] -> aux, aux ->
@@ -213,7 +236,32 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
       __syncthreads();
       BR_PHASE(1);
       // ---- warp w sums and pushes slots [w*SPW, (w+1)*SPW) to every CTA ----
-      if (warp < NPW) {
+      if (PRE && warp < NPW) {
+        const bool push_row = owner_cta;
+#pragma unroll
+        for (int tt = 0; tt < MAXT; ++tt) {
+          const int c = tc_[tt];
+          if (c >= 0) {
+            double u0[LW], u1[LW];  // fixed pairwise tree over the warps
+#pragma unroll
+            for (int w = 0; w < LW; ++w) {
+              u0[w] = wred[w][c];
+              u1[w] = wred[w][c + 1];
+            }
+#pragma unroll
+            for (int h = LW / 2; h >= 1; h >>= 1)
+#pragma unroll
+              for (int w = 0; w < h; ++w) {
+                u0[w] += u0[w + h];
+                u1[w] += u1[w + h];
+              }
+            const uint32_t rm = ra_mbar[tt] + buf * 8u;
+            st_async_v2(ra_recv[tt] + buf * (uint32_t)(LEAF_MAXC * NB * 8), u0[0], u1[0], rm);
+            if (push_row)
+              st_async_v2(ra_row[tt] + buf * (uint32_t)(NB * 8), rowi[c], rowi[c + 1], rm);
+          }
+        }
+      } else if (!PRE && warp < NPW) {
         constexpr int NP = SPW / 2;  // slot pairs per warp
         const int ntask = NP * (int)ncta;
         const bool push_row = owner_cta;
@@ -236,9 +284,8 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
                 u0[w] += u0[w + h];
                 u1[w] += u1[w + h];
               }
-            const double s0 = u0[0], s1 = u1[0];
             const uint32_t rm = map_cluster(&mbar[buf], q);
-            st_async_v2(map_cluster(&recv[buf][rank][c], q), s0, s1, rm);
+            st_async_v2(map_cluster(&recv[buf][rank][c], q), u0[0], u1[0], rm);
             if (push_row) st_async_v2(map_cluster(&recv_row[buf][c], q), rowi[c], rowi[c + 1], rm);
           }
         }
