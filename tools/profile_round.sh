@@ -3,11 +3,11 @@
 # of the same command that exited 0. Outputs land in gpurun_out/.
 set -x
 mkdir -p gpurun_out
-CMD="python bench.py --config c4 --steps 1 --warmup 1 --no-cpu --e2e-steps 1"
+CMD="python tools/one_reduction.py c4"
 $CMD > gpurun_out/prof_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 40000 --csv \
     --log-file gpurun_out/launches_c4.csv $CMD > gpurun_out/ncu_launch.log 2>&1
-CMD1="python bench.py --config c1 --steps 1 --warmup 1 --no-cpu --e2e-steps 1"
+CMD1="python tools/one_reduction.py c1"
 $CMD1 > gpurun_out/prof_plain1.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv \
     --log-file gpurun_out/launches_c1.csv $CMD1 > gpurun_out/ncu_launch1.log 2>&1
