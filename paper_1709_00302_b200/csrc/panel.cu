@@ -54,7 +54,8 @@ struct LeafArgs {
 };
 
 }  // namespace br
-#include "panel_leaf.cuh"  // leaf_reg_kernel<NB, R, LT>
+#include "panel_leaf.cuh"   // leaf_reg_kernel<NB, R, LT>
+#include "panel_leaf2.cuh"  // leaf2_kernel<NB, NW>
 namespace br {
 
 // Rows one cluster holds at leaf width nb: 16 CTAs x 256 threads x R rows
@@ -125,6 +126,81 @@ static int launch_leaf_t(cudaStream_t st, const LeafArgs& a) {
   return 0;
 }
 
+// 2D-layout leaf (leaf2_kernel): NW warps of 8 columns x 256 rows each.
+template <int NB, int NW>
+static int launch_leaf2_t(cudaStream_t st, const LeafArgs& a) {
+  auto kern = leaf2_kernel<NB, NW>;
+  constexpr int ROWS = (NW / (NB / 8)) * 256;
+  int C = 1;
+  while (C < cdiv(a.L, ROWS)) C *= 2;
+  const size_t smem = (size_t)NB * ROWS * sizeof(double);
+  static int attr_dev_mask = 0;
+  int dev = 0;
+  BR_CUDA(cudaGetDevice(&dev));
+  if (!(attr_dev_mask & (1 << dev))) {
+    BR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    BR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_dev_mask |= (1 << dev);
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[3];
+  cfg.gridDim = dim3(C);
+  cfg.blockDim = dim3(NW * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  at[2].id = cudaLaunchAttributePriority;
+  at[2].val.priority = stream_priority(st);
+  cfg.attrs = at;
+  cfg.numAttrs = 3;
+  if (g_preload_only) {
+    cudaFuncAttributes fa;
+    BR_CUDA(cudaFuncGetAttributes(&fa, kern));
+    return 0;
+  }
+  count_launch();
+  BR_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+  return 0;
+}
+
+// BR_LEAF2=0 selects the 1D-layout leaf_reg_kernel everywhere (A/B aid);
+// BR_LEAF2_WIDE=1 prefers 8-warp CTAs (fewer CTAs per cluster).
+static int leaf2_mode() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = std::getenv("BR_LEAF2");
+    const char* w = std::getenv("BR_LEAF2_WIDE");
+    m = (e && std::atoi(e) == 0) ? 0 : ((w && std::atoi(w) == 1) ? 2 : 1);
+  }
+  return m;
+}
+
+// Launch the 2D-layout leaf when it covers (nb, L) (sets *done).
+static int launch_leaf2(cudaStream_t st, const LeafArgs& a, bool* done) {
+  const int mode = leaf2_mode();
+  *done = true;
+  if (mode == 0 || a.nleaves != 1) return *done = false, 0;
+  const int64_t L = a.L;
+  const bool wide = mode == 2;
+  if (a.nb > 32) return *done = false, 0;
+  if (a.nb > 16) {
+    if (!wide && L <= (int64_t)LEAF_MAXC * 256) return launch_leaf2_t<32, 4>(st, a);
+    if (L <= (int64_t)LEAF_MAXC * 512) return launch_leaf2_t<32, 8>(st, a);
+    return *done = false, 0;
+  }
+  if (L <= 256) return launch_leaf2_t<16, 2>(st, a);
+  if (!wide && L <= (int64_t)LEAF_MAXC * 512) return launch_leaf2_t<16, 4>(st, a);
+  // 16 x 1024-row CTAs (4 row groups): the 1D layout measured faster (16384 x 16:
+  // 53 vs 62 us), so the 8-warp 2D form is only taken with BR_LEAF2_WIDE=1
+  if (wide && L <= (int64_t)LEAF_MAXC * 1024) return launch_leaf2_t<16, 8>(st, a);
+  return *done = false, 0;
+}
+
 static int launch_leaf(cudaStream_t st, MatView P, MatView Y, double* tau, double* T, int64_t ldt,
                        MatView* W, int wt = 0, int nleaves = 1, int lw = 0,
                        unsigned* flags = nullptr, unsigned epoch = 0) {
@@ -159,6 +235,11 @@ static int launch_leaf(cudaStream_t st, MatView P, MatView Y, double* tau, doubl
       BR_CUDA(cudaMemset(g_leaf_prof, 0, 16 * sizeof(long long)));
     }
     a.prof = g_leaf_prof;
+  }
+  {
+    bool done = false;
+    const int r = launch_leaf2(st, a, &done);
+    if (done || r != 0) return r;
   }
   // 128-thread CTAs (one warp per SM sub-partition: the per-step reduction is
   // issue-bound per warp) while one cluster of them holds the leaf; 256
@@ -386,6 +467,17 @@ static int stream_set_flag(cudaStream_t st, unsigned* f, unsigned v) {
   return 0;
 }
 
+// Multi-leaf panels: the leaf forms Y T^T for the block update (default) or
+// the update applies T^T with one more small GEMM (BR_LEAF_W=0).
+static bool leaf_w_mode() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = std::getenv("BR_LEAF_W");
+    m = (e && std::atoi(e) == 0) ? 0 : 1;
+  }
+  return m == 1;
+}
+
 int64_t panel_scratch_doubles(int64_t b) {
   return b * b + LEAF_NB * LEAF_NB + 2 * LEAF_NB * b + (b > TAB_MAXB ? b * TAB_MAXB : 0);
 }
@@ -455,7 +547,7 @@ int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView 
     const int64_t w = e - s;
     MatView leafP = P.sub(s, s, j - s, w);
     MatView leafY = Y.sub(s, s, j - s, w);
-    if (e < b && W) {
+    if (e < b && W && leaf_w_mode()) {
       // P[s:, e:b] += (Y_blk T_blk^T)(Y_blk^T P[s:, e:b]); the leaf writes
       // Y_blk T_blk^T into W's columns (W itself is formed at the end)
       MatView What = W->sub(s, s, j - s, w);
@@ -540,6 +632,11 @@ int preload_panel_kernels() {
   BR_CHECK((launch_leaf_t<16, 4, 256>(0, a)));
   BR_CHECK((launch_leaf_t<8, 8, 128>(0, a)));
   BR_CHECK((launch_leaf_t<8, 8, 256>(0, a)));
+  BR_CHECK((launch_leaf2_t<32, 4>(0, a)));
+  BR_CHECK((launch_leaf2_t<32, 8>(0, a)));
+  BR_CHECK((launch_leaf2_t<16, 2>(0, a)));
+  BR_CHECK((launch_leaf2_t<16, 4>(0, a)));
+  BR_CHECK((launch_leaf2_t<16, 8>(0, a)));
   cudaFuncAttributes fa;
   BR_CUDA(cudaFuncGetAttributes(&fa, t_assemble_kernel));
   BR_CUDA(cudaFuncGetAttributes(&fa, house_gen_kernel));

@@ -13,6 +13,20 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* m, uint32_t byte
                "r"(bytes)
                : "memory");
 }
+// CTA-scope acquire: the st.async bytes land in this CTA's shared memory and
+// are complete when the phase flips; a cluster-scope acquire would also
+// invalidate L1 (CCTL.IVALL) on every poll, which measured as the largest
+// single stall of the leaf's step loop.
+__device__ __forceinline__ bool mbar_try_wait_cta(uint64_t* m, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+      "selp.u32 %0, 1, 0, p; }"
+      : "=r"(ok)
+      : "r"(smem_u32(m)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* m, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -291,7 +305,7 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
         }
       }
       BR_PHASE(2);
-      while (!mbar_try_wait(&mbar[buf], (gstep >> 1) & 1)) {
+      while (!mbar_try_wait_cta(&mbar[buf], (gstep >> 1) & 1)) {
       }
       BR_PHASE(3);
       // ---- every warp: the same scalars from the same received vectors ----

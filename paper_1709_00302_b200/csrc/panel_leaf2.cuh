@@ -1,0 +1,423 @@
+// Register-resident cluster leaf, 2D thread layout (included by panel.cu).
+#pragma once
+#include "common.cuh"
+
+namespace br {
+
+__device__ __forceinline__ void st_async_f64(uint32_t raddr, double a, uint32_t rmbar) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(raddr),
+      "d"(a), "r"(rmbar)
+      : "memory");
+}
+
+// One leaf (L x nb, nb <= NB, NB in {16, 32}) of a Householder panel, same
+// outputs and arithmetic contract as leaf_reg_kernel (Y, tau, T, W, R rows of
+// P), with a 2D layout: warp w owns the 8 columns 8*(w % CG) .. +8 (CG = NB/8
+// column groups) of the 256 rows of its row group rg = w / CG, and lane l of
+// it rows rg*256 + 32 r + l (r < 8) of the CTA's block: 8 x 8 doubles per
+// thread, nothing rotates, every index is compile-time inside the unrolled
+// 8-column sweep of a column group.
+//
+// Step i (column i lives in column group cg = i / 8, register column ci):
+//   1. the owner warps publish x = column i (rows >= i, zero above) to shared
+//      memory; CTA 0's lane i publishes row i; one __syncthreads;
+//   2. every warp forms its 8 partial sums x^T p[.][c] over its rows plus
+//      ||x||^2 and transpose-reduces them (9 + 5 shuffles instead of the 32
+//      slots per warp of the 1D layout); the slot of a finished column is the
+//      Gram entry x^T Y_y, as in leaf_reg_kernel;
+//   3. exchange (several CTAs or row groups): every warp pushes its 8 slot
+//      totals (st.async, completing bytes on the receiver's mbarrier) to every
+//      CTA; with one CTA and one row group the warp already has the totals;
+//   4. every warp forms the same scalars from the same data in the same
+//      order: beta = -sign(x0)||x||, alpha_c = P_ic - (x^T P_c)/beta,
+//      v = x / (x0 - beta), and updates its columns.
+// Deterministic: all CTAs sum the same received vectors in the same order.
+template <int NB, int NW>
+__global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
+  constexpr int CG = NB / 8;      // column groups
+  constexpr int RG = NW / CG;     // row groups (256 rows each)
+  constexpr int ROWS = RG * 256;  // rows per CTA
+  constexpr int NT = NW * 32;
+  constexpr int MAXSRC = LEAF_MAXC * RG;
+  static_assert(CG * RG == NW && RG >= 1, "warp layout");
+  extern __shared__ __align__(16) double Ys[];  // [NB][ROWS], epilogue only
+  __shared__ __align__(16) double xs[2][ROWS];
+  __shared__ __align__(16) double rowl[2][NB];           // row i (CTA 0 local)
+  __shared__ __align__(16) double recv[2][MAXSRC][NB];   // slot partials per source
+  __shared__ __align__(16) double recvn[2][MAXSRC];      // ||x||^2 partials per source
+  __shared__ __align__(16) double recvr[2][NB];          // row i from CTA 0
+  __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ double scal[NB][3];  // x0 -> tau, beta, rinv
+  __shared__ double G[NB][NB + 1];
+  __shared__ double Ts[NB][NB + 1];
+
+  const uint32_t rank = cluster_ctarank(), ncta = cluster_nctarank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wcg = warp % CG, rg = warp / CG;
+  const int64_t base = (int64_t)rank * ROWS;
+  const int lrow0 = rg * 256 + lane;  // local row of register row r: lrow0 + 32 r
+  const int64_t gr0 = base + lrow0;
+  const bool xch = (ncta > 1) || (RG > 1);
+  const int nsrc = (int)ncta * RG;
+  const int nb = a.nb;
+  const int64_t Lr = a.L;
+  const MatView P = a.P;
+  constexpr unsigned FULL = 0xffffffffu;
+
+#ifdef BR_LEAF_PROF  // phase counters: build with BR_BUILD_PROF=1, run with BR_LEAF_PROF=1
+  const bool pr = a.prof != nullptr && rank == 0 && tid == 0;
+  long long tp[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long tc = pr ? clock64() : 0;
+#define BR_PHASE2(k)                \
+  if (pr) {                         \
+    const long long t_ = clock64(); \
+    tp[k] += t_ - tc;               \
+    tc = t_;                        \
+  }
+#else
+#define BR_PHASE2(k)
+#endif
+  pdl_wait();  // the panel columns were written by the previous kernel
+  if (xch && tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  double p[8][8];
+  {
+    // branch-free addressing of the (possibly transposed) view
+    const int64_t rs = P.trans ? P.ld : 1, cs = P.trans ? 1 : P.ld;
+    const double* pb = P.p + gr0 * rs + (int64_t)(wcg * 8) * cs;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const bool rok = gr0 + 32 * r < Lr;
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        p[r][c] = (rok && wcg * 8 + c < nb) ? __ldcg(pb + (32 * r) * rs + c * cs) : 0.0;
+    }
+  }
+  if (xch) cluster_sync_all();  // mbarriers initialized cluster-wide before any st.async
+  BR_PHASE2(7);
+
+  // The owner warps of column group cg rotate their 8 register columns left
+  // by one per step (the finished Y column moves to the end), so the current
+  // column is always p[r][0] and every register index stays compile-time with
+  // a non-unrolled step loop (the unrolled 8-step sweep overflowed the
+  // instruction cache). Register slot s of an owner warp holds column
+  // (ci + s) & 7 of its group; slot-ordered exchange buffers need no remap.
+  // rows < 32 (the only ones that can lie above the pivot) are register row 0
+  // of row group 0 in CTA 0
+  const bool top = (rank == 0 && rg == 0);
+  // remote addresses of this lane's pushes (buffer 0; buffer 1 at a fixed offset)
+  const int src = (int)rank * RG + rg;
+  const int pu = lane & 7, ppair = lane >> 3;
+  uint32_t ra_s[2] = {0, 0}, ra_sm[2] = {0, 0}, ra_n = 0, ra_nm = 0, ra_r[2] = {0, 0},
+           ra_rm[2] = {0, 0};
+  unsigned vmask = 0;  // bit k: slot push k, bit 2 + k: row-i push k, bit 4: norm push
+  if (xch) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int q = pu + 8 * k;
+      if (q < (int)ncta) {
+        vmask |= 1u << k;
+        ra_s[k] = map_cluster(&recv[0][src][wcg * 8 + 2 * ppair], (uint32_t)q);
+        ra_sm[k] = map_cluster(&mbar[0], (uint32_t)q);
+      }
+      const int t = lane + 32 * k;  // row-i pushes (CTA 0, row group 0): pair t & 3 -> CTA t >> 2
+      if (top && t < 4 * (int)ncta) {
+        vmask |= 4u << k;
+        ra_r[k] = map_cluster(&recvr[0][wcg * 8 + 2 * (t & 3)], (uint32_t)(t >> 2));
+        ra_rm[k] = map_cluster(&mbar[0], (uint32_t)(t >> 2));
+      }
+    }
+    if (lane < (int)ncta && wcg == 0) {
+      vmask |= 16u;
+      ra_n = map_cluster(&recvn[0][src], (uint32_t)lane);
+      ra_nm = map_cluster(&mbar[0], (uint32_t)lane);
+    }
+  }
+  constexpr uint32_t RECV_B = MAXSRC * NB * 8, RECVN_B = MAXSRC * 8, RECVR_B = NB * 8;
+  constexpr int SPL = MAXSRC / 4;  // sources summed per lane (4 lanes per slot)
+
+#pragma unroll 1
+  for (int i = 0; i < nb; ++i) {
+    const int cg = i >> 3, ci = i & 7;
+    const bool own = (wcg == cg);
+    const int buf = i & 1;
+    const bool above0 = top && lane < i;  // register row 0 lies above the pivot
+    const bool piv0 = top && lane == i;   // register row 0 is the pivot row
+    if (xch && tid == 0) mbar_arrive_expect_tx(&mbar[buf], (uint32_t)(nsrc * (NB + 1) * 8 + NB * 8));
+    // ---- 1. publish x (owner warps) and row i (CTA 0, row group 0, lane i) ----
+    if (own) {
+      xs[buf][lrow0] = above0 ? 0.0 : p[0][0];
+#pragma unroll
+      for (int r = 1; r < 8; ++r) xs[buf][lrow0 + 32 * r] = p[r][0];
+    }
+    if (piv0) {
+#pragma unroll
+      for (int c = 0; c < 8; c += 2)
+        *reinterpret_cast<double2*>(&rowl[buf][wcg * 8 + c]) = make_double2(p[0][c], p[0][c + 1]);
+    }
+    __syncthreads();
+    BR_PHASE2(1);
+    if (xch && top) {  // row i to every CTA: 4 slot pairs x ncta
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+        if (vmask & (4u << k)) {
+          const int c = wcg * 8 + 2 * (lane & 3);
+          st_async_v2(ra_r[k] + buf * RECVR_B, rowl[buf][c], rowl[buf][c + 1], ra_rm[k] + buf * 8u);
+        }
+    }
+    // ---- 2. partial sums over this warp's rows ----
+    double xv[8], s[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) xv[r] = xs[buf][lrow0 + 32 * r];
+    double nr0 = 0.0, nr1 = 0.0;
+#pragma unroll
+    for (int r = 0; r < 8; r += 2) {
+      nr0 = fma(xv[r], xv[r], nr0);
+      nr1 = fma(xv[r + 1], xv[r + 1], nr1);
+    }
+    const double nr = warp_sum(nr0 + nr1);  // independent of the slots: overlaps them
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+      for (int r = 0; r < 8; r += 2) {
+        t0 = fma(xv[r], p[r][c], t0);
+        t1 = fma(xv[r + 1], p[r + 1][c], t1);
+      }
+      s[c] = t0 + t1;
+    }
+    warp_transpose_reduce<8>(s, lane);  // s[0]: warp total of register slot lane / 4
+    const int sl = lane >> 2;
+    BR_PHASE2(0);
+    double tot, nrm2;
+    if (!xch) {
+      tot = s[0];
+      nrm2 = nr;
+    } else {
+      // ---- 3. push slot pairs (and the norm from column group 0) to every CTA ----
+      const double oth = __shfl_xor_sync(FULL, s[0], 4);
+      const double v0 = (pu < 4) ? s[0] : oth, v1 = (pu < 4) ? oth : s[0];
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+        if (vmask & (1u << k)) st_async_v2(ra_s[k] + buf * RECV_B, v0, v1, ra_sm[k] + buf * 8u);
+      if (vmask & 16u) st_async_f64(ra_n + buf * RECVN_B, nr, ra_nm + buf * 8u);
+      BR_PHASE2(2);
+      while (!mbar_try_wait_cta(&mbar[buf], (i >> 1) & 1)) {
+      }
+      BR_PHASE2(3);
+      // slot sl and the norm: the 4 lanes of a slot split the sources (all
+      // loads issued at once), then a fixed two-level tree
+      const int c = wcg * 8 + sl, q4 = lane & 3;
+      double ts[SPL], tn[SPL];
+#pragma unroll
+      for (int k = 0; k < SPL; ++k) {
+        const int sidx = q4 + 4 * k;
+        ts[k] = (sidx < nsrc) ? recv[buf][sidx][c] : 0.0;
+        tn[k] = (sidx < nsrc) ? recvn[buf][sidx] : 0.0;
+      }
+#pragma unroll
+      for (int h = SPL / 2; h >= 1; h >>= 1)
+#pragma unroll
+        for (int k = 0; k < h; ++k) {
+          ts[k] += ts[k + h];
+          tn[k] += tn[k + h];
+        }
+      ts[0] += __shfl_xor_sync(FULL, ts[0], 1);
+      tn[0] += __shfl_xor_sync(FULL, tn[0], 1);
+      ts[0] += __shfl_xor_sync(FULL, ts[0], 2);
+      tn[0] += __shfl_xor_sync(FULL, tn[0], 2);
+      tot = ts[0];
+      nrm2 = tn[0];
+    }
+    // ---- 4. scalars (identical in every warp and CTA) ----
+    const double* rowv = xch ? recvr[buf] : rowl[buf];
+    const double x0 = rowv[cg * 8];                      // owner slot 0 = column i
+    const double pic = rowv[wcg * 8 + sl];                // row i of this lane's slot
+    const int cs = wcg * 8 + (own ? ((ci + sl) & 7) : sl);  // its column
+    double beta = 0.0, rb = 0.0, rinv = 0.0;
+    if (nrm2 != 0.0) {
+      // ||x|| and 1/||x|| from one rsqrt, 1/(x0 - beta) by rcp (as leaf_reg_kernel)
+      const double rs = rsqrt(nrm2), nrm = nrm2 * rs;
+      beta = (x0 < 0.0) ? nrm : -nrm;
+      rb = (x0 < 0.0) ? rs : -rs;
+      rinv = __drcp_rn(x0 - beta);
+    }
+    const double alpha = (nrm2 != 0.0 && cs > i && cs < nb) ? fma(-tot, rb, pic) : 0.0;
+    if (cs < i && rg == 0 && (lane & 3) == 0) G[cs][i] = fma(fma(-pic, x0, tot), rinv, pic);
+    if (tid == 0) {
+      scal[i][0] = x0;
+      scal[i][1] = beta;
+      scal[i][2] = rinv;
+    }
+    BR_PHASE2(4);
+    if (wcg >= cg) {  // earlier groups hold finished Y columns only
+      double al[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) al[c] = __shfl_sync(FULL, alpha, 4 * c);
+      double vk[8];
+      vk[0] = piv0 ? 1.0 : xv[0] * rinv;  // 0 above row i (x masked)
+#pragma unroll
+      for (int r = 1; r < 8; ++r) vk[r] = xv[r] * rinv;
+      if (own) {  // rotate: slot s <- slot s+1 updated; Y column i (R kept above) to slot 7
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const double x = p[r][0];
+#pragma unroll
+          for (int c = 0; c < 7; ++c) p[r][c] = fma(-vk[r], al[c + 1], p[r][c + 1]);
+          p[r][7] = (r == 0 && above0) ? x : vk[r];
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) p[r][c] = fma(-vk[r], al[c], p[r][c]);
+      }
+    }
+    BR_PHASE2(6);
+  }
+  // a partial last group leaves its owners rotated by nb & 7: finish the turn
+  if (nb & 7) {
+    if (wcg == ((nb - 1) >> 3)) {
+#pragma unroll 1
+      for (int t = nb & 7; t < 8; ++t) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const double x = p[r][0];
+#pragma unroll
+          for (int c = 0; c < 7; ++c) p[r][c] = p[r][c + 1];
+          p[r][7] = x;
+        }
+      }
+    }
+  }
+  pdl_trigger();
+  __syncthreads();  // scal / G complete
+  BR_PHASE2(5);
+  // ---- T by the reference recurrence (ref kernels.py:152-162), warp 0, while
+  // the other warps store Y; then warp 0 stores its own Y ----
+  auto store_y = [&]() {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int lrow = lrow0 + 32 * r;
+      const int64_t row = base + lrow;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int col = wcg * 8 + c;
+        const double y = (col < nb && row >= col) ? p[r][c] : 0.0;
+        Ys[col * ROWS + lrow] = y;
+        if (col < nb && row < Lr) a.Y[row + (int64_t)col * a.ldy] = y;
+      }
+    }
+    if (top && lane < nb) {  // R rows
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int col = wcg * 8 + c;
+        if (col >= lane && col < nb) *P.at(lane, col) = (col == lane) ? scal[lane][1] : p[0][c];
+      }
+    }
+  };
+  if (warp == 0) {
+    // tau = (beta - x0) / beta (ref kernels.py:109), lane i -> slot i
+    double tau_l = 0.0;
+    if (lane < nb) {
+      const double be = scal[lane][1];
+      tau_l = (be != 0.0) ? (be - scal[lane][0]) / be : 0.0;
+    }
+    const int r = lane;
+    double tr[NB];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) tr[c] = (c == r && r < nb) ? -tau_l : 0.0;
+#pragma unroll
+    for (int i = 1; i < NB; ++i) {
+      const double ti = __shfl_sync(FULL, tau_l, i);
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int c = 0; c + 1 < i; c += 2) {
+        s0 = fma(tr[c], G[c][i], s0);
+        s1 = fma(tr[c + 1], G[c + 1][i], s1);
+      }
+      if (i & 1) s0 = fma(tr[i - 1], G[i - 1][i], s0);
+      if (i > r && i < nb) tr[i] = -ti * (s0 + s1);
+    }
+    if (lane < NB) {
+#pragma unroll
+      for (int c = 0; c < NB; ++c) Ts[r][c] = tr[c];
+    }
+    if (lane < nb) scal[lane][0] = tau_l;  // every read of scal[.][0] (x0) precedes this
+    __syncwarp();
+    store_y();
+  } else {
+    store_y();
+  }
+  __syncthreads();
+  BR_PHASE2(8);
+  // ---- W = Y T (or Y T^T) on the tensor cores ----
+  if (a.W) {
+    const int gq = lane >> 2, tq = lane & 3;
+    constexpr int U = 4;
+    for (int rb = warp * 8; rb < ROWS; rb += NW * 8 * U) {
+      if (base + rb >= Lr) break;
+      double acc[U][NB / 8][2];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int n = 0; n < NB / 8; ++n) acc[u][n][0] = acc[u][n][1] = 0.0;
+#pragma unroll
+      for (int k0 = 0; k0 < NB; k0 += 4) {
+        double bt[NB / 8];
+#pragma unroll
+        for (int n = 0; n < NB / 8; ++n)
+          bt[n] = a.wt ? Ts[n * 8 + gq][k0 + tq] : Ts[k0 + tq][n * 8 + gq];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int r0 = rb + u * NW * 8;
+          const double av = (r0 < ROWS) ? Ys[(k0 + tq) * ROWS + r0 + gq] : 0.0;
+#pragma unroll
+          for (int n = 0; n < NB / 8; ++n) {
+            if (!a.wt && k0 >= n * 8 + 8) continue;  // zero blocks of the triangular T
+            if (a.wt && k0 + 4 <= n * 8) continue;
+            dmma884(acc[u][n][0], acc[u][n][1], av, bt[n]);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int r0 = rb + u * NW * 8;
+        const int64_t row = base + r0 + gq;
+        if (r0 < ROWS && row < Lr) {
+#pragma unroll
+          for (int n = 0; n < NB / 8; ++n)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int c = n * 8 + 2 * tq + h;
+              if (c < nb) a.W[row + (int64_t)c * a.ldw] = acc[u][n][h];
+            }
+        }
+      }
+    }
+  }
+  BR_PHASE2(10);
+#ifdef BR_LEAF_PROF
+  if (pr) {
+    for (int k = 0; k < 11; ++k) atomicAdd((unsigned long long*)&a.prof[k], (unsigned long long)tp[k]);
+    atomicAdd((unsigned long long*)&a.prof[11], (unsigned long long)nb);
+    atomicAdd((unsigned long long*)&a.prof[12], 1ull);
+  }
+#endif
+#undef BR_PHASE2
+  if (rank == 0) {
+    if (tid < nb) a.tau[tid] = scal[tid][0];
+    if (a.T)
+      for (int q = tid; q < nb * nb; q += NT) {
+        const int r = q % nb, c = q / nb;
+        a.T[r + (int64_t)c * a.ldt] = Ts[r][c];
+      }
+  }
+  if (xch) cluster_sync_all();  // no remote traffic is in flight when any CTA exits
+}
+
+}  // namespace br

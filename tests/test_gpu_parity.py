@@ -473,3 +473,39 @@ def test_streamed_band_output_matches(br, kind):
     assert np.array_equal(outs[0], outs[1])
     lo, up = {"sevp": (w, w), "tri": (0, w), "band": (w, w)}[kind]
     assert br.band_check(outs[0], lo, up) == 0.0
+
+
+@pytest.mark.gpu
+def test_leaf_layouts_agree(tmp_path):
+    """The 2D-layout leaf (default; 1 CTA without exchange, clusters of 4- or
+    8-warp CTAs) and the 1D-layout leaf (BR_LEAF2=0) factor the same panels
+    to rounding, including zero columns and zero tails."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, paper_1709_00302_b200 as br\n"
+        "out = []\n"
+        "for j, b, s in [(200, 32, 1), (3000, 32, 2), (6000, 32, 3), (250, 12, 4), (5000, 16, 5),\n"
+        "                (12000, 16, 6), (777, 29, 7), (4096, 256, 8)]:\n"
+        "    A = np.random.default_rng(s).standard_normal((j, b))\n"
+        "    if s == 7:\n"
+        "        A[:, 3] = 0.0; A[5:, 9] = 0.0\n"
+        "    P = br.qr_panel(np.asfortranarray(A))\n"
+        "    out += [P.y, P.w, P.t, P.r_or_l, P.tau]\n"
+        "np.savez(r'%s', *out)\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for mode in ({"BR_LEAF2": "0"}, {"BR_LEAF2": "1"}, {"BR_LEAF2": "1", "BR_LEAF2_WIDE": "1"}):
+        path = tmp_path / f"leaf{len(outs)}.npz"
+        env = dict(os.environ, **mode)
+        r = subprocess.run([sys.executable, "-c", code % path], cwd=root, env=env,
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        z = np.load(path)
+        outs.append([z[k] for k in sorted(z.files, key=lambda s: int(s.split("_")[1]))])
+    for other in outs[1:]:
+        for a, b in zip(outs[0], other):
+            assert a.shape == b.shape
+            assert np.max(np.abs(a - b)) <= 1e-12 * max(1.0, np.max(np.abs(a)))

@@ -10,7 +10,7 @@ __global__ void lat(double* out, long long* t, int n) {
   long long t1 = clock64();
   for (int i = 0; i < n; ++i) a = fma(a, b, b);     // DFMA chain
   long long t2 = clock64();
-  for (int i = 0; i < n; ++i) a = __shfl_xor_sync(0xffffffffu, a, 1);  // SHFL chain (2x32)
+  for (int i = 0; i < n; ++i) a = __shfl_sync(0xffffffffu, a, (threadIdx.x + i) & 31);  // SHFL chain (2x32)
   long long t3 = clock64();
   int idx = threadIdx.x & 31;
   double s = 0;
