@@ -289,108 +289,115 @@ constexpr int TAB = 32;      // block size
 constexpr int TAB_MAXB = 256;  // widest panel handled (smem: row block + diagonal blocks + G stage)
 static size_t t_assemble_smem(int b) {
   const int nblk = (b + TAB - 1) / TAB;
-  return sizeof(double) * ((size_t)TAB * b + (size_t)nblk * TAB * (TAB + 1) + (size_t)b * TAB +
+  return sizeof(double) * ((size_t)TAB * (b + 1) + (size_t)nblk * TAB * (TAB + 1) + (size_t)b * TAB +
                            TAB * (TAB + 1));
 }
 
+// diag_given: the diagonal blocks T_ee are already in T (written by the
+// leaves, which form them from the same reflectors); otherwise the CTA forms
+// them from G first. G is the symmetric Gram matrix: the G[q-rows, e-cols]
+// stage is read as G[e-rows, q-cols] so that consecutive threads read
+// consecutive addresses.
 __global__ void __launch_bounds__(256) t_assemble_kernel(const double* __restrict__ G, int64_t ldg,
                                                          const double* __restrict__ tau, int b,
-                                                         double* __restrict__ T, int64_t ldt) {
+                                                         double* __restrict__ T, int64_t ldt,
+                                                         int diag_given) {
   extern __shared__ double sm[];
   pdl_wait();
   pdl_trigger();
   const int nblk = (b + TAB - 1) / TAB;
   const int q = blockIdx.x, q0 = q * TAB;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double* Trow = sm;                       // [TAB][b]   row block q of T
-  double* Td = Trow + TAB * b;             // [nblk][TAB][TAB+1] diagonal blocks
-  double* Gs = Td + nblk * TAB * (TAB + 1);  // [b][TAB]  G[q0:s, e-block]
+  const int LDR = b + 1;                   // padded row stride of Trow
+  double* Trow = sm;                       // [TAB][b + 1]  row block q of T
+  double* Td = Trow + TAB * LDR;           // [nblk][TAB][TAB+1] diagonal blocks
+  double* Gs = Td + nblk * TAB * (TAB + 1);  // [b][TAB]  G[q0:e0, e-block]
   double* Xs = Gs + b * TAB;               // [TAB][TAB+1]
-  for (int i = tid; i < TAB * b; i += 256) Trow[i] = 0.0;
-  // diagonal G blocks e >= q into Td (overwritten in place by T_ee below)
+  for (int i = tid; i < TAB * LDR; i += 256) Trow[i] = 0.0;
   for (int e = q; e < nblk; ++e) {
     const int e0 = e * TAB;
     for (int i = tid; i < TAB * TAB; i += 256) {
       const int r = i % TAB, c = i / TAB;
+      const bool ok = e0 + r < b && e0 + c < b;
       Td[(e * TAB + r) * (TAB + 1) + c] =
-          (e0 + r < b && e0 + c < b) ? G[(e0 + r) + (int64_t)(e0 + c) * ldg] : 0.0;
+          !ok ? 0.0 : (diag_given ? T[(e0 + r) + (int64_t)(e0 + c) * ldt] : G[(e0 + r) + (int64_t)(e0 + c) * ldg]);
     }
   }
   __syncthreads();
-  for (int e = q + warp; e < nblk; e += 8) {  // T_ee: lane r = row r
-    const int e0 = e * TAB, r = lane;
-    double* D = Td + e * TAB * (TAB + 1);
-    double tr[TAB];
+  if (!diag_given) {
+    for (int e = q + warp; e < nblk; e += 8) {  // T_ee: lane r = row r
+      const int e0 = e * TAB, r = lane;
+      double* D = Td + e * TAB * (TAB + 1);
+      double tr[TAB];
 #pragma unroll
-    for (int c = 0; c < TAB; ++c) tr[c] = (c == r && e0 + r < b) ? -tau[e0 + r] : 0.0;
+      for (int c = 0; c < TAB; ++c) tr[c] = (c == r && e0 + r < b) ? -tau[e0 + r] : 0.0;
 #pragma unroll
-    for (int i = 1; i < TAB; ++i) {
-      double s0 = 0.0, s1 = 0.0;
+      for (int i = 1; i < TAB; ++i) {
+        double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-      for (int c = 0; c + 1 < i; c += 2) {
-        s0 = fma(tr[c], D[c * (TAB + 1) + i], s0);
-        s1 = fma(tr[c + 1], D[(c + 1) * (TAB + 1) + i], s1);
+        for (int c = 0; c + 1 < i; c += 2) {
+          s0 = fma(tr[c], D[c * (TAB + 1) + i], s0);
+          s1 = fma(tr[c + 1], D[(c + 1) * (TAB + 1) + i], s1);
+        }
+        if (i & 1) s0 = fma(tr[i - 1], D[(i - 1) * (TAB + 1) + i], s0);
+        if (i > r && e0 + i < b) tr[i] = -tau[e0 + i] * (s0 + s1);
       }
-      if (i & 1) s0 = fma(tr[i - 1], D[(i - 1) * (TAB + 1) + i], s0);
-      if (i > r && e0 + i < b) tr[i] = -tau[e0 + i] * (s0 + s1);
-    }
-    __syncwarp();
+      __syncwarp();
 #pragma unroll
-    for (int c = 0; c < TAB; ++c) D[r * (TAB + 1) + c] = tr[c];
+      for (int c = 0; c < TAB; ++c) D[r * (TAB + 1) + c] = tr[c];
+    }
+    __syncthreads();
   }
-  __syncthreads();
   for (int i = tid; i < TAB * TAB; i += 256) {
     const int r = i / TAB, c = i % TAB;
-    if (q0 + c < b) Trow[r * b + q0 + c] = Td[(q * TAB + r) * (TAB + 1) + c];
+    if (q0 + c < b) Trow[r * LDR + q0 + c] = Td[(q * TAB + r) * (TAB + 1) + c];
   }
   __syncthreads();
   const int cc = tid % TAB, r0 = (tid / TAB) * 4;  // 4 rows x 1 column per thread
   for (int e = q + 1; e < nblk; ++e) {
     const int e0 = e * TAB, kk = e0 - q0;  // K range [q0, e0)
     for (int i = tid; i < kk * TAB; i += 256) {
-      const int k = i / TAB, c = i % TAB;
-      Gs[k * TAB + c] = (e0 + c < b) ? G[(q0 + k) + (int64_t)(e0 + c) * ldg] : 0.0;
+      const int c = i % TAB, k = i / TAB;  // G[q0 + k][e0 + c] == G[e0 + c][q0 + k]
+      Gs[k * TAB + c] = (e0 + c < b) ? G[(e0 + c) + (int64_t)(q0 + k) * ldg] : 0.0;
     }
     __syncthreads();
-    double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;
-    for (int k = 0; k < kk; ++k) {
-      const double gv = Gs[k * TAB + cc];
-      x0 = fma(Trow[(r0 + 0) * b + q0 + k], gv, x0);
-      x1 = fma(Trow[(r0 + 1) * b + q0 + k], gv, x1);
-      x2 = fma(Trow[(r0 + 2) * b + q0 + k], gv, x2);
-      x3 = fma(Trow[(r0 + 3) * b + q0 + k], gv, x3);
+    double x[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    for (int k = 0; k < kk; k += 2) {  // kk is a multiple of TAB
+      const double g0 = Gs[k * TAB + cc], g1 = Gs[(k + 1) * TAB + cc];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        x[u][0] = fma(Trow[(r0 + u) * LDR + q0 + k], g0, x[u][0]);
+        x[u][1] = fma(Trow[(r0 + u) * LDR + q0 + k + 1], g1, x[u][1]);
+      }
     }
-    Xs[(r0 + 0) * (TAB + 1) + cc] = x0;
-    Xs[(r0 + 1) * (TAB + 1) + cc] = x1;
-    Xs[(r0 + 2) * (TAB + 1) + cc] = x2;
-    Xs[(r0 + 3) * (TAB + 1) + cc] = x3;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) Xs[(r0 + u) * (TAB + 1) + cc] = x[u][0] + x[u][1];
     __syncthreads();
     const double* D = Td + e * TAB * (TAB + 1);
-    double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
+    double y[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll 8
-    for (int k = 0; k < TAB; ++k) {
-      const double dv = D[k * (TAB + 1) + cc];
-      y0 = fma(Xs[(r0 + 0) * (TAB + 1) + k], dv, y0);
-      y1 = fma(Xs[(r0 + 1) * (TAB + 1) + k], dv, y1);
-      y2 = fma(Xs[(r0 + 2) * (TAB + 1) + k], dv, y2);
-      y3 = fma(Xs[(r0 + 3) * (TAB + 1) + k], dv, y3);
+    for (int k = 0; k < TAB; k += 2) {
+      const double d0 = D[k * (TAB + 1) + cc], d1 = D[(k + 1) * (TAB + 1) + cc];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        y[u][0] = fma(Xs[(r0 + u) * (TAB + 1) + k], d0, y[u][0]);
+        y[u][1] = fma(Xs[(r0 + u) * (TAB + 1) + k + 1], d1, y[u][1]);
+      }
     }
     if (e0 + cc < b) {
-      Trow[(r0 + 0) * b + e0 + cc] = y0;
-      Trow[(r0 + 1) * b + e0 + cc] = y1;
-      Trow[(r0 + 2) * b + e0 + cc] = y2;
-      Trow[(r0 + 3) * b + e0 + cc] = y3;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) Trow[(r0 + u) * LDR + e0 + cc] = y[u][0] + y[u][1];
     }
     __syncthreads();
   }
   for (int i = tid; i < TAB * b; i += 256) {
     const int r = i % TAB, c = i / TAB;
-    if (q0 + r < b) T[(q0 + r) + (int64_t)c * ldt] = Trow[r * b + c];
+    if (q0 + r < b) T[(q0 + r) + (int64_t)c * ldt] = Trow[r * LDR + c];
   }
 }
 
 int t_from_gram(cudaStream_t st, const double* G, int64_t ldg, const double* tau, int64_t b,
-                double* T, int64_t ldt) {
+                double* T, int64_t ldt, bool diag_given) {
   if (b < 1 || b > TAB_MAXB) {
     set_error("t_from_gram: b = %lld outside [1, %d]", (long long)b, TAB_MAXB);
     return -1;
@@ -407,7 +414,7 @@ int t_from_gram(cudaStream_t st, const double* G, int64_t ldg, const double* tau
   }
   count_launch();
   BR_CUDA(launch_pdl(t_assemble_kernel, dim3(nblk), dim3(256), smem, st, G, ldg, tau, (int)b, T,
-                     ldt));
+                     ldt, diag_given ? 1 : 0));
   return 0;
 }
 
@@ -551,36 +558,39 @@ int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView 
       // P[s:, e:b] += (Y_blk T_blk^T)(Y_blk^T P[s:, e:b]); the leaf writes
       // Y_blk T_blk^T into W's columns (W itself is formed at the end)
       MatView What = W->sub(s, s, j - s, w);
-      BR_CHECK(launch_leaf(st, leafP, leafY, tau + s, tblk, LEAF_NB, &What, 1));
+      BR_CHECK(launch_leaf(st, leafP, leafY, tau + s, T.p + s + s * T.ld, T.ld, &What, 1));
       MatView rest = P.sub(s, e, j - s, b - e);
       MatView Zs = Z.sub(0, 0, w, b - e);
       BR_CHECK(gemm(st, ws, Zs, leafY.T(), rest, 1.0, 0.0, nullptr, max_ctas));
       BR_CHECK(gemm(st, ws, rest, What, Zs, 1.0, 1.0, nullptr, max_ctas));
       continue;
     }
-    BR_CHECK(launch_leaf(st, leafP, leafY, tau + s, tblk, LEAF_NB, nullptr));
+    BR_CHECK(launch_leaf(st, leafP, leafY, tau + s, T.p + s + s * T.ld, T.ld, nullptr));
     if (e < b) {
       // P[s:, e:b] += Y_blk (T_blk^T (Y_blk^T P[s:, e:b]))
       MatView rest = P.sub(s, e, j - s, b - e);
       MatView Zs = Z.sub(0, 0, w, b - e), Z2s = Z2.sub(0, 0, w, b - e);
-      MatView Tb(tblk, LEAF_NB, w, w);
+      MatView Tb(T.p + s + s * T.ld, T.ld, w, w);  // the leaf's T block
       BR_CHECK(gemm(st, ws, Zs, leafY.T(), rest, 1.0, 0.0, nullptr, max_ctas));
       BR_CHECK(gemm(st, ws, Z2s, Tb.T(), Zs, 1.0, 0.0, nullptr, max_ctas));
       BR_CHECK(gemm(st, ws, rest, leafY, Z2s, 1.0, 1.0, nullptr, max_ctas));
     }
   }
   // full T: Gram, then the blocked recurrence in one kernel (T is written whole,
-  // zeros below the diagonal)
+  // zeros below the diagonal). 32-wide leaves already wrote the 32 x 32
+  // diagonal blocks of T.
+  const bool diag_given = !persist && nbl == TAB;
   BR_CHECK(gemm(st, ws, G, Y.T(), Y, 1.0, 0.0, nullptr, max_ctas));
   if (b <= TAB_MAXB) {
-    BR_CHECK(t_from_gram(st, G.p, G.ld, tau, b, T.p, T.ld));
+    BR_CHECK(t_from_gram(st, G.p, G.ld, tau, b, T.p, T.ld, diag_given));
   } else {
     // wider than one assembly kernel: diagonal super-blocks by the kernel,
     // T[0:s, s:e] = T[0:s,0:s] (G[0:s,s:e] T[s:e,s:e]) by GEMMs
     double* tmpp = scratch + b * b + LEAF_NB * LEAF_NB + 2 * LEAF_NB * b;
     for (int64_t s = 0; s < b; s += TAB_MAXB) {
       const int64_t e = std::min<int64_t>(s + TAB_MAXB, b);
-      BR_CHECK(t_from_gram(st, G.p + s + s * G.ld, G.ld, tau + s, e - s, T.p + s + s * T.ld, T.ld));
+      BR_CHECK(t_from_gram(st, G.p + s + s * G.ld, G.ld, tau + s, e - s, T.p + s + s * T.ld, T.ld,
+                           diag_given));
       if (s == 0) continue;
       MatView tmp(tmpp, s, s, e - s);
       BR_CHECK(gemm(st, ws, tmp, G.sub(0, s, s, e - s), T.sub(s, s, e - s, e - s), 1.0, 0.0, nullptr, max_ctas));
