@@ -202,7 +202,7 @@ def run_reference(args, rank, world):
         "warmup": args.warmup,
         "ms_per_step": sample[1] * 1e3,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
@@ -361,7 +361,7 @@ def run_ours(args, rank, world, local_rank):
             "warmup": args.warmup,
             "ms_per_step": ms,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong",
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic",
