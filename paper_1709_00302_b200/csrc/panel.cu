@@ -30,7 +30,7 @@
 
 namespace br {
 
-constexpr int LEAF_NB = 32;    // max leaf width
+constexpr int LEAF_NB = 64;    // max leaf width (64 only for the 2D-layout leaf)
 constexpr int LEAF_MAXC = 16;  // max cluster size (non-portable)
 static long long* g_leaf_prof = nullptr;  // BR_LEAF_PROF phase counters
 
@@ -60,7 +60,20 @@ namespace br {
 
 // Rows one cluster holds at leaf width nb: 16 CTAs x 256 threads x R rows
 // with R * NB = 64 register doubles per thread.
-static int leaf_rows_per_thread(int nb) { return nb > 16 ? 2 : (nb > 8 ? 4 : 8); }
+static int leaf_rows_per_thread(int nb) { return nb > 32 ? 1 : (nb > 16 ? 2 : (nb > 8 ? 4 : 8)); }
+// 64-wide leaves (8 column-group warps, <= 4096 rows): opt-in with
+// BR_LEAF64=1. Measured slower than two 32-wide leaves plus their block update
+// (4096 x 256 panel 760 vs 686 us): two warps per SM sub-partition lengthen
+// every column step more than the saved launches and epilogues win back.
+static bool leaf64_enabled() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = std::getenv("BR_LEAF64");
+    const char* l2 = std::getenv("BR_LEAF2");
+    m = (e && std::atoi(e) == 1 && !(l2 && std::atoi(l2) == 0)) ? 1 : 0;
+  }
+  return m == 1;
+}
 // Threads per leaf CTA at most (BR_LEAF_LT=128: half-SM CTAs only; tuning aid).
 static int leaf_max_lt() {
   static int lt = 0;
@@ -77,8 +90,9 @@ static int64_t leaf_capacity(int nb) {
 // Leaf width for a j x b panel: the widest of {32, 16, 8} (or b if narrower)
 // whose L rows fit one cluster.
 static int leaf_width(int64_t L, int64_t b) {
-  const int cand[3] = {32, 16, 8};
+  const int cand[4] = {64, 32, 16, 8};
   for (int nb : cand) {
+    if (nb == 64 && (b <= 32 || !leaf64_enabled())) continue;
     const int use = (int)std::min<int64_t>(nb, b);
     if (L <= leaf_capacity(use)) return use;
   }
@@ -133,7 +147,7 @@ static int launch_leaf2_t(cudaStream_t st, const LeafArgs& a) {
   constexpr int ROWS = (NW / (NB / 8)) * 256;
   int C = 1;
   while (C < cdiv(a.L, ROWS)) C *= 2;
-  const size_t smem = (size_t)NB * ROWS * sizeof(double);
+  const size_t smem = ((size_t)NB * ROWS + 2 * (size_t)NB * (NB + 1)) * sizeof(double);
   static int attr_dev_mask = 0;
   int dev = 0;
   BR_CUDA(cudaGetDevice(&dev));
@@ -187,7 +201,10 @@ static int launch_leaf2(cudaStream_t st, const LeafArgs& a, bool* done) {
   if (mode == 0 || a.nleaves != 1) return *done = false, 0;
   const int64_t L = a.L;
   const bool wide = mode == 2;
-  if (a.nb > 32) return *done = false, 0;
+  if (a.nb > 32) {
+    if (a.nb <= 64 && L <= (int64_t)LEAF_MAXC * 256) return launch_leaf2_t<64, 8>(st, a);
+    return *done = false, 0;
+  }
   if (a.nb > 16) {
     if (!wide && L <= (int64_t)LEAF_MAXC * 256) return launch_leaf2_t<32, 4>(st, a);
     if (L <= (int64_t)LEAF_MAXC * 512) return launch_leaf2_t<32, 8>(st, a);
@@ -519,7 +536,7 @@ int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView 
   MatView Z(tblk + LEAF_NB * LEAF_NB, LEAF_NB, LEAF_NB, b);
   MatView Z2(Z.p + LEAF_NB * b, LEAF_NB, LEAF_NB, b);
   const int nleaves = (int)cdiv(b, nbl);
-  const bool persist = pws && W && nleaves <= 64 && persistent_panel_enabled(j);
+  const bool persist = pws && W && nleaves <= 64 && nbl <= 32 && persistent_panel_enabled(j);
   if (persist) {
     // Persistent panel: one cluster launch factors every leaf; the block
     // update of leaf s is applied on the aux stream, first to the next
@@ -579,7 +596,7 @@ int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView 
   // full T: Gram, then the blocked recurrence in one kernel (T is written whole,
   // zeros below the diagonal). 32-wide leaves already wrote the 32 x 32
   // diagonal blocks of T.
-  const bool diag_given = !persist && nbl == TAB;
+  const bool diag_given = !persist && nbl % TAB == 0;
   BR_CHECK(gemm(st, ws, G, Y.T(), Y, 1.0, 0.0, nullptr, max_ctas));
   if (b <= TAB_MAXB) {
     BR_CHECK(t_from_gram(st, G.p, G.ld, tau, b, T.p, T.ld, diag_given));
@@ -642,6 +659,7 @@ int preload_panel_kernels() {
   BR_CHECK((launch_leaf_t<16, 4, 256>(0, a)));
   BR_CHECK((launch_leaf_t<8, 8, 128>(0, a)));
   BR_CHECK((launch_leaf_t<8, 8, 256>(0, a)));
+  BR_CHECK((launch_leaf2_t<64, 8>(0, a)));
   BR_CHECK((launch_leaf2_t<32, 4>(0, a)));
   BR_CHECK((launch_leaf2_t<32, 8>(0, a)));
   BR_CHECK((launch_leaf2_t<16, 2>(0, a)));

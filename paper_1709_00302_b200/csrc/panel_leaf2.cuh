@@ -11,7 +11,7 @@ __device__ __forceinline__ void st_async_f64(uint32_t raddr, double a, uint32_t 
       : "memory");
 }
 
-// One leaf (L x nb, nb <= NB, NB in {16, 32}) of a Householder panel, same
+// One leaf (L x nb, nb <= NB, NB in {16, 32, 64}) of a Householder panel, same
 // outputs and arithmetic contract as leaf_reg_kernel (Y, tau, T, W, R rows of
 // P), with a 2D layout: warp w owns the 8 columns 8*(w % CG) .. +8 (CG = NB/8
 // column groups) of the 256 rows of its row group rg = w / CG, and lane l of
@@ -40,8 +40,10 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
   constexpr int ROWS = RG * 256;  // rows per CTA
   constexpr int NT = NW * 32;
   constexpr int MAXSRC = LEAF_MAXC * RG;
+  constexpr int RB = (NB + 31) / 32;  // register rows that can hold rows < NB
   static_assert(CG * RG == NW && RG >= 1, "warp layout");
-  extern __shared__ __align__(16) double Ys[];  // [NB][ROWS], epilogue only
+  // dynamic: Ys [NB][ROWS] (epilogue), G [NB][NB+1] (Gram), Ts [NB][NB+1] (T)
+  extern __shared__ __align__(16) double Ys[];
   __shared__ __align__(16) double xs[2][ROWS];
   __shared__ __align__(16) double rowl[2][NB];           // row i (CTA 0 local)
   __shared__ __align__(16) double recv[2][MAXSRC][NB];   // slot partials per source
@@ -49,8 +51,8 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
   __shared__ __align__(16) double recvr[2][NB];          // row i from CTA 0
   __shared__ __align__(8) uint64_t mbar[2];
   __shared__ double scal[NB][3];  // x0 -> tau, beta, rinv
-  __shared__ double G[NB][NB + 1];
-  __shared__ double Ts[NB][NB + 1];
+  double(*G)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(Ys + NB * ROWS);
+  double(*Ts)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(Ys + NB * ROWS + NB * (NB + 1));
 
   const uint32_t rank = cluster_ctarank(), ncta = cluster_nctarank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -145,20 +147,27 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
     const int cg = i >> 3, ci = i & 7;
     const bool own = (wcg == cg);
     const int buf = i & 1;
-    const bool above0 = top && lane < i;  // register row 0 lies above the pivot
-    const bool piv0 = top && lane == i;   // register row 0 is the pivot row
+    // register rows r < RB of CTA 0's row group 0 hold rows 32 r + lane < NB,
+    // the only rows that can lie above (or be) the pivot row i
+    bool above[RB], piv[RB];
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      above[r] = top && lane + 32 * r < i;
+      piv[r] = top && lane + 32 * r == i;
+    }
     if (xch && tid == 0) mbar_arrive_expect_tx(&mbar[buf], (uint32_t)(nsrc * (NB + 1) * 8 + NB * 8));
     // ---- 1. publish x (owner warps) and row i (CTA 0, row group 0, lane i) ----
     if (own) {
-      xs[buf][lrow0] = above0 ? 0.0 : p[0][0];
 #pragma unroll
-      for (int r = 1; r < 8; ++r) xs[buf][lrow0 + 32 * r] = p[r][0];
+      for (int r = 0; r < 8; ++r) xs[buf][lrow0 + 32 * r] = (r < RB && above[r]) ? 0.0 : p[r][0];
     }
-    if (piv0) {
 #pragma unroll
-      for (int c = 0; c < 8; c += 2)
-        *reinterpret_cast<double2*>(&rowl[buf][wcg * 8 + c]) = make_double2(p[0][c], p[0][c + 1]);
-    }
+    for (int r = 0; r < RB; ++r)
+      if (piv[r]) {
+#pragma unroll
+        for (int c = 0; c < 8; c += 2)
+          *reinterpret_cast<double2*>(&rowl[buf][wcg * 8 + c]) = make_double2(p[r][c], p[r][c + 1]);
+      }
     __syncthreads();
     BR_PHASE2(1);
     if (xch && top) {  // row i to every CTA: 4 slot pairs x ncta
@@ -259,16 +268,15 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
 #pragma unroll
       for (int c = 0; c < 8; ++c) al[c] = __shfl_sync(FULL, alpha, 4 * c);
       double vk[8];
-      vk[0] = piv0 ? 1.0 : xv[0] * rinv;  // 0 above row i (x masked)
 #pragma unroll
-      for (int r = 1; r < 8; ++r) vk[r] = xv[r] * rinv;
+      for (int r = 0; r < 8; ++r) vk[r] = (r < RB && piv[r]) ? 1.0 : xv[r] * rinv;  // 0 above row i
       if (own) {  // rotate: slot s <- slot s+1 updated; Y column i (R kept above) to slot 7
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
           const double x = p[r][0];
 #pragma unroll
           for (int c = 0; c < 7; ++c) p[r][c] = fma(-vk[r], al[c + 1], p[r][c + 1]);
-          p[r][7] = (r == 0 && above0) ? x : vk[r];
+          p[r][7] = (r < RB && above[r]) ? x : vk[r];
         }
       } else {
 #pragma unroll
@@ -312,28 +320,32 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
         if (col < nb && row < Lr) a.Y[row + (int64_t)col * a.ldy] = y;
       }
     }
-    if (top && lane < nb) {  // R rows
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const int col = wcg * 8 + c;
-        if (col >= lane && col < nb) *P.at(lane, col) = (col == lane) ? scal[lane][1] : p[0][c];
+    for (int r = 0; r < RB; ++r) {
+      const int row = lane + 32 * r;
+      if (top && row < nb) {  // R rows
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int col = wcg * 8 + c;
+          if (col >= row && col < nb) *P.at(row, col) = (col == row) ? scal[row][1] : p[r][c];
+        }
       }
     }
   };
-  if (warp == 0) {
-    // tau = (beta - x0) / beta (ref kernels.py:109), lane i -> slot i
-    double tau_l = 0.0;
-    if (lane < nb) {
-      const double be = scal[lane][1];
-      tau_l = (be != 0.0) ? (be - scal[lane][0]) / be : 0.0;
-    }
-    const int r = lane;
+  if (tid < nb) {  // tau = (beta - x0) / beta (ref kernels.py:109); x0 is read by its owner only
+    const double be = scal[tid][1];
+    scal[tid][0] = (be != 0.0) ? (be - scal[tid][0]) / be : 0.0;
+  }
+  __syncthreads();
+  if (warp < NB / 32 || (NB < 32 && warp == 0)) {
+    // T rows 32 warp + lane by the reference recurrence
+    // T[r][i] = -tau_i sum_{c<i} T[r][c] G[c][i] (ref kernels.py:152-162)
+    const int r = warp * 32 + lane;
     double tr[NB];
 #pragma unroll
-    for (int c = 0; c < NB; ++c) tr[c] = (c == r && r < nb) ? -tau_l : 0.0;
+    for (int c = 0; c < NB; ++c) tr[c] = (c == r && r < nb) ? -scal[c][0] : 0.0;
 #pragma unroll
     for (int i = 1; i < NB; ++i) {
-      const double ti = __shfl_sync(FULL, tau_l, i);
       double s0 = 0.0, s1 = 0.0;
 #pragma unroll
       for (int c = 0; c + 1 < i; c += 2) {
@@ -341,13 +353,12 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
         s1 = fma(tr[c + 1], G[c + 1][i], s1);
       }
       if (i & 1) s0 = fma(tr[i - 1], G[i - 1][i], s0);
-      if (i > r && i < nb) tr[i] = -ti * (s0 + s1);
+      if (i > r && i < nb) tr[i] = -scal[i][0] * (s0 + s1);
     }
-    if (lane < NB) {
+    if (r < NB) {
 #pragma unroll
       for (int c = 0; c < NB; ++c) Ts[r][c] = tr[c];
     }
-    if (lane < nb) scal[lane][0] = tau_l;  // every read of scal[.][0] (x0) precedes this
     __syncwarp();
     store_y();
   } else {

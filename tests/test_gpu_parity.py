@@ -478,8 +478,9 @@ def test_streamed_band_output_matches(br, kind):
 @pytest.mark.gpu
 def test_leaf_layouts_agree(tmp_path):
     """The 2D-layout leaf (default; 1 CTA without exchange, clusters of 4- or
-    8-warp CTAs) and the 1D-layout leaf (BR_LEAF2=0) factor the same panels
-    to rounding, including zero columns and zero tails."""
+    8-warp CTAs, opt-in 64-wide leaves up to 4096 rows) and the 1D-layout leaf
+    (BR_LEAF2=0, at most 32 wide) factor the same panels to rounding,
+    including zero columns and zero tails."""
     import os
     import subprocess
     import sys
@@ -488,7 +489,8 @@ def test_leaf_layouts_agree(tmp_path):
         "import numpy as np, paper_1709_00302_b200 as br\n"
         "out = []\n"
         "for j, b, s in [(200, 32, 1), (3000, 32, 2), (6000, 32, 3), (250, 12, 4), (5000, 16, 5),\n"
-        "                (12000, 16, 6), (777, 29, 7), (4096, 256, 8)]:\n"
+        "                (12000, 16, 6), (777, 29, 7), (4096, 256, 8), (3000, 64, 9),\n"
+        "                (1000, 50, 10), (2500, 128, 11)]:\n"
         "    A = np.random.default_rng(s).standard_normal((j, b))\n"
         "    if s == 7:\n"
         "        A[:, 3] = 0.0; A[5:, 9] = 0.0\n"
@@ -497,7 +499,8 @@ def test_leaf_layouts_agree(tmp_path):
         "np.savez(r'%s', *out)\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
-    for mode in ({"BR_LEAF2": "0"}, {"BR_LEAF2": "1"}, {"BR_LEAF2": "1", "BR_LEAF2_WIDE": "1"}):
+    for mode in ({"BR_LEAF2": "0"}, {"BR_LEAF2": "1"}, {"BR_LEAF2": "1", "BR_LEAF2_WIDE": "1"},
+                 {"BR_LEAF2": "1", "BR_LEAF64": "1"}):
         path = tmp_path / f"leaf{len(outs)}.npz"
         env = dict(os.environ, **mode)
         r = subprocess.run([sys.executable, "-c", code % path], cwd=root, env=env,
