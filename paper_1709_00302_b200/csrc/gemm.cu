@@ -28,6 +28,46 @@ __global__ void splitk_reduce_kernel(int64_t M, int64_t N, int S, const double* 
   }
 }
 
+// Fixed-order split-K reduction followed by a small triangular product:
+// C (M x N, M <= 64) = T^T * sum_z ws[z], T upper triangular M x M. CTA per 32
+// output columns; the block reflector step of a panel (Z = T^T (Y^T P)) in
+// one pass over the partials.
+constexpr int TT_MAXM = 64;
+__global__ void __launch_bounds__(256) splitk_reduce_tt_kernel(int64_t M, int64_t N, int S,
+                                                               const double* __restrict__ ws,
+                                                               const double* __restrict__ T,
+                                                               int64_t ldt, double* C, int64_t ldc) {
+  __shared__ double Ts[TT_MAXM][TT_MAXM + 1];
+  __shared__ double Zs[TT_MAXM][33];
+  pdl_wait();
+  pdl_trigger();
+  const int tid = threadIdx.x;
+  const int64_t c0 = (int64_t)blockIdx.x * 32;
+  const int m = (int)M;
+  for (int i = tid; i < m * m; i += 256) {
+    const int r = i % m, c = i / m;
+    Ts[r][c] = (r <= c) ? T[r + (int64_t)c * ldt] : 0.0;
+  }
+  const int64_t total = M * N;
+  for (int i = tid; i < m * 32; i += 256) {
+    const int r = i % m, c = i / m;
+    double s = 0.0;
+    if (c0 + c < N) {
+      const double* src = ws + (c0 + c) * M + r;
+      for (int z = 0; z < S; ++z) s += src[(int64_t)z * total];
+    }
+    Zs[r][c] = s;
+  }
+  __syncthreads();
+  for (int i = tid; i < m * 32; i += 256) {
+    const int r = i % m, c = i / m;
+    if (c0 + c >= N) continue;
+    double s = 0.0;
+    for (int k = 0; k <= r; ++k) s = fma(Ts[k][r], Zs[k][c], s);
+    C[r + (c0 + c) * ldc] = s;
+  }
+}
+
 static inline bool al16(const void* p, int64_t ld) {
   return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && (ld % 2 == 0);
 }
@@ -108,7 +148,7 @@ static int64_t pick_kps(int cfg, const Scratch& ws, const GemmArgs& g, int max_c
 // for the whole product (gemm_plan_kps), so every element is summed in the
 // same order whatever the pieces are (bitwise split invariance).
 static int run_gemm(int am, cudaStream_t st, Scratch& ws, GemmArgs g, bool btrans, int max_ctas,
-                    int64_t fixed_kps) {
+                    int64_t fixed_kps, const double* tt = nullptr, int64_t ldtt = 0) {
   if (g.M <= 0 || g.N <= 0) return 0;
   if (g.K <= 0) {  // C = beta*Cin
     const int64_t total = g.M * g.N;
@@ -131,6 +171,18 @@ static int run_gemm(int am, cudaStream_t st, Scratch& ws, GemmArgs g, bool btran
   g.k_per_split = S > 1 ? kps : g.K;
   dim3 grid((unsigned)cdiv(g.M, bm), (unsigned)cdiv(g.N, bn), (unsigned)S);
   const int bmd = btrans ? B_T : B_N;
+  if (tt) {  // C = T^T (sum of partials): always through the workspace
+    if (S * g.M * g.N > ws.cap) {
+      set_error("gemm_tt: split-K scratch too small");
+      return -1;
+    }
+    g.ws = ws.p;
+    BR_CHECK(launch_tile(cfg, am, bmd, EPI_SPLIT, st, g, grid));
+    count_launch();
+    BR_CUDA(launch_pdl(splitk_reduce_tt_kernel, dim3((unsigned)cdiv(g.N, 32)), dim3(256), 0, st, g.M,
+                       g.N, (int)S, (const double*)ws.p, tt, ldtt, g.C, g.ldc));
+    return 0;
+  }
   if (S == 1) {
     BR_CHECK(launch_tile(cfg, am, bmd, EPI_GEN, st, g, grid));
   } else {
@@ -205,6 +257,18 @@ int gemm(cudaStream_t st, Scratch& ws, MatView C, MatView A, MatView B, double a
   BR_CHECK(make_args(C, A, B, alpha, beta, Cin, g, am, bt));
   g.b_upper = b_upper ? 1 : 0;
   return run_gemm(am, st, ws, g, bt, max_ctas, kps);
+}
+
+int gemm_tt(cudaStream_t st, Scratch& ws, MatView C, MatView A, MatView B, MatView T) {
+  GemmArgs g;
+  int am = 0;
+  bool bt = false;
+  if (C.trans || T.trans || C.rows > TT_MAXM || T.rows != C.rows || T.cols != C.rows) {
+    set_error("gemm_tt: C must be a plain view with at most %d rows and T square", TT_MAXM);
+    return -1;
+  }
+  BR_CHECK(make_args(C, A, B, 1.0, 0.0, nullptr, g, am, bt));
+  return run_gemm(am, st, ws, g, bt, 0, 0, T.p, T.ld);
 }
 
 int64_t gemm_plan_kps(const Scratch& ws, MatView C, MatView A, MatView B, double beta) {
@@ -307,6 +371,7 @@ int preload_gemm_kernels() {
   }
   cudaFuncAttributes fa;
   BR_CUDA(cudaFuncGetAttributes(&fa, splitk_reduce_kernel));
+  BR_CUDA(cudaFuncGetAttributes(&fa, splitk_reduce_tt_kernel));
   return 0;
 }
 

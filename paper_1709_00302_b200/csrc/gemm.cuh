@@ -60,6 +60,9 @@ struct GemmArgs {
 int gemm(cudaStream_t st, Scratch& ws, MatView C, MatView A, MatView B, double alpha,
          double beta, const MatView* Cin = nullptr, int max_ctas = 0, int64_t kps = 0,
          bool b_upper = false);
+// C = T^T * op(A) * op(B) for a small C (at most 64 rows; T upper triangular,
+// C.rows x C.rows): split-K partials reduced and multiplied by T^T in one pass.
+int gemm_tt(cudaStream_t st, Scratch& ws, MatView C, MatView A, MatView B, MatView T);
 // The split-K chunk gemm() would choose for this whole product. Updating the
 // product in row/column pieces with this kps sums every element in the same
 // order as the whole call, so the result is bitwise independent of the pieces.

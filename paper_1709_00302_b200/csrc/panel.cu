@@ -491,8 +491,10 @@ static int stream_set_flag(cudaStream_t st, unsigned* f, unsigned v) {
   return 0;
 }
 
-// Multi-leaf panels: the leaf forms Y T^T for the block update (default) or
-// the update applies T^T with one more small GEMM (BR_LEAF_W=0).
+// Multi-leaf panels: the leaf forms Y T^T on DMMA for the block update
+// (default), or the update applies T^T inside the split-K reduction and the
+// leaf skips W (BR_LEAF_W=0; measured flat to slower: c4 447.2 vs 445.4 ms,
+// the reduction pass is then always launched).
 static bool leaf_w_mode() {
   static int m = -1;
   if (m < 0) {
@@ -584,12 +586,12 @@ int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView 
     }
     BR_CHECK(launch_leaf(st, leafP, leafY, tau + s, T.p + s + s * T.ld, T.ld, nullptr));
     if (e < b) {
-      // P[s:, e:b] += Y_blk (T_blk^T (Y_blk^T P[s:, e:b]))
+      // P[s:, e:b] += Y_blk (T_blk^T (Y_blk^T P[s:, e:b])): the T_blk^T product
+      // rides on the split-K reduction, so the leaf needs no W
       MatView rest = P.sub(s, e, j - s, b - e);
-      MatView Zs = Z.sub(0, 0, w, b - e), Z2s = Z2.sub(0, 0, w, b - e);
+      MatView Z2s = Z2.sub(0, 0, w, b - e);
       MatView Tb(T.p + s + s * T.ld, T.ld, w, w);  // the leaf's T block
-      BR_CHECK(gemm(st, ws, Zs, leafY.T(), rest, 1.0, 0.0, nullptr, max_ctas));
-      BR_CHECK(gemm(st, ws, Z2s, Tb.T(), Zs, 1.0, 0.0, nullptr, max_ctas));
+      BR_CHECK(gemm_tt(st, ws, Z2s, leafY.T(), rest, Tb));
       BR_CHECK(gemm(st, ws, rest, leafY, Z2s, 1.0, 1.0, nullptr, max_ctas));
     }
   }

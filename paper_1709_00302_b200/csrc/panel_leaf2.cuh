@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
       for (int c = 0; c < 8; ++c) {
         const int col = wcg * 8 + c;
         const double y = (col < nb && row >= col) ? p[r][c] : 0.0;
-        Ys[col * ROWS + lrow] = y;
+        if (a.W) Ys[col * ROWS + lrow] = y;  // staged for W = Y T only
         if (col < nb && row < Lr) a.Y[row + (int64_t)col * a.ldy] = y;
       }
     }

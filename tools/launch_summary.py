@@ -19,9 +19,12 @@ def family(name: str) -> str:
         return f"dgemm {bm}x{bn}x{bk} A{amn}B{bmn} {epn}"
     m = re.search(r"leaf_reg_kernel<(\d+), (\d+), (\d+)>", name)
     if m:
-        return f"panel leaf NB={m.group(1)} R={m.group(2)} LT={m.group(3)}"
-    for key in ("splitk_reduce", "t_diag", "finalize_sym", "mask_band", "identity_kernel",
-                "house_gen"):
+        return f"panel leaf (1D) NB={m.group(1)} R={m.group(2)} LT={m.group(3)}"
+    m = re.search(r"leaf2_kernel<(\d+), (\d+)>", name)
+    if m:
+        return f"panel leaf (2D) NB={m.group(1)} warps={m.group(2)}"
+    for key in ("splitk_reduce", "t_assemble", "t_diag", "finalize_sym", "mask_band",
+                "identity_kernel", "house_gen", "zero_fill", "copy_kernel"):
         if key in name:
             return key
     return "other (torch: inputs/copies/cuBLAS peak)"
