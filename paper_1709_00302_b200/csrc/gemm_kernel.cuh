@@ -120,8 +120,10 @@ __device__ __forceinline__ int sym_case(int64_t k0, int64_t m0, int BK, int BM) 
   return 2;
 }
 
+// One output tile (bx, by) of K-split bz.
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, int AM, int BMD, int EPI>
-__global__ void __launch_bounds__(WM* WN * 32, MINB) dgemm_kernel(const GemmArgs g) {
+__device__ __forceinline__ void dgemm_tile(const GemmArgs& g, const unsigned bx, const unsigned by,
+                                           const unsigned bz) {
   constexpr int NT = WM * WN * 32;
   constexpr int WTM = BM / WM, WTN = BN / WN, MI = WTM / 8, NI = WTN / 8;
   constexpr int LDA_KM = BM + 4, LDA_MK = BK + 4;
@@ -142,15 +144,15 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB) dgemm_kernel(const GemmArgs
 
   int64_t m0, n0, kbeg, kend;
   if (EPI == EPI_LOWER) {
-    if (blockIdx.x < blockIdx.y) return;
-    m0 = g.c0 + (int64_t)blockIdx.x * BM;
-    n0 = g.c0 + (int64_t)blockIdx.y * BN;
+    if (bx < by) return;
+    m0 = g.c0 + (int64_t)bx * BM;
+    n0 = g.c0 + (int64_t)by * BN;
     kbeg = 0;
     kend = g.K;
   } else {
-    m0 = (int64_t)blockIdx.x * BM;
-    n0 = (int64_t)blockIdx.y * BN;
-    kbeg = (int64_t)blockIdx.z * g.k_per_split;
+    m0 = (int64_t)bx * BM;
+    n0 = (int64_t)by * BN;
+    kbeg = (int64_t)bz * g.k_per_split;
     kend = min(g.K, kbeg + g.k_per_split);
     if (BMD == B_N && g.b_upper) kend = max(kbeg, min(kend, n0 + BN));  // rows > n of B are 0
   }
@@ -362,7 +364,7 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB) dgemm_kernel(const GemmArgs
           }
           g.C[r + c * g.ldc] = out;
         } else if (EPI == EPI_SPLIT) {
-          g.ws[((int64_t)blockIdx.z * g.N + c) * g.M + r] = v;
+          g.ws[((int64_t)bz * g.N + c) * g.M + r] = v;
         } else {
           if (r >= c) g.C[r + c * g.ldc] = v;
         }
@@ -371,6 +373,26 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB) dgemm_kernel(const GemmArgs
   }
 }
 
+
+
+// One CTA per tile.
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, int AM, int BMD, int EPI>
+__global__ void __launch_bounds__(WM* WN * 32, MINB) dgemm_kernel(const GemmArgs g) {
+  dgemm_tile<BM, BN, BK, WM, WN, STAGES, MINB, AM, BMD, EPI>(g, blockIdx.x, blockIdx.y, blockIdx.z);
+}
+// Capped grid (g.persist): CTAs walk the tiles in order, so a panel's small
+// GEMMs hold at most gridDim.x CTA slots of the SMs the concurrent trailing
+// update runs on. A separate instantiation keeps the one-tile kernels' code
+// (and register allocation) unchanged.
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, int AM, int BMD, int EPI>
+__global__ void __launch_bounds__(WM* WN * 32, MINB) dgemm_kernel_persist(const GemmArgs g) {
+  const unsigned tx = (unsigned)g.tiles_x, txy = tx * (unsigned)g.tiles_y;
+  const unsigned total = txy * (unsigned)g.tiles_z;
+  for (unsigned t = blockIdx.x; t < total; t += gridDim.x) {
+    dgemm_tile<BM, BN, BK, WM, WN, STAGES, MINB, AM, BMD, EPI>(g, t % tx, (t % txy) / tx, t / txy);
+    __syncthreads();  // shared-memory stages are reused by the next tile
+  }
+}
 
 template <int BM, int BN, int BK, int STAGES, int AM, int BMD>
 constexpr int smem_bytes() {
@@ -385,15 +407,21 @@ constexpr int smem_bytes() {
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, int AM, int BMD, int EPI>
 static int launch(cudaStream_t st, const GemmArgs& g, dim3 grid) {
   constexpr int smem = smem_bytes<BM, BN, BK, STAGES, AM, BMD>();
-  auto kern = dgemm_kernel<BM, BN, BK, WM, WN, STAGES, MINB, AM, BMD, EPI>;
+  auto kern1 = dgemm_kernel<BM, BN, BK, WM, WN, STAGES, MINB, AM, BMD, EPI>;
+  auto kernp = dgemm_kernel_persist<BM, BN, BK, WM, WN, STAGES, MINB, AM, BMD, EPI>;
+  auto kern = g.persist ? kernp : kern1;
   static int attr_dev_mask = 0;  // per-instantiation, per-device
   int dev = 0;
   BR_CUDA(cudaGetDevice(&dev));
   if (!(attr_dev_mask & (1 << dev))) {
-    BR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    BR_CUDA(cudaFuncSetAttribute(kern1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    BR_CUDA(cudaFuncSetAttribute(kernp, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_dev_mask |= 1 << dev;
   }
-  if (g_preload_only) return (int)launch_pdl(kern, grid, dim3(WM * WN * 32), smem, st, g);
+  if (g_preload_only) {
+    BR_CUDA(launch_pdl(kernp, grid, dim3(WM * WN * 32), smem, st, g));
+    return (int)launch_pdl(kern1, grid, dim3(WM * WN * 32), smem, st, g);
+  }
   count_launch();
   BR_CUDA(launch_pdl(kern, grid, dim3(WM * WN * 32), smem, st, g));
   return 0;
