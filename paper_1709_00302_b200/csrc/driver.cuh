@@ -122,8 +122,16 @@ int ws_collect_timing(Workspace& ws);  // after a sync: fold events into t_ms
 // -T_larft), W = Y*T (j x b, optional). R (or L) is written into P's top
 // b x b triangle; the strictly-lower part of P is left unspecified (the
 // reductions zero it in their final band mask).
+// Completion points of a panel's leaves: Y columns [c0[s], c1[s]) are final
+// once ev[s] (recorded on the panel's stream) has completed.
+struct LeafMarks {
+  int n = 0;
+  int64_t c0[64], c1[64];
+  cudaEvent_t ev[64];
+};
 int panel_qr(cudaStream_t st, Scratch& sk, DevBuf& pscratch, MatView P, MatView Y, double* tau,
-             MatView T, MatView* W, int max_ctas = 0, Workspace* pws = nullptr);
+             MatView T, MatView* W, int max_ctas = 0, Workspace* pws = nullptr,
+             LeafMarks* marks = nullptr);
 int64_t panel_scratch_doubles(int64_t b);
 int t_from_gram(cudaStream_t st, const double* G, int64_t ldg, const double* tau, int64_t b,
                 double* T, int64_t ldt, bool diag_given = false);

@@ -29,27 +29,27 @@ __global__ void splitk_reduce_kernel(int64_t M, int64_t N, int S, const double* 
 }
 
 // Fixed-order split-K reduction followed by a small triangular product:
-// C (M x N, M <= 64) = T^T * sum_z ws[z], T upper triangular M x M. CTA per 32
+// C (M x N, M <= 64) = T^T * sum_z ws[z], T upper triangular M x M. CTA per 16
 // output columns; the block reflector step of a panel (Z = T^T (Y^T P)) in
 // one pass over the partials.
-constexpr int TT_MAXM = 64;
+constexpr int TT_MAXM = 64, TT_COLS = 16;
 __global__ void __launch_bounds__(256) splitk_reduce_tt_kernel(int64_t M, int64_t N, int S,
                                                                const double* __restrict__ ws,
                                                                const double* __restrict__ T,
                                                                int64_t ldt, double* C, int64_t ldc) {
   __shared__ double Ts[TT_MAXM][TT_MAXM + 1];
-  __shared__ double Zs[TT_MAXM][33];
+  __shared__ double Zs[TT_MAXM][TT_COLS + 1];
   pdl_wait();
   pdl_trigger();
   const int tid = threadIdx.x;
-  const int64_t c0 = (int64_t)blockIdx.x * 32;
+  const int64_t c0 = (int64_t)blockIdx.x * TT_COLS;
   const int m = (int)M;
   for (int i = tid; i < m * m; i += 256) {
     const int r = i % m, c = i / m;
     Ts[r][c] = (r <= c) ? T[r + (int64_t)c * ldt] : 0.0;
   }
   const int64_t total = M * N;
-  for (int i = tid; i < m * 32; i += 256) {
+  for (int i = tid; i < m * TT_COLS; i += 256) {
     const int r = i % m, c = i / m;
     double s = 0.0;
     if (c0 + c < N) {
@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(256) splitk_reduce_tt_kernel(int64_t M, int64_
     Zs[r][c] = s;
   }
   __syncthreads();
-  for (int i = tid; i < m * 32; i += 256) {
+  for (int i = tid; i < m * TT_COLS; i += 256) {
     const int r = i % m, c = i / m;
     if (c0 + c >= N) continue;
     double s = 0.0;
@@ -186,7 +186,7 @@ static int run_gemm(int am, cudaStream_t st, Scratch& ws, GemmArgs g, bool btran
     g.ws = ws.p;
     BR_CHECK(launch_tile(cfg, am, bmd, EPI_SPLIT, st, g, grid));
     count_launch();
-    BR_CUDA(launch_pdl(splitk_reduce_tt_kernel, dim3((unsigned)cdiv(g.N, 32)), dim3(256), 0, st, g.M,
+    BR_CUDA(launch_pdl(splitk_reduce_tt_kernel, dim3((unsigned)cdiv(g.N, TT_COLS)), dim3(256), 0, st, g.M,
                        g.N, (int)S, (const double*)ws.p, tt, ldtt, g.C, g.ldc));
     return 0;
   }

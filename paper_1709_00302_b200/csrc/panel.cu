@@ -509,8 +509,23 @@ int64_t panel_scratch_doubles(int64_t b) {
 }
 
 int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView Y, double* tau,
-             MatView T, MatView* W, int max_ctas, Workspace* pws) {
+             MatView T, MatView* W, int max_ctas, Workspace* pws, LeafMarks* marks) {
   const int64_t j = P.rows, b = P.cols;
+  if (marks) marks->n = 0;
+  auto mark = [&](int64_t c0, int64_t c1) -> int {  // Y[:, c0:c1) final on st
+    if (!marks || !pws) return 0;
+    if (marks->n >= 64) {
+      set_error("panel_qr: more than 64 leaf marks");
+      return -1;
+    }
+    cudaEvent_t ev = ws_event(*pws);
+    BR_CUDA(cudaEventRecord(ev, st));
+    marks->c0[marks->n] = c0;
+    marks->c1[marks->n] = c1;
+    marks->ev[marks->n] = ev;
+    ++marks->n;
+    return 0;
+  };
   if (j < b || b < 1) {
     set_error("panel_qr needs j >= b >= 1, got %lld x %lld", (long long)j, (long long)b);
     return -1;
@@ -523,7 +538,8 @@ int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView 
   }
   if (b <= nbl) {
     // single leaf: Y, tau, T and W in one kernel
-    return launch_leaf(st, P, Y, tau, T.p, T.ld, W);
+    BR_CHECK(launch_leaf(st, P, Y, tau, T.p, T.ld, W));
+    return mark(0, b);
   }
   // multi-leaf, right-looking
   BR_CHECK(zero_fill(st, Y));
@@ -567,6 +583,7 @@ int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView 
     }
     BR_CUDA(cudaEventRecord(w.ev_aux1, w.aux));
     BR_CUDA(cudaStreamWaitEvent(st, w.ev_aux1, 0));
+    BR_CHECK(mark(0, b));
   }
   for (int64_t s = 0; s < b && !persist; s += nbl) {
     const int64_t e = std::min<int64_t>(s + nbl, b);
@@ -578,6 +595,7 @@ int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView 
       // Y_blk T_blk^T into W's columns (W itself is formed at the end)
       MatView What = W->sub(s, s, j - s, w);
       BR_CHECK(launch_leaf(st, leafP, leafY, tau + s, T.p + s + s * T.ld, T.ld, &What, 1));
+      BR_CHECK(mark(s, e));
       MatView rest = P.sub(s, e, j - s, b - e);
       MatView Zs = Z.sub(0, 0, w, b - e);
       BR_CHECK(gemm(st, ws, Zs, leafY.T(), rest, 1.0, 0.0, nullptr, max_ctas));
@@ -585,6 +603,7 @@ int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView 
       continue;
     }
     BR_CHECK(launch_leaf(st, leafP, leafY, tau + s, T.p + s + s * T.ld, T.ld, nullptr));
+    BR_CHECK(mark(s, e));
     if (e < b) {
       // P[s:, e:b] += Y_blk (T_blk^T (Y_blk^T P[s:, e:b])): the T_blk^T product
       // rides on the split-K reduction, so the leaf needs no W

@@ -44,6 +44,19 @@ static int panel_cap(int64_t rows) {
   return rows >= min_rows ? cap : 0;
 }
 
+// Trailing heights at or below which the triangular-band reduction pipelines
+// its Z products with the panels (BR_PZ_ROWS; 0 disables). Measured on c4
+// (2 x 3 runs): off 447.2 ms, 6144 445.9 ms, 8192 446.3 ms, 10240 469 ms (the
+// 16-wide leaves of taller panels make the leaf products too small to hide).
+static int64_t pz_rows() {
+  static int64_t r = -1;
+  if (r < 0) {
+    const char* e = std::getenv("BR_PZ_ROWS");
+    r = e ? std::atoll(e) : 6144;
+  }
+  return r;
+}
+
 static double panel_flops(int64_t j, int64_t b) {
   return 2.0 * j * b * b - 2.0 * b * b * b / 3.0 + (double)j * b * b;  // QR + T/W
 }
@@ -231,7 +244,7 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
   }
 
   const int64_t nYu = m * b, nYv = n * b, nT = b * b;
-  const int64_t total = 4 * nYu + 2 * nT + 2 * b + 2 * nYv + nT + b + b * n + m * b;
+  const int64_t total = 4 * nYu + 2 * nT + 2 * b + 2 * nYv + nT + b + 2 * (b * n + m * b);
   BR_CHECK(devbuf_reserve(ws.factors, total));
   BR_CHECK(devbuf_reserve(ws.skbuf_main, 4 * std::max(m, n) * b + (1 << 20)));
   BR_CHECK(devbuf_reserve(ws.skbuf_panel, 4 * std::max(m, n) * b + (1 << 20)));
@@ -258,6 +271,9 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
   double* tauv = f; f += b;
   double* ZL = f; f += b * n;
   double* ZR = f; f += m * b;
+  double* ZLr = f; f += b * n;  // Y_U^T E, leaf by leaf (pipelined Z_L)
+  double* ZRr = f; f += m * b;  // D Y_V, leaf by leaf (pipelined Z_R)
+  LeafMarks mk_qr[2], mk_lq;
 
   auto Aat = [&](int64_t r, int64_t c) { return A + r + c * lda; };
   auto qr = [&](cudaStream_t st, Scratch& sk, int64_t k, int64_t bp, int par) -> int {
@@ -265,14 +281,14 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
     MatView P(Aat(k, k), lda, i, bp);
     MatView Y(Yu[par], m, i, bp), T(Tu[par], b, bp, bp), W(Wu[par], m, i, bp);
     TimeScope ts(ws, st, TC_PANEL, panel_flops(i, bp), "qr", k);
-    return panel_qr(st, sk, ws.pscratch, P, Y, tauu[par], T, &W, panel_cap(i), &ws);
+    return panel_qr(st, sk, ws.pscratch, P, Y, tauu[par], T, &W, panel_cap(i), &ws, &mk_qr[par]);
   };
   auto lq = [&](cudaStream_t st, Scratch& sk, int64_t k, int64_t bq) -> int {
     const int64_t jr = n - k - w;
     MatView P(Aat(k, k + w), lda, jr, bq, true);  // transposed view of the bq x jr rows
     MatView Y(Yv, n, jr, bq), T(Tv, b, bq, bq), W(Wv, n, jr, bq);
     TimeScope ts(ws, st, TC_PANEL, panel_flops(jr, bq), "lq", k);
-    return panel_qr(st, sk, ws.pscratch, P, Y, tauv, T, &W, panel_cap(jr), &ws);
+    return panel_qr(st, sk, ws.pscratch, P, Y, tauv, T, &W, panel_cap(jr), &ws, &mk_lq);
   };
   auto handoff = [&]() -> int {  // main -> panel ordering point
     cudaEvent_t ev = ws_event(ws);
@@ -295,7 +311,12 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
   for (size_t idx = 0; idx < its.size(); ++idx) {
     const int64_t k = its[idx].k, bp = its[idx].bp, i = m - k;
     const int par = (int)(idx & 1);
-    if (ev_qr) {
+    // pipelined Z (short trailing matrices, where the panels are the critical
+    // path): Z_L = T_U^T (Y_U^T E) and Z_R = (D Y_V) T_V, the Y products taken
+    // leaf by leaf while the panel is still factoring its later leaves. The
+    // choice depends on i only, so depth 0 and depth 1 stay bitwise equal.
+    const bool pz = i <= pz_rows() && bp >= 64;  // multi-leaf panels only
+    if (ev_qr && !pz) {
       BR_CHECK(join(ev_qr));
       ev_qr = nullptr;
     }
@@ -320,7 +341,23 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
       // left update E := Q_U^T E = E + Y_U (W_U^T E)  (ref svd.py:191)
       MatView E(Aat(k, k + bp), lda, i, ncE);
       MatView Z(ZL, b, bp, ncE);
-      {
+      if (pz) {
+        const LeafMarks& mk = mk_qr[par];
+        MatView Zr(ZLr, b, bp, ncE);
+        for (int s = 0; s < mk.n; ++s) {
+          const int64_t c0 = mk.c0[s], wc = mk.c1[s] - c0;
+          BR_CUDA(cudaStreamWaitEvent(ws.main, mk.ev[s], 0));
+          TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(wc, ncE, i - c0), "zleft-leaf", k);
+          BR_CHECK(gemm(ws.main, ws.sk_main, Zr.sub(c0, 0, wc, ncE), Yuv.sub(c0, c0, i - c0, wc).T(),
+                        E.sub(c0, 0, i - c0, ncE), 1.0, 0.0));
+        }
+        if (ev_qr) {
+          BR_CHECK(join(ev_qr));
+          ev_qr = nullptr;
+        }
+        TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(bp, ncE, bp), "zleft", k);
+        BR_CHECK(gemm(ws.main, ws.sk_main, Z, MatView(Tu[par], b, bp, bp).T(), Zr, 1.0, 0.0));
+      } else {
         TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(bp, ncE, i), "zleft", k);
         BR_CHECK(gemm(ws.main, ws.sk_main, Z, Wuv.T(), E, 1.0, 0.0));
       }
@@ -343,14 +380,27 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
         }
         const int64_t splitc = has_next ? std::max<int64_t>(0, bp + bpn - w) : 0;
         if (la && splitc == 0) BR_CHECK(next_qr_on_panel());  // next panel is left-only
-        if (lookahead) BR_CHECK(join(ev_lq));
-        else BR_CHECK(lq(ws.main, ws.sk_main, k, bq));
+        if (!lookahead) BR_CHECK(lq(ws.main, ws.sk_main, k, bq));
+        else if (!pz) BR_CHECK(join(ev_lq));
         // right update D := D Q_V = D + (D W_V) Y_V^T (ref svd.py:199)
         MatView D(Aat(k + bq, k + w), lda, i - bq, jr);
         MatView Yvv(Yv, n, jr, bq), Wvv(Wv, n, jr, bq);
         MatView Zr(ZR, m, i - bq, bq);
+        if (pz && lookahead && i - bq <= 0) BR_CHECK(join(ev_lq));
         if (i - bq > 0) {
-          {
+          if (pz) {
+            MatView Zrr(ZRr, m, i - bq, bq);
+            for (int s = 0; s < mk_lq.n; ++s) {
+              const int64_t c0 = mk_lq.c0[s], wc = mk_lq.c1[s] - c0;
+              BR_CUDA(cudaStreamWaitEvent(ws.main, mk_lq.ev[s], 0));
+              TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, wc, jr - c0), "zright-leaf", k);
+              BR_CHECK(gemm(ws.main, ws.sk_main, Zrr.sub(0, c0, i - bq, wc), D.sub(0, c0, i - bq, jr - c0),
+                            Yvv.sub(c0, c0, jr - c0, wc), 1.0, 0.0));
+            }
+            if (lookahead) BR_CHECK(join(ev_lq));
+            TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, bq, bq), "zright", k);
+            BR_CHECK(gemm(ws.main, ws.sk_main, Zr, Zrr, MatView(Tv, b, bq, bq), 1.0, 0.0));
+          } else {
             TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, bq, jr), "zright", k);
             BR_CHECK(gemm(ws.main, ws.sk_main, Zr, D, Wvv, 1.0, 0.0));
           }
