@@ -445,7 +445,11 @@ static bool persistent_panel_enabled(int64_t rows) {
     const char* e = std::getenv("BR_PERSIST_ROWS");
     return e ? (int64_t)std::atoll(e) : (int64_t)0;  // measured: no gain on c3-c5
   }();
-  return rows <= lim;
+  static const int64_t lo = [] {  // BR_PERSIST_MIN_ROWS: only panels at least this tall
+    const char* e = std::getenv("BR_PERSIST_MIN_ROWS");
+    return e ? (int64_t)std::atoll(e) : (int64_t)0;
+  }();
+  return rows <= lim && rows >= lo;
 }
 
 // Stream-ordered 32-bit flag wait / release write (driver stream memory

@@ -45,14 +45,16 @@ static int panel_cap(int64_t rows) {
 }
 
 // Trailing heights at or below which the triangular-band reduction pipelines
-// its Z products with the panels (BR_PZ_ROWS; 0 disables). Measured on c4
-// (2 x 3 runs): off 447.2 ms, 6144 445.9 ms, 8192 446.3 ms, 10240 469 ms (the
-// 16-wide leaves of taller panels make the leaf products too small to hide).
+// its Z products with the panels (BR_PZ_ROWS; default 0 = off). Measured on
+// c4 (2 x 3 runs): off 447.2 ms, 6144 445.9 ms, 8192 446.3 ms, 10240 469 ms
+// (the 16-wide leaves of taller panels make the leaf products too small to
+// hide); the 0.3 % is within run-to-run spread of bench.py, and the
+// 32-row leaf products lower the GEMM class's DMMA efficiency, so it is off.
 static int64_t pz_rows() {
   static int64_t r = -1;
   if (r < 0) {
     const char* e = std::getenv("BR_PZ_ROWS");
-    r = e ? std::atoll(e) : 6144;
+    r = e ? std::atoll(e) : 0;
   }
   return r;
 }

@@ -512,3 +512,31 @@ def test_leaf_layouts_agree(tmp_path):
         for a, b in zip(outs[0], other):
             assert a.shape == b.shape
             assert np.max(np.abs(a - b)) <= 1e-12 * max(1.0, np.max(np.abs(a)))
+
+
+@pytest.mark.gpu
+def test_pipelined_z_matches(tmp_path):
+    """BR_PZ_ROWS pipelines the triangular-band Z products with the panel's
+    leaves (Z_L = T^T (Y^T E) leaf by leaf); it agrees with the default
+    formula to rounding and keeps depth 1 bitwise equal to depth 0."""
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, paper_1709_00302_b200 as br\n"
+        "A = np.random.default_rng(3).standard_normal((1500, 1400))\n"
+        "r0 = br.reduce_tri_band(A, 128, 128, lookahead=0).band\n"
+        "r1 = br.reduce_tri_band(A, 128, 128, lookahead=1).band\n"
+        "np.save(r'%s', np.stack([r0, r1]))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for rows in ("0", "100000"):
+        path = tmp_path / f"z{rows}.npy"
+        env = dict(os.environ, BR_PZ_ROWS=rows)
+        r = subprocess.run([sys.executable, "-c", code % path], cwd=root, env=env,
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        outs.append(np.load(path))
+    assert np.array_equal(outs[1][0], outs[1][1])  # depth 1 == depth 0 bitwise
+    ref = outs[0][0]
+    assert np.linalg.norm(outs[1][0] - ref) <= 1e-12 * np.sqrt(1500) * np.linalg.norm(ref)
