@@ -271,7 +271,8 @@ int timed_reduction(Workspace& ws, br_stats* stats, double nominal, Workspace::G
   // events recorded by captured graph nodes cannot be timed, so the timing /
   // trace modes stay eager
   const bool graphable =
-      graphs_enabled(nominal) && ws.timing == 0 && ws.main != nullptr && ws.band_out == nullptr;
+      graphs_enabled(nominal) && ws.timing == 0 && ws.main != nullptr && ws.band_out == nullptr &&
+      ws.band_in == nullptr;
   const bool same = graphable && key == ws.gkey;
   int rc = 0;
   int64_t iters = 0;
@@ -341,6 +342,32 @@ int timed_reduction(Workspace& ws, br_stats* stats, double nominal, Workspace::G
     stats->nominal_flops = nominal;
     stats->launches = launch_count() - l0;
   }
+  return 0;
+}
+
+int band_in_start(Workspace& ws, BandIn* bi) {
+  // the device buffer may still be read by work queued on main (none between
+  // synchronous calls, but order the copies after it anyway)
+  cudaEvent_t ev0 = ws_event(ws);
+  BR_CUDA(cudaEventRecord(ev0, ws.main));
+  BR_CUDA(cudaStreamWaitEvent(ws.copy_in, ev0, 0));
+  for (int c = 0; c < bi->nchunks; ++c) {
+    const int64_t c0 = (int64_t)c * bi->chunk, nc = std::min(bi->chunk, bi->cols - c0);
+    BR_CUDA(cudaMemcpy2DAsync(bi->A + c0 * bi->lda, bi->lda * sizeof(double), bi->host + c0 * bi->ldh,
+                              bi->ldh * sizeof(double), bi->rows * sizeof(double), nc,
+                              cudaMemcpyHostToDevice, ws.copy_in));
+    bi->ev[c] = ws_event(ws);
+    BR_CUDA(cudaEventRecord(bi->ev[c], ws.copy_in));
+  }
+  bi->waited = 0;
+  return 0;
+}
+
+int band_in_wait(Workspace& ws, BandIn* bi, int64_t upto) {
+  if (!bi) return 0;
+  const int need = (int)std::min<int64_t>(bi->nchunks, cdiv(std::max<int64_t>(upto, 0), bi->chunk));
+  for (; bi->waited < need; ++bi->waited)
+    BR_CUDA(cudaStreamWaitEvent(ws.main, bi->ev[bi->waited], 0));
   return 0;
 }
 
@@ -419,6 +446,7 @@ int br_create(int device, br_handle_t* out) {
   h->ws.panel = h->ws.own_panel;
   BR_CUDA(cudaStreamCreateWithPriority(&h->ws.aux, cudaStreamNonBlocking, hi));
   BR_CUDA(cudaStreamCreateWithFlags(&h->ws.copy, cudaStreamNonBlocking));
+  BR_CUDA(cudaStreamCreateWithFlags(&h->ws.copy_in, cudaStreamNonBlocking));
   BR_CUDA(cudaMalloc(&h->ws.flags, 128 * sizeof(unsigned)));
   BR_CUDA(cudaMemset(h->ws.flags, 0, 128 * sizeof(unsigned)));
   BR_CUDA(cudaEventCreateWithFlags(&h->ws.ev_aux0, cudaEventDisableTiming));
@@ -458,6 +486,7 @@ int br_destroy(br_handle_t h) {
   if (ws.ev_aux1) cudaEventDestroy(ws.ev_aux1);
   if (ws.aux) cudaStreamDestroy(ws.aux);
   if (ws.copy) cudaStreamDestroy(ws.copy);
+  if (ws.copy_in) cudaStreamDestroy(ws.copy_in);
   for (auto e : ws.events) cudaEventDestroy(e);
   for (auto e : ws.tevents) cudaEventDestroy(e);
   if (ws.gexec) cudaGraphExecDestroy(ws.gexec);
@@ -822,6 +851,16 @@ int br_reduce_band(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b, in
                          });
 }
 
+// BR_STREAM_IN=0 turns the streamed input off (A/B aid).
+static bool stream_in_enabled() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = std::getenv("BR_STREAM_IN");
+    m = (e && std::atoi(e) == 0) ? 0 : 1;
+  }
+  return m == 1;
+}
+
 // Stream the band out while reducing when the destination is pinned host
 // memory and the matrix is large (pageable D2H copies block the host thread).
 static bool setup_band_out(Workspace& ws, BandOut& bo, double* band, int64_t ldb, double* dA,
@@ -900,13 +939,41 @@ int br_reduce_tri_band_host(br_handle_t h, int64_t m, int64_t n, int64_t w, int6
   Workspace& ws = h->ws;
   DevBuf& dA = ws.stageA;
   int64_t ldd = 0;
-  BR_CHECK(host_stage_in(ws, m, n, A, lda, dA, ldd));
+  // pinned, large input: stream it in by column chunks while the first
+  // iteration's panel and left update start on the columns already there
+  cudaPointerAttributes pa;
+  const bool pinned_in = cudaPointerGetAttributes(&pa, A) == cudaSuccess &&
+                         pa.type == cudaMemoryTypeHost && stream_in_enabled();
+  cudaGetLastError();
+  BandIn bi;
+  const bool stream_in = pinned_in && m * n * (int64_t)sizeof(double) >= ((int64_t)64 << 20);
+  if (stream_in) {
+    ldd = (m + 31) / 32 * 32;
+    BR_CHECK(devbuf_reserve(dA, ldd * n));
+    bi.host = A;
+    bi.ldh = lda;
+    bi.A = dA.p;
+    bi.lda = ldd;
+    bi.rows = m;
+    bi.cols = n;
+    bi.chunk = std::max<int64_t>(b, cdiv(std::max<int64_t>(n / 16, 1), b) * b);
+    bi.nchunks = (int)cdiv(n, bi.chunk);
+    if (bi.nchunks > 256) {
+      bi.chunk = cdiv(cdiv(n, 256), b) * b;
+      bi.nchunks = (int)cdiv(n, bi.chunk);
+    }
+    ws.band_in = &bi;
+  } else {
+    BR_CHECK(host_stage_in(ws, m, n, A, lda, dA, ldd));
+  }
   BandOut bo;
   bo.lo = 0;
   bo.up = w;
   const bool streamed = setup_band_out(ws, bo, band, ldb, dA.p, ldd, m, n);
   const int rc = br_reduce_tri_band(h, m, n, w, b, lookahead, dA.p, ldd, stats);
   ws.band_out = nullptr;
+  ws.band_in = nullptr;
+  if (stream_in) BR_CUDA(cudaStreamSynchronize(ws.copy_in));
   if (streamed) BR_CUDA(cudaStreamSynchronize(ws.copy));
   BR_CHECK(rc);
   if (!streamed)

@@ -59,6 +59,8 @@ struct Workspace {
   GraphKey gkey;
   struct BandOut* band_out = nullptr;  // set by the host entry points while streaming out
   cudaStream_t copy = nullptr;         // D2H stream of the streamed band
+  struct BandIn* band_in = nullptr;    // set by the host entry points while streaming in
+  cudaStream_t copy_in = nullptr;      // H2D stream of the streamed input
   int gseen = 0;  // eager runs of gkey so far
   cudaGraphExec_t gexec = nullptr;
   int64_t g_iters = 0, g_launches = 0;
@@ -161,6 +163,21 @@ struct BandOut {
   int64_t done = 0;  // columns already queued
 };
 int band_out_flush(Workspace& ws, BandOut* bo, int64_t upto);
+// Input streamed in by column chunks (pinned host source): the reduction
+// starts on the first chunks while the rest are still in flight.
+struct BandIn {
+  const double* host = nullptr;
+  int64_t ldh = 0;
+  double* A = nullptr;
+  int64_t lda = 0, rows = 0, cols = 0;
+  int64_t chunk = 0;   // columns per chunk
+  int nchunks = 0;
+  int waited = 0;      // chunks the main stream already waits for
+  cudaEvent_t ev[256];
+};
+int band_in_start(Workspace& ws, BandIn* bi);
+// Main stream waits until columns [0, upto) have arrived.
+int band_in_wait(Workspace& ws, BandIn* bi, int64_t upto);
 int zero_fill(cudaStream_t st, MatView V);
 int set_identity(cudaStream_t st, double* Q, int64_t ldq, int64_t n);
 

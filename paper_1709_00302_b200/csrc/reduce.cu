@@ -240,7 +240,10 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
     k += bp;
   }
   *iterations = (int64_t)its.size();
+  BandIn* bi = ws.band_in;
+  if (bi) BR_CHECK(band_in_start(ws, bi));
   if (its.empty()) {
+    BR_CHECK(band_in_wait(ws, bi, n));
     if (bo) return band_out_flush(ws, bo, n);
     return mask_tri(ws.main, A, lda, m, n, 0, w);
   }
@@ -308,6 +311,7 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
     return 0;
   };
 
+  BR_CHECK(band_in_wait(ws, bi, its[0].bp));  // the first panel's columns
   BR_CHECK(qr(ws.main, ws.sk_main, its[0].k, its[0].bp, 0));
   cudaEvent_t ev_qr = nullptr;
   for (size_t idx = 0; idx < its.size(); ++idx) {
@@ -339,7 +343,70 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
       return 0;
     };
 
-    if (ncE > 0) {
+    // streamed input: iteration 0's left update runs column chunk by column
+    // chunk as the chunks arrive (every piece with its whole product's
+    // split-K plan, so the result is bitwise that of the one-shot update)
+    const bool chunked = bi && idx == 0 && ncE > 0 && bq > 0 && !pz;
+    if (!chunked) BR_CHECK(band_in_wait(ws, bi, n));
+    if (chunked) {
+      MatView E(Aat(k, k + bp), lda, i, ncE);
+      MatView Z(ZL, b, bp, ncE);
+      const int64_t kz = gemm_plan_kps(ws.sk_main, Z, Wuv.T(), E, 0.0);
+      const int64_t kr = gemm_plan_kps(ws.sk_main, E.sub(0, 0, bq, ncE), Yuv.sub(0, 0, bq, bp), Z, 1.0);
+      const int64_t ks = gemm_plan_kps(ws.sk_main, E.sub(bq, 0, i - bq, ncE), Yuv.sub(bq, 0, i - bq, bp),
+                                       Z, 1.0);
+      for (int64_t a0 = k + bp; a0 < n;) {
+        const int64_t a1 = std::min(n, (a0 / bi->chunk + 1) * bi->chunk);
+        BR_CHECK(band_in_wait(ws, bi, a1));
+        const int64_t e0 = a0 - k - bp, ne = a1 - a0;
+        MatView Ec = E.sub(0, e0, i, ne), Zc = Z.sub(0, e0, bp, ne);
+        TimeScope ts(ws, ws.main, TC_GEMM, 2 * gemm_flops(bp, ne, i), "left-chunk", k);
+        BR_CHECK(gemm(ws.main, ws.sk_main, Zc, Wuv.T(), Ec, 1.0, 0.0, nullptr, 0, kz));
+        BR_CHECK(gemm(ws.main, ws.sk_main, Ec.sub(0, 0, bq, ne), Yuv.sub(0, 0, bq, bp), Zc, 1.0, 1.0,
+                      nullptr, 0, kr));
+        BR_CHECK(gemm(ws.main, ws.sk_main, Ec.sub(bq, 0, i - bq, ne), Yuv.sub(bq, 0, i - bq, bp), Zc,
+                      1.0, 1.0, nullptr, 0, ks));
+        a0 = a1;
+      }
+      BR_CHECK(band_in_wait(ws, bi, n));
+      cudaEvent_t ev_lq = nullptr;
+      if (lookahead) {
+        BR_CHECK(handoff());
+        BR_CHECK(lq(ws.panel, ws.sk_panel, k, bq));
+        ev_lq = mark_panel();
+      }
+      const int64_t splitc = has_next ? std::max<int64_t>(0, bp + bpn - w) : 0;
+      if (la && splitc == 0) BR_CHECK(next_qr_on_panel());
+      if (lookahead) BR_CHECK(join(ev_lq));
+      else BR_CHECK(lq(ws.main, ws.sk_main, k, bq));
+      MatView D(Aat(k + bq, k + w), lda, i - bq, jr);
+      MatView Yvv(Yv, n, jr, bq), Wvv(Wv, n, jr, bq);
+      MatView Zr(ZR, m, i - bq, bq);
+      if (i - bq > 0) {
+        {
+          TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, bq, jr), "zright", k);
+          BR_CHECK(gemm(ws.main, ws.sk_main, Zr, D, Wvv, 1.0, 0.0));
+        }
+        if (la && !next_issued && splitc > 0) {
+          const int64_t sc = std::min(splitc, jr);
+          const int64_t kps = gemm_plan_kps(ws.sk_main, D, Zr, Yvv.T(), 1.0);
+          {
+            TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, sc, bq), "right-head", k);
+            BR_CHECK(gemm(ws.main, ws.sk_main, D.sub(0, 0, i - bq, sc), Zr, Yvv.sub(0, 0, sc, bq).T(),
+                          1.0, 1.0, nullptr, 0, kps));
+          }
+          BR_CHECK(next_qr_on_panel());
+          if (sc < jr) {
+            TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, jr - sc, bq), "right", k);
+            BR_CHECK(gemm(ws.main, ws.sk_main, D.sub(0, sc, i - bq, jr - sc), Zr,
+                          Yvv.sub(sc, 0, jr - sc, bq).T(), 1.0, 1.0, nullptr, 0, kps));
+          }
+        } else {
+          TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, jr, bq), "right", k);
+          BR_CHECK(gemm(ws.main, ws.sk_main, D, Zr, Yvv.T(), 1.0, 1.0));
+        }
+      }
+    } else if (ncE > 0) {
       // left update E := Q_U^T E = E + Y_U (W_U^T E)  (ref svd.py:191)
       MatView E(Aat(k, k + bp), lda, i, ncE);
       MatView Z(ZL, b, bp, ncE);
@@ -437,6 +504,7 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
     BR_CHECK(band_out_flush(ws, bo, k + bp));  // columns [0, k + bp) are final
   }
   if (ev_qr) BR_CHECK(join(ev_qr));
+  BR_CHECK(band_in_wait(ws, bi, n));
   if (bo) {
     BR_CHECK(band_out_flush(ws, bo, n));
     ws_events_reset(ws);

@@ -473,6 +473,14 @@ def test_streamed_band_output_matches(br, kind):
     assert np.array_equal(outs[0], outs[1])
     lo, up = {"sevp": (w, w), "tri": (0, w), "band": (w, w)}[kind]
     assert br.band_check(outs[0], lo, up) == 0.0
+    if kind == "tri":
+        # a pinned input is streamed in by column chunks (iteration 0's left
+        # update runs chunk by chunk); a pageable one is staged whole first
+        Ap = torch.from_numpy(np.asfortranarray(A).T.copy())
+        Bt = torch.empty((n, n), dtype=torch.float64).pin_memory()
+        _lib.check(lib.br_reduce_tri_band_host(h, n, n, w, b, 1, Ap.data_ptr(), n, Bt.data_ptr(), n,
+                                               _lib.BrStats()), kind)
+        assert np.array_equal(Bt.numpy().T, outs[0])
 
 
 @pytest.mark.gpu
