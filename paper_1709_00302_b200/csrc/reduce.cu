@@ -348,69 +348,15 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
     // split-K plan, so the result is bitwise that of the one-shot update)
     const bool chunked = bi && idx == 0 && ncE > 0 && bq > 0 && !pz;
     if (!chunked) BR_CHECK(band_in_wait(ws, bi, n));
-    if (chunked) {
-      MatView E(Aat(k, k + bp), lda, i, ncE);
-      MatView Z(ZL, b, bp, ncE);
-      const int64_t kz = gemm_plan_kps(ws.sk_main, Z, Wuv.T(), E, 0.0);
-      const int64_t kr = gemm_plan_kps(ws.sk_main, E.sub(0, 0, bq, ncE), Yuv.sub(0, 0, bq, bp), Z, 1.0);
-      const int64_t ks = gemm_plan_kps(ws.sk_main, E.sub(bq, 0, i - bq, ncE), Yuv.sub(bq, 0, i - bq, bp),
-                                       Z, 1.0);
-      for (int64_t a0 = k + bp; a0 < n;) {
-        const int64_t a1 = std::min(n, (a0 / bi->chunk + 1) * bi->chunk);
-        BR_CHECK(band_in_wait(ws, bi, a1));
-        const int64_t e0 = a0 - k - bp, ne = a1 - a0;
-        MatView Ec = E.sub(0, e0, i, ne), Zc = Z.sub(0, e0, bp, ne);
-        TimeScope ts(ws, ws.main, TC_GEMM, 2 * gemm_flops(bp, ne, i), "left-chunk", k);
-        BR_CHECK(gemm(ws.main, ws.sk_main, Zc, Wuv.T(), Ec, 1.0, 0.0, nullptr, 0, kz));
-        BR_CHECK(gemm(ws.main, ws.sk_main, Ec.sub(0, 0, bq, ne), Yuv.sub(0, 0, bq, bp), Zc, 1.0, 1.0,
-                      nullptr, 0, kr));
-        BR_CHECK(gemm(ws.main, ws.sk_main, Ec.sub(bq, 0, i - bq, ne), Yuv.sub(bq, 0, i - bq, bp), Zc,
-                      1.0, 1.0, nullptr, 0, ks));
-        a0 = a1;
-      }
-      BR_CHECK(band_in_wait(ws, bi, n));
-      cudaEvent_t ev_lq = nullptr;
-      if (lookahead) {
-        BR_CHECK(handoff());
-        BR_CHECK(lq(ws.panel, ws.sk_panel, k, bq));
-        ev_lq = mark_panel();
-      }
-      const int64_t splitc = has_next ? std::max<int64_t>(0, bp + bpn - w) : 0;
-      if (la && splitc == 0) BR_CHECK(next_qr_on_panel());
-      if (lookahead) BR_CHECK(join(ev_lq));
-      else BR_CHECK(lq(ws.main, ws.sk_main, k, bq));
-      MatView D(Aat(k + bq, k + w), lda, i - bq, jr);
-      MatView Yvv(Yv, n, jr, bq), Wvv(Wv, n, jr, bq);
-      MatView Zr(ZR, m, i - bq, bq);
-      if (i - bq > 0) {
-        {
-          TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, bq, jr), "zright", k);
-          BR_CHECK(gemm(ws.main, ws.sk_main, Zr, D, Wvv, 1.0, 0.0));
-        }
-        if (la && !next_issued && splitc > 0) {
-          const int64_t sc = std::min(splitc, jr);
-          const int64_t kps = gemm_plan_kps(ws.sk_main, D, Zr, Yvv.T(), 1.0);
-          {
-            TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, sc, bq), "right-head", k);
-            BR_CHECK(gemm(ws.main, ws.sk_main, D.sub(0, 0, i - bq, sc), Zr, Yvv.sub(0, 0, sc, bq).T(),
-                          1.0, 1.0, nullptr, 0, kps));
-          }
-          BR_CHECK(next_qr_on_panel());
-          if (sc < jr) {
-            TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, jr - sc, bq), "right", k);
-            BR_CHECK(gemm(ws.main, ws.sk_main, D.sub(0, sc, i - bq, jr - sc), Zr,
-                          Yvv.sub(sc, 0, jr - sc, bq).T(), 1.0, 1.0, nullptr, 0, kps));
-          }
-        } else {
-          TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, jr, bq), "right", k);
-          BR_CHECK(gemm(ws.main, ws.sk_main, D, Zr, Yvv.T(), 1.0, 1.0));
-        }
-      }
-    } else if (ncE > 0) {
+    if (ncE > 0) {
       // left update E := Q_U^T E = E + Y_U (W_U^T E)  (ref svd.py:191)
       MatView E(Aat(k, k + bp), lda, i, ncE);
       MatView Z(ZL, b, bp, ncE);
-      if (pz) {
+      auto zleft = [&]() -> int {
+        if (!pz) {
+          TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(bp, ncE, i), "zleft", k);
+          return gemm(ws.main, ws.sk_main, Z, Wuv.T(), E, 1.0, 0.0);
+        }
         const LeafMarks& mk = mk_qr[par];
         MatView Zr(ZLr, b, bp, ncE);
         for (int s = 0; s < mk.n; ++s) {
@@ -425,27 +371,48 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
           ev_qr = nullptr;
         }
         TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(bp, ncE, bp), "zleft", k);
-        BR_CHECK(gemm(ws.main, ws.sk_main, Z, MatView(Tu[par], b, bp, bp).T(), Zr, 1.0, 0.0));
-      } else {
-        TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(bp, ncE, i), "zleft", k);
-        BR_CHECK(gemm(ws.main, ws.sk_main, Z, Wuv.T(), E, 1.0, 0.0));
-      }
+        return gemm(ws.main, ws.sk_main, Z, MatView(Tu[par], b, bp, bp).T(), Zr, 1.0, 0.0);
+      };
       if (bq > 0) {
-        {  // rows of the LQ panel first
-          TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(bq, ncE, bp), "left-lq-rows", k);
-          BR_CHECK(gemm(ws.main, ws.sk_main, E.sub(0, 0, bq, ncE), Yuv.sub(0, 0, bq, bp), Z, 1.0,
-                        1.0));
-        }
         cudaEvent_t ev_lq = nullptr;
-        if (lookahead) {
+        auto issue_lq = [&]() -> int {  // LQ on the panel stream once its rows are updated
+          if (!lookahead) return 0;
           BR_CHECK(handoff());
           BR_CHECK(lq(ws.panel, ws.sk_panel, k, bq));
           ev_lq = mark_panel();
-        }
-        {
+          return 0;
+        };
+        if (chunked) {
+          const int64_t kz = gemm_plan_kps(ws.sk_main, Z, Wuv.T(), E, 0.0);
+          const int64_t kr = gemm_plan_kps(ws.sk_main, E.sub(0, 0, bq, ncE), Yuv.sub(0, 0, bq, bp), Z, 1.0);
+          const int64_t ks = gemm_plan_kps(ws.sk_main, E.sub(bq, 0, i - bq, ncE),
+                                           Yuv.sub(bq, 0, i - bq, bp), Z, 1.0);
+          for (int64_t a0 = k + bp; a0 < n;) {
+            const int64_t a1 = std::min(n, (a0 / bi->chunk + 1) * bi->chunk);
+            BR_CHECK(band_in_wait(ws, bi, a1));
+            const int64_t e0 = a0 - k - bp, ne = a1 - a0;
+            MatView Ec = E.sub(0, e0, i, ne), Zc = Z.sub(0, e0, bp, ne);
+            TimeScope ts(ws, ws.main, TC_GEMM, 2 * gemm_flops(bp, ne, i), "left-chunk", k);
+            BR_CHECK(gemm(ws.main, ws.sk_main, Zc, Wuv.T(), Ec, 1.0, 0.0, nullptr, 0, kz));
+            BR_CHECK(gemm(ws.main, ws.sk_main, Ec.sub(0, 0, bq, ne), Yuv.sub(0, 0, bq, bp), Zc, 1.0,
+                          1.0, nullptr, 0, kr));
+            BR_CHECK(gemm(ws.main, ws.sk_main, Ec.sub(bq, 0, i - bq, ne), Yuv.sub(bq, 0, i - bq, bp),
+                          Zc, 1.0, 1.0, nullptr, 0, ks));
+            a0 = a1;
+          }
+          BR_CHECK(band_in_wait(ws, bi, n));
+          BR_CHECK(issue_lq());
+        } else {
+          BR_CHECK(zleft());
+          {  // rows of the LQ panel first
+            TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(bq, ncE, bp), "left-lq-rows", k);
+            BR_CHECK(gemm(ws.main, ws.sk_main, E.sub(0, 0, bq, ncE), Yuv.sub(0, 0, bq, bp), Z, 1.0,
+                          1.0));
+          }
+          BR_CHECK(issue_lq());
           TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, ncE, bp), "left", k);
-          BR_CHECK(gemm(ws.main, ws.sk_main, E.sub(bq, 0, i - bq, ncE), Yuv.sub(bq, 0, i - bq, bp),
-                        Z, 1.0, 1.0));
+          BR_CHECK(gemm(ws.main, ws.sk_main, E.sub(bq, 0, i - bq, ncE), Yuv.sub(bq, 0, i - bq, bp), Z,
+                        1.0, 1.0));
         }
         const int64_t splitc = has_next ? std::max<int64_t>(0, bp + bpn - w) : 0;
         if (la && splitc == 0) BR_CHECK(next_qr_on_panel());  // next panel is left-only
@@ -493,6 +460,7 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
           }
         }
       } else {
+        BR_CHECK(zleft());
         TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i, ncE, bp), "left", k);
         BR_CHECK(gemm(ws.main, ws.sk_main, E, Yuv, Z, 1.0, 1.0));
       }
