@@ -132,7 +132,12 @@ int br_reduce_sym_band(br_handle_t h, int64_t n, int64_t w, int64_t b, int looka
 int br_reduce_tri_band(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b, int lookahead,
                        double* A, int64_t lda, br_stats* stats);
 /* Host-buffer variants: copy A (host, lda) to the device, reduce, copy the
- * band back to `band` (host, ldb). Host buffers may be pageable or pinned. */
+ * band back to `band` (host, ldb). Host buffers may be pageable or pinned.
+ * Pinned buffers of 64 MiB and more are streamed: finished band column
+ * blocks are copied out while the reduction runs, and (triangular band) the
+ * input is copied in by column chunks while iteration 0's panel and left
+ * update start on the chunks already there. Results are bitwise those of
+ * the staged copies. */
 int br_reduce_sym_band_host(br_handle_t h, int64_t n, int64_t w, int64_t b, int lookahead,
                             const double* A, int64_t lda, double* band, int64_t ldb, double* Q,
                             int64_t ldq, br_stats* stats);
