@@ -147,7 +147,7 @@ static int launch_leaf2_t(cudaStream_t st, const LeafArgs& a) {
   constexpr int ROWS = (NW / (NB / 8)) * 256;
   int C = 1;
   while (C < cdiv(a.L, ROWS)) C *= 2;
-  const size_t smem = ((size_t)NB * ROWS + 2 * (size_t)NB * (NB + 1)) * sizeof(double);
+  const size_t smem = ((size_t)NB * (ROWS + 8) + 2 * (size_t)NB * (NB + 1)) * sizeof(double);
   static int attr_dev_mask = 0;
   int dev = 0;
   BR_CUDA(cudaGetDevice(&dev));

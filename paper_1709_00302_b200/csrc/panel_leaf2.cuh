@@ -51,8 +51,11 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
   __shared__ __align__(16) double recvr[2][NB];          // row i from CTA 0
   __shared__ __align__(8) uint64_t mbar[2];
   __shared__ double scal[NB][3];  // x0 -> tau, beta, rinv
-  double(*G)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(Ys + NB * ROWS);
-  double(*Ts)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(Ys + NB * ROWS + NB * (NB + 1));
+  // Ys column stride padded by 8 doubles: the W fragment loads
+  // Ys[(k0 + tq) * YLD + r] of tq = 0,1 (and 2,3) then fill distinct banks
+  constexpr int YLD = ROWS + 8;
+  double(*G)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(Ys + NB * YLD);
+  double(*Ts)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(Ys + NB * YLD + NB * (NB + 1));
 
   const uint32_t rank = cluster_ctarank(), ncta = cluster_nctarank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -316,7 +319,7 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
       for (int c = 0; c < 8; ++c) {
         const int col = wcg * 8 + c;
         const double y = (col < nb && row >= col) ? p[r][c] : 0.0;
-        if (a.W) Ys[col * ROWS + lrow] = y;  // staged for W = Y T only
+        if (a.W) Ys[col * YLD + lrow] = y;  // staged for W = Y T only
         if (col < nb && row < Lr) a.Y[row + (int64_t)col * a.ldy] = y;
       }
     }
@@ -386,7 +389,7 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int r0 = rb + u * NW * 8;
-          const double av = (r0 < ROWS) ? Ys[(k0 + tq) * ROWS + r0 + gq] : 0.0;
+          const double av = (r0 < ROWS) ? Ys[(k0 + tq) * YLD + r0 + gq] : 0.0;
 #pragma unroll
           for (int n = 0; n < NB / 8; ++n) {
             if (!a.wt && k0 >= n * 8 + 8) continue;  // zero blocks of the triangular T
