@@ -298,14 +298,19 @@ def reduce_tri_band_dist(Aloc: CMat, lay: Layout, w: int, ops, comm, lookahead: 
     Tu = [ops.alloc(b, b, zero=True), ops.alloc(b, b, zero=True)]
     tauu = [ops.alloc(b, 1), ops.alloc(b, 1)]
     Yv, Wv, Tv, tauv = ops.alloc(n, b), ops.alloc(n, b), ops.alloc(b, b, zero=True), ops.alloc(b, 1)
-    Zl = ops.alloc(b, b)
+    Zl = ops.alloc(b, max(b, lay.ncols_local))
     Zr = ops.alloc(m, b)
     rowp = ops.alloc(b, n)  # gathered LQ row panel (b x jr)
-    send = ops.alloc(b, b * max(1, len(lay.owned)))
+    Yg = ops.alloc(lay.ncols_local + b, b)  # Y_V / W_V rows of the owned blocks, gathered
+    Wg = ops.alloc(lay.ncols_local + b, b)
 
     def block(t, r0, r1=None):
         s = lay.slot(t)
         return Aloc.view(r0, m if r1 is None else r1, s * b, (s + 1) * b)
+
+    def blocks(s0, r0, r1=None):
+        """Owned block columns from local slot s0 on: one contiguous local range."""
+        return Aloc.view(r0, m if r1 is None else r1, s0 * b, lay.ncols_local)
 
     its = []
     k = 0
@@ -329,49 +334,56 @@ def reduce_tri_band_dist(Aloc: CMat, lay: Layout, w: int, ops, comm, lookahead: 
         comm.broadcast(T, owner)
         ops.gemm(W, Y, T)  # same kernel on every rank -> identical W everywhere
         mine = [c for c in lay.owned if c > t]
-        # ---- left update, local per owned block column ----
-        for c in mine:
-            E = block(c, k)
-            ops.gemm(Zl, W, E, 1.0, 0.0, ta=True)
-            ops.gemm(E, Y, Zl, 1.0, 1.0)
+        nown = len(mine)
+        s0 = lay.slot(mine[0]) if nown else lay.ncols_local // b
+        # ---- left update of all owned trailing block columns (one local range) ----
+        if nown:
+            E = blocks(s0, k)
+            Z = Zl.view(0, b, 0, nown * b)
+            ops.gemm(Z, W, E, 1.0, 0.0, ta=True)
+            ops.gemm(E, Y, Z, 1.0, 1.0)
         jr = n - k - w
         if jr < 1:
             continue
         # ---- LQ row panel: all-gather the owned b x b pieces, factor everywhere ----
         nb_right = (n - (k + b)) // b  # blocks t+1 .. nblk-1
-        nown = len(mine)
-        sendv = send.view(0, b, 0, b * max(1, nown))
-        for q, c in enumerate(mine):
-            ops.copy(sendv.view(0, b, q * b, (q + 1) * b), block(c, k, k + b))
         per = -(-nb_right // P)  # max blocks any rank owns among t+1..
         stage = torch.zeros((P, per * b, b), dtype=torch.float64, device=Aloc.t.device)
         if nown:
-            stage[me, : nown * b].copy_(sendv.t[: nown * b, :b])
+            stage[me, : nown * b].copy_(Aloc.t[s0 * b: lay.ncols_local, k: k + b])
         parts = [torch.empty_like(stage[0]) for _ in range(P)]
         comm.all_gather(parts, stage[me].contiguous())
         R = rowp.view(0, b, 0, jr)
+        R3 = rowp.t[: nb_right * b].view(nb_right, b, rowp.t.shape[1])
         for r in range(P):
-            blks = [c for c in range(t + 1, lay.nblk) if c % P == r]
-            for q, c in enumerate(blks):
-                cc = (c - t - 1) * b
-                R.t[cc : cc + b, :b].copy_(parts[r][q * b : (q + 1) * b])
+            first = (r - (t + 1)) % P  # first block t+1+first owned by rank r
+            cnt = len(range(first, nb_right, P))
+            if cnt:
+                R3[first::P, :, :b].copy_(parts[r][: cnt * b].view(cnt, b, b))
         Yvv, Wvv = Yv.view(0, jr, 0, b), Wv.view(0, jr, 0, b)
         ops.qr_panel(R, Yvv, Tv, Wvv, tauv, lq=True)
         if lay.owner(t + 1) == me:  # L into block t+1's rows k..k+b
             ops.copy(block(t + 1, k, k + b), R.view(0, b, 0, b))
         # ---- right update: partial Z over owned columns, all-reduce, local apply ----
         Zv = Zr.view(0, i - b, 0, b)
-        ops.zero(Zv)
-        for c in mine:
-            cc = (c - t - 1) * b
-            ops.gemm(Zv, block(c, k + b), Wvv.view(cc, cc + b, 0, b), 1.0, 1.0)
+        if nown:
+            # rows of Y_V / W_V belonging to the owned blocks, in local order
+            first = (me - (t + 1)) % P
+            Yg3 = Yg.t[:b, : nown * b].view(b, nown, b)
+            Wg3 = Wg.t[:b, : nown * b].view(b, nown, b)
+            Yv3 = Yv.t[:b, : nb_right * b].view(b, nb_right, b)
+            Wv3 = Wv.t[:b, : nb_right * b].view(b, nb_right, b)
+            Yg3.copy_(Yv3[:, first::P, :])
+            Wg3.copy_(Wv3[:, first::P, :])
+            ops.gemm(Zv, blocks(s0, k + b), Wg.view(0, nown * b, 0, b), 1.0, 0.0)
+        else:
+            ops.zero(Zv)
         comm.all_reduce(Zv)
         nxt = t + 1 if idx + 1 < len(its) else None
-        order = list(mine)
-        if lookahead and nxt is not None and lay.owner(nxt) == me and nxt in order:
-            cc = (nxt - t - 1) * b
-            ops.gemm(block(nxt, k + b), Zv, Yvv.view(cc, cc + b, 0, b), 1.0, 1.0, tb=True)
-            order.remove(nxt)
+        lead = 0
+        if lookahead and nxt is not None and lay.owner(nxt) == me and nown and mine[0] == nxt:
+            ops.gemm(block(nxt, k + b), Zv, Yg.view(0, b, 0, b), 1.0, 1.0, tb=True)
+            lead = 1
             kn = its[idx + 1]
             ops.join(waiter_panel=True)
             ops.panel_stream(True)
@@ -379,9 +391,9 @@ def reduce_tri_band_dist(Aloc: CMat, lay: Layout, w: int, ops, comm, lookahead: 
                          tauu[par ^ 1])
             ops.panel_stream(False)
             prefetched = True
-        for c in order:
-            cc = (c - t - 1) * b
-            ops.gemm(block(c, k + b), Zv, Yvv.view(cc, cc + b, 0, b), 1.0, 1.0, tb=True)
+        if nown > lead:
+            ops.gemm(blocks(s0 + lead, k + b), Zv, Yg.view(lead * b, nown * b, 0, b), 1.0, 1.0,
+                     tb=True)
     return len(its)
 
 
