@@ -210,11 +210,16 @@ static int launch_leaf2(cudaStream_t st, const LeafArgs& a, bool* done) {
     if (L <= (int64_t)LEAF_MAXC * 512) return launch_leaf2_t<32, 8>(st, a);
     return *done = false, 0;
   }
+  if (a.nb <= 8 && L > (int64_t)LEAF_MAXC * 1024) {
+    // 8-wide leaves of the tallest panels (c5): 16 x 2048-row CTAs, 8 row groups
+    if (L <= (int64_t)LEAF_MAXC * 2048) return launch_leaf2_t<8, 8>(st, a);
+    return *done = false, 0;
+  }
   if (L <= 256) return launch_leaf2_t<16, 2>(st, a);
   if (!wide && L <= (int64_t)LEAF_MAXC * 512) return launch_leaf2_t<16, 4>(st, a);
-  // 16 x 1024-row CTAs (4 row groups): the 1D layout measured faster (16384 x 16:
-  // 53 vs 62 us), so the 8-warp 2D form is only taken with BR_LEAF2_WIDE=1
-  if (wide && L <= (int64_t)LEAF_MAXC * 1024) return launch_leaf2_t<16, 8>(st, a);
+  // 16 x 1024-row CTAs (4 row groups, combined in shared memory before the
+  // cluster exchange): 16384 x 16 51.9 us vs 53-57 us for the 1D layout
+  if (L <= (int64_t)LEAF_MAXC * 1024) return launch_leaf2_t<16, 8>(st, a);
   return *done = false, 0;
 }
 
@@ -685,6 +690,7 @@ int preload_panel_kernels() {
   BR_CHECK((launch_leaf_t<8, 8, 128>(0, a)));
   BR_CHECK((launch_leaf_t<8, 8, 256>(0, a)));
   BR_CHECK((launch_leaf2_t<64, 8>(0, a)));
+  BR_CHECK((launch_leaf2_t<8, 8>(0, a)));
   BR_CHECK((launch_leaf2_t<32, 4>(0, a)));
   BR_CHECK((launch_leaf2_t<32, 8>(0, a)));
   BR_CHECK((launch_leaf2_t<16, 2>(0, a)));

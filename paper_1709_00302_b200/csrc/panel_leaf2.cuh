@@ -11,7 +11,7 @@ __device__ __forceinline__ void st_async_f64(uint32_t raddr, double a, uint32_t 
       : "memory");
 }
 
-// One leaf (L x nb, nb <= NB, NB in {16, 32, 64}) of a Householder panel, same
+// One leaf (L x nb, nb <= NB, NB in {8, 16, 32, 64}) of a Householder panel, same
 // outputs and arithmetic contract as leaf_reg_kernel (Y, tau, T, W, R rows of
 // P), with a 2D layout: warp w owns the 8 columns 8*(w % CG) .. +8 (CG = NB/8
 // column groups) of the 256 rows of its row group rg = w / CG, and lane l of
@@ -39,7 +39,11 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
   constexpr int RG = NW / CG;     // row groups (256 rows each)
   constexpr int ROWS = RG * 256;  // rows per CTA
   constexpr int NT = NW * 32;
-  constexpr int MAXSRC = LEAF_MAXC * RG;
+  // PRE: the RG row-group warps of a column group first combine their slot
+  // partials through shared memory (named barrier), so each CTA pushes one
+  // partial vector instead of RG (fewer st.async, 4x shorter receive sums at RG = 4)
+  constexpr bool PRE = RG > 1;
+  constexpr int MAXSRC = PRE ? LEAF_MAXC : LEAF_MAXC * RG;
   constexpr int RB = (NB + 31) / 32;  // register rows that can hold rows < NB
   static_assert(CG * RG == NW && RG >= 1, "warp layout");
   // dynamic: Ys [NB][ROWS] (epilogue), G [NB][NB+1] (Gram), Ts [NB][NB+1] (T)
@@ -49,6 +53,8 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
   __shared__ __align__(16) double recv[2][MAXSRC][NB];   // slot partials per source
   __shared__ __align__(16) double recvn[2][MAXSRC];      // ||x||^2 partials per source
   __shared__ __align__(16) double recvr[2][NB];          // row i from CTA 0
+  __shared__ double pre[RG][NB];                         // PRE: row-group slot partials
+  __shared__ double pren[RG];
   __shared__ __align__(8) uint64_t mbar[2];
   __shared__ double scal[NB][3];  // x0 -> tau, beta, rinv
   // Ys column stride padded by 8 doubles: the W fragment loads
@@ -64,7 +70,7 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
   const int lrow0 = rg * 256 + lane;  // local row of register row r: lrow0 + 32 r
   const int64_t gr0 = base + lrow0;
   const bool xch = (ncta > 1) || (RG > 1);
-  const int nsrc = (int)ncta * RG;
+  const int nsrc = PRE ? (int)ncta : (int)ncta * RG;
   const int nb = a.nb;
   const int64_t Lr = a.L;
   const MatView P = a.P;
@@ -115,7 +121,8 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
   // of row group 0 in CTA 0
   const bool top = (rank == 0 && rg == 0);
   // remote addresses of this lane's pushes (buffer 0; buffer 1 at a fixed offset)
-  const int src = (int)rank * RG + rg;
+  const int src = PRE ? (int)rank : (int)rank * RG + rg;
+  const bool pusher = !PRE || rg == 0;  // warps whose slot totals leave the CTA
   const int pu = lane & 7, ppair = lane >> 3;
   uint32_t ra_s[2] = {0, 0}, ra_sm[2] = {0, 0}, ra_n = 0, ra_nm = 0, ra_r[2] = {0, 0},
            ra_rm[2] = {0, 0};
@@ -124,7 +131,7 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       const int q = pu + 8 * k;
-      if (q < (int)ncta) {
+      if (q < (int)ncta && pusher) {
         vmask |= 1u << k;
         ra_s[k] = map_cluster(&recv[0][src][wcg * 8 + 2 * ppair], (uint32_t)q);
         ra_sm[k] = map_cluster(&mbar[0], (uint32_t)q);
@@ -136,7 +143,7 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
         ra_rm[k] = map_cluster(&mbar[0], (uint32_t)(t >> 2));
       }
     }
-    if (lane < (int)ncta && wcg == 0) {
+    if (lane < (int)ncta && wcg == 0 && pusher) {
       vmask |= 16u;
       ra_n = map_cluster(&recvn[0][src], (uint32_t)lane);
       ra_nm = map_cluster(&mbar[0], (uint32_t)lane);
@@ -191,7 +198,7 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
       nr0 = fma(xv[r], xv[r], nr0);
       nr1 = fma(xv[r + 1], xv[r + 1], nr1);
     }
-    const double nr = warp_sum(nr0 + nr1);  // independent of the slots: overlaps them
+    double nr = warp_sum(nr0 + nr1);  // independent of the slots: overlaps them
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       double t0 = 0.0, t1 = 0.0;
@@ -211,6 +218,23 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
       nrm2 = nr;
     } else {
       // ---- 3. push slot pairs (and the norm from column group 0) to every CTA ----
+      if (PRE) {  // combine the row groups of this column group first (fixed order)
+        if ((lane & 3) == 0) pre[rg][wcg * 8 + sl] = s[0];
+        if (wcg == 0 && lane == 0) pren[rg] = nr;
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + wcg), "r"(RG * 32) : "memory");
+        if (rg == 0) {
+          double t = 0.0;
+#pragma unroll
+          for (int g = 0; g < RG; ++g) t += pre[g][wcg * 8 + sl];
+          s[0] = t;
+          if (wcg == 0) {
+            double u = 0.0;
+#pragma unroll
+            for (int g = 0; g < RG; ++g) u += pren[g];
+            nr = u;
+          }
+        }
+      }
       const double oth = __shfl_xor_sync(FULL, s[0], 4);
       const double v0 = (pu < 4) ? s[0] : oth, v1 = (pu < 4) ? oth : s[0];
 #pragma unroll

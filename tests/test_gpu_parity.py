@@ -498,7 +498,7 @@ def test_leaf_layouts_agree(tmp_path):
         "out = []\n"
         "for j, b, s in [(200, 32, 1), (3000, 32, 2), (6000, 32, 3), (250, 12, 4), (5000, 16, 5),\n"
         "                (12000, 16, 6), (777, 29, 7), (4096, 256, 8), (3000, 64, 9),\n"
-        "                (1000, 50, 10), (2500, 128, 11)]:\n"
+        "                (1000, 50, 10), (2500, 128, 11), (20000, 8, 12)]:\n"
         "    A = np.random.default_rng(s).standard_normal((j, b))\n"
         "    if s == 7:\n"
         "        A[:, 3] = 0.0; A[5:, 9] = 0.0\n"
