@@ -548,3 +548,39 @@ def test_pipelined_z_matches(tmp_path):
     assert np.array_equal(outs[1][0], outs[1][1])  # depth 1 == depth 0 bitwise
     ref = outs[0][0]
     assert np.linalg.norm(outs[1][0] - ref) <= 1e-12 * np.sqrt(1500) * np.linalg.norm(ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env", [{"BR_LEAF_W": "0"},
+                                 {"BR_PANEL_CAP": "16", "BR_PANEL_CAP_ROWS": "0"},
+                                 {"BR_PANEL_CAP": "16", "BR_PANEL_CAP_ROWS": "0", "BR_PANEL_CAP_GRID": "0"},
+                                 {"BR_PERSIST_ROWS": "100000"},
+                                 {"BR_LEAF2": "0"}])
+def test_tuning_modes_agree(tmp_path, env):
+    """The measured-and-kept tuning modes (T^T inside the split-K reduction,
+    capped panel GEMMs, persistent panels, the 1D leaf) reduce to the same
+    bands as the default path, to rounding, with depth 1 == depth 0 bitwise."""
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, paper_1709_00302_b200 as br\n"
+        "G = np.random.default_rng(11).standard_normal((900, 900))\n"
+        "S = (G + G.T) / 2\n"
+        "out = []\n"
+        "for la in (0, 1):\n"
+        "    out.append(br.reduce_tri_band(G, 96, 96, lookahead=la).band)\n"
+        "    out.append(br.reduce_sym_band(S, br.SevpConfig(900, 96, 96), lookahead=la).band)\n"
+        "np.save(r'%s', np.stack(out))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for e in ({}, env):
+        path = tmp_path / f"m{len(outs)}.npy"
+        r = subprocess.run([sys.executable, "-c", code % path], cwd=root, env=dict(os.environ, **e),
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        outs.append(np.load(path))
+    base, mode = outs
+    assert np.array_equal(mode[0], mode[2]) and np.array_equal(mode[1], mode[3])
+    for a, b in zip(base, mode):
+        assert np.linalg.norm(a - b) <= 1e-12 * np.sqrt(900) * np.linalg.norm(a)
