@@ -170,17 +170,6 @@ static int run_gemm(int am, cudaStream_t st, Scratch& ws, GemmArgs g, bool btran
   }
   g.k_per_split = S > 1 ? kps : g.K;
   dim3 grid((unsigned)cdiv(g.M, bm), (unsigned)cdiv(g.N, bn), (unsigned)S);
-  static const bool grid_cap = [] {  // BR_PANEL_CAP_GRID=0: a cap only shapes split-K
-    const char* e = std::getenv("BR_PANEL_CAP_GRID");
-    return !(e && std::atoi(e) == 0);
-  }();
-  if (grid_cap && max_ctas > 0 && (int64_t)grid.x * grid.y * grid.z > max_ctas) {
-    g.persist = 1;
-    g.tiles_x = (int)grid.x;
-    g.tiles_y = (int)grid.y;
-    g.tiles_z = (int)grid.z;
-    grid = dim3((unsigned)max_ctas, 1, 1);
-  }
   const int bmd = btrans ? B_T : B_N;
   if (tt) {  // C = T^T (sum of partials): always through the workspace
     if (S * g.M * g.N > ws.cap) {

@@ -51,8 +51,6 @@ struct GemmArgs {
   int64_t c0, c1;       // EPI_LOWER: rows [c0, M) x cols [c0, c1)
   int vecA, vecB;       // 16-byte cp.async allowed for A / B
   int b_upper;          // B_N with B upper triangular: K range of a tile ends at its last column
-  int persist;          // capped grid: CTAs loop over tiles_x * tiles_y * tiles_z tiles
-  int tiles_x, tiles_y, tiles_z;
 };
 
 // Host-side launch helpers (gemm.cu). All return 0 or a positive CUDA error.

@@ -380,19 +380,6 @@ template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, int AM, 
 __global__ void __launch_bounds__(WM* WN * 32, MINB) dgemm_kernel(const GemmArgs g) {
   dgemm_tile<BM, BN, BK, WM, WN, STAGES, MINB, AM, BMD, EPI>(g, blockIdx.x, blockIdx.y, blockIdx.z);
 }
-// Capped grid (g.persist): CTAs walk the tiles in order, so a panel's small
-// GEMMs hold at most gridDim.x CTA slots of the SMs the concurrent trailing
-// update runs on. A separate instantiation keeps the one-tile kernels' code
-// (and register allocation) unchanged.
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, int AM, int BMD, int EPI>
-__global__ void __launch_bounds__(WM* WN * 32, MINB) dgemm_kernel_persist(const GemmArgs g) {
-  const unsigned tx = (unsigned)g.tiles_x, txy = tx * (unsigned)g.tiles_y;
-  const unsigned total = txy * (unsigned)g.tiles_z;
-  for (unsigned t = blockIdx.x; t < total; t += gridDim.x) {
-    dgemm_tile<BM, BN, BK, WM, WN, STAGES, MINB, AM, BMD, EPI>(g, t % tx, (t % txy) / tx, t / txy);
-    __syncthreads();  // shared-memory stages are reused by the next tile
-  }
-}
 
 template <int BM, int BN, int BK, int STAGES, int AM, int BMD>
 constexpr int smem_bytes() {
@@ -407,21 +394,15 @@ constexpr int smem_bytes() {
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, int AM, int BMD, int EPI>
 static int launch(cudaStream_t st, const GemmArgs& g, dim3 grid) {
   constexpr int smem = smem_bytes<BM, BN, BK, STAGES, AM, BMD>();
-  auto kern1 = dgemm_kernel<BM, BN, BK, WM, WN, STAGES, MINB, AM, BMD, EPI>;
-  auto kernp = dgemm_kernel_persist<BM, BN, BK, WM, WN, STAGES, MINB, AM, BMD, EPI>;
-  auto kern = g.persist ? kernp : kern1;
+  auto kern = dgemm_kernel<BM, BN, BK, WM, WN, STAGES, MINB, AM, BMD, EPI>;
   static int attr_dev_mask = 0;  // per-instantiation, per-device
   int dev = 0;
   BR_CUDA(cudaGetDevice(&dev));
   if (!(attr_dev_mask & (1 << dev))) {
-    BR_CUDA(cudaFuncSetAttribute(kern1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    BR_CUDA(cudaFuncSetAttribute(kernp, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    BR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_dev_mask |= 1 << dev;
   }
-  if (g_preload_only) {
-    BR_CUDA(launch_pdl(kernp, grid, dim3(WM * WN * 32), smem, st, g));
-    return (int)launch_pdl(kern1, grid, dim3(WM * WN * 32), smem, st, g);
-  }
+  if (g_preload_only) return (int)launch_pdl(kern, grid, dim3(WM * WN * 32), smem, st, g);
   count_launch();
   BR_CUDA(launch_pdl(kern, grid, dim3(WM * WN * 32), smem, st, g));
   return 0;

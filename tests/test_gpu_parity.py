@@ -553,12 +553,11 @@ def test_pipelined_z_matches(tmp_path):
 @pytest.mark.gpu
 @pytest.mark.parametrize("env", [{"BR_LEAF_W": "0"},
                                  {"BR_PANEL_CAP": "16", "BR_PANEL_CAP_ROWS": "0"},
-                                 {"BR_PANEL_CAP": "16", "BR_PANEL_CAP_ROWS": "0", "BR_PANEL_CAP_GRID": "0"},
                                  {"BR_PERSIST_ROWS": "100000"},
                                  {"BR_LEAF2": "0"}])
 def test_tuning_modes_agree(tmp_path, env):
     """The measured-and-kept tuning modes (T^T inside the split-K reduction,
-    capped panel GEMMs, persistent panels, the 1D leaf) reduce to the same
+    split-K shaped by a panel CTA cap, persistent panels, the 1D leaf) reduce to the same
     bands as the default path, to rounding, with depth 1 == depth 0 bitwise."""
     import subprocess
     import sys
