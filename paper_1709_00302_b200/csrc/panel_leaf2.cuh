@@ -16,8 +16,9 @@ __device__ __forceinline__ void st_async_f64(uint32_t raddr, double a, uint32_t 
 // P), with a 2D layout: warp w owns the 8 columns 8*(w % CG) .. +8 (CG = NB/8
 // column groups) of the 256 rows of its row group rg = w / CG, and lane l of
 // it rows rg*256 + 32 r + l (r < 8) of the CTA's block: 8 x 8 doubles per
-// thread, nothing rotates, every index is compile-time inside the unrolled
-// 8-column sweep of a column group.
+// thread. The warps owning the current column rotate their 8 register
+// columns by one per step, so every register index is compile-time in a
+// non-unrolled step loop (see below).
 //
 // Step i (column i lives in column group cg = i / 8, register column ci):
 //   1. the owner warps publish x = column i (rows >= i, zero above) to shared
@@ -26,9 +27,11 @@ __device__ __forceinline__ void st_async_f64(uint32_t raddr, double a, uint32_t 
 //      ||x||^2 and transpose-reduces them (9 + 5 shuffles instead of the 32
 //      slots per warp of the 1D layout); the slot of a finished column is the
 //      Gram entry x^T Y_y, as in leaf_reg_kernel;
-//   3. exchange (several CTAs or row groups): every warp pushes its 8 slot
-//      totals (st.async, completing bytes on the receiver's mbarrier) to every
-//      CTA; with one CTA and one row group the warp already has the totals;
+//   3. exchange (several CTAs or row groups): the row groups of a column
+//      group combine their partials in shared memory, then one warp per
+//      column group pushes its 8 slot totals (st.async, completing bytes on
+//      the receiver's mbarrier) to every CTA; with one CTA and one row group
+//      the warp already has the totals;
 //   4. every warp forms the same scalars from the same data in the same
 //      order: beta = -sign(x0)||x||, alpha_c = P_ic - (x^T P_c)/beta,
 //      v = x / (x0 - beta), and updates its columns.
