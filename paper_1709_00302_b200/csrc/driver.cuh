@@ -127,9 +127,10 @@ int ws_collect_timing(Workspace& ws);  // after a sync: fold events into t_ms
 // Completion points of a panel's leaves: Y columns [c0[s], c1[s]) are final
 // once ev[s] (recorded on the panel's stream) has completed.
 struct LeafMarks {
+  static constexpr int kMax = 256;
   int n = 0;
-  int64_t c0[64], c1[64];
-  cudaEvent_t ev[64];
+  int64_t c0[kMax], c1[kMax];
+  cudaEvent_t ev[kMax];
 };
 int panel_qr(cudaStream_t st, Scratch& sk, DevBuf& pscratch, MatView P, MatView Y, double* tau,
              MatView T, MatView* W, int max_ctas = 0, Workspace* pws = nullptr,

@@ -523,8 +523,8 @@ int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView 
   if (marks) marks->n = 0;
   auto mark = [&](int64_t c0, int64_t c1) -> int {  // Y[:, c0:c1) final on st
     if (!marks || !pws) return 0;
-    if (marks->n >= 64) {
-      set_error("panel_qr: more than 64 leaf marks");
+    if (marks->n >= LeafMarks::kMax) {
+      set_error("panel_qr: more than %d leaf marks", LeafMarks::kMax);
       return -1;
     }
     cudaEvent_t ev = ws_event(*pws);

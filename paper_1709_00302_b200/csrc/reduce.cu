@@ -286,14 +286,16 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
     MatView P(Aat(k, k), lda, i, bp);
     MatView Y(Yu[par], m, i, bp), T(Tu[par], b, bp, bp), W(Wu[par], m, i, bp);
     TimeScope ts(ws, st, TC_PANEL, panel_flops(i, bp), "qr", k);
-    return panel_qr(st, sk, ws.pscratch, P, Y, tauu[par], T, &W, panel_cap(i), &ws, &mk_qr[par]);
+    return panel_qr(st, sk, ws.pscratch, P, Y, tauu[par], T, &W, panel_cap(i), &ws,
+                    pz_rows() > 0 ? &mk_qr[par] : nullptr);
   };
   auto lq = [&](cudaStream_t st, Scratch& sk, int64_t k, int64_t bq) -> int {
     const int64_t jr = n - k - w;
     MatView P(Aat(k, k + w), lda, jr, bq, true);  // transposed view of the bq x jr rows
     MatView Y(Yv, n, jr, bq), T(Tv, b, bq, bq), W(Wv, n, jr, bq);
     TimeScope ts(ws, st, TC_PANEL, panel_flops(jr, bq), "lq", k);
-    return panel_qr(st, sk, ws.pscratch, P, Y, tauv, T, &W, panel_cap(jr), &ws, &mk_lq);
+    return panel_qr(st, sk, ws.pscratch, P, Y, tauv, T, &W, panel_cap(jr), &ws,
+                    pz_rows() > 0 ? &mk_lq : nullptr);
   };
   auto handoff = [&]() -> int {  // main -> panel ordering point
     cudaEvent_t ev = ws_event(ws);
