@@ -246,11 +246,11 @@ def run_ours(args, rank, world, local_rank):
     def one_step(st):
         A.copy_(A0)
         if kind == "sevp":
-            rc = lib.br_reduce_sym_band(h, n, w, b, la, A.data_ptr(), ld, None, 0, st)
+            rc = lib.br_reduce_sym_band(h, n, w, b, la, A.data_ptr(), ld, None, 0, None, st)
         elif kind == "band":
-            rc = lib.br_reduce_band(h, n, n, w, b, 1, la, A.data_ptr(), ld, st)
+            rc = lib.br_reduce_band(h, n, n, w, b, 1, la, A.data_ptr(), ld, None, st)
         else:
-            rc = lib.br_reduce_tri_band(h, n, n, w, b, la, A.data_ptr(), ld, st)
+            rc = lib.br_reduce_tri_band(h, n, n, w, b, la, A.data_ptr(), ld, None, st)
         _lib.check(rc, "reduce")
 
     # the library runs on its own streams: make it follow torch's stream
@@ -309,12 +309,11 @@ def run_ours(args, rank, world, local_rank):
     def host_call():
         if kind == "sevp":
             rc = lib.br_reduce_sym_band_host(h, n, w, b, la, Ah.data_ptr(), n, Bh.data_ptr(), n,
-                                             None, 0, st)
+                                             None, 0, None, st)
         elif kind == "band":
-            rc = lib.br_reduce_band_host(h, n, n, w, b, 1, la, Ah.data_ptr(), n, Bh.data_ptr(), n,
-                                         st)
+            rc = lib.br_reduce_band_host(h, n, n, w, b, 1, la, Ah.data_ptr(), n, Bh.data_ptr(), n, None, st)
         else:
-            rc = lib.br_reduce_tri_band_host(h, n, n, w, b, la, Ah.data_ptr(), n, Bh.data_ptr(), n, st)
+            rc = lib.br_reduce_tri_band_host(h, n, n, w, b, la, Ah.data_ptr(), n, Bh.data_ptr(), n, None, st)
         _lib.check(rc, "reduce_host")
 
     for _ in range(2):  # eager call sizes the staging buffers, the second captures the graph

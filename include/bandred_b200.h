@@ -40,6 +40,41 @@ typedef struct br_stats {
   int64_t launches;     /* kernels launched by the reduction */
 } br_stats;
 
+/* Householder factors of a reduction (extension: the reference keeps them
+ * only in private state, ref sevp.py:106,128-134 state.factors[k] and
+ * svd.py:185,195 fu/fv; SURVEY 8(b) `return_factors` / `factors_out`).
+ * Every panel's compact-WY factors Q_k = I + W_k Y_k^T, W_k = Y_k T_k
+ * (T = -T_larft), are stored packed, panel by panel, like LAPACK's
+ * sytrd_sy2sb / gebrd keep their reflectors below/right of the band:
+ *   left chain (QR panels: SEVP, the SVD's U side), panel at leading column k
+ *   with bp columns and j rows starting at row r0 (SEVP and band form
+ *   r0 = k + w, triangular band r0 = k):
+ *     Y_k  -> yl[r0 + r + (k + c) * ldyl], r < j, c < bp (unit lower
+ *             trapezoidal, explicit zeros above the unit diagonal)
+ *     T_k  -> tl[r + (k + c) * ldtl],       r, c < bp (upper triangular)
+ *     tau  -> taul[k + c]
+ *   right chain (LQ panels, SVD only, ignored for SEVP), panel at leading
+ *   column k with bq reflectors acting on columns k + w .. n:
+ *     Y_k  -> yr[(k + w) + r + (k + c) * ldyr], r < n - k - w, c < bq
+ *     T_k  -> tr[r + (k + c) * ldtr];  tau -> taur[k + c]
+ * Sizes: yl m x n (SEVP n x n), tl b x n, taul n, yr n x n, tr b x n, taur
+ * n. Entries outside the panels are not written. The reduced matrix A then
+ * equals Q_L B Q_R^T with Q_L = Q_0 Q_1 ... (left chain) and Q_R likewise
+ * (SEVP: A = Q B Q^T). Device pointers for the device entry points, host
+ * pointers for the _host ones. Any chain pointer may be NULL (not stored). */
+typedef struct br_factors {
+  double* yl;
+  int64_t ldyl;
+  double* tl;
+  int64_t ldtl;
+  double* taul;
+  double* yr;
+  int64_t ldyr;
+  double* tr;
+  int64_t ldtr;
+  double* taur;
+} br_factors;
+
 /* ---- context ---------------------------------------------------------- */
 int br_version(void);
 const char* br_last_error(void);
@@ -66,6 +101,14 @@ int br_get_timing(br_handle_t h, int cls, double* ms, double* flops, int64_t* la
  * microseconds since the call began. Overlap of the two streams is the
  * look-ahead. br_trace_count returns the record count (-1 for a NULL h). */
 int64_t br_trace_count(br_handle_t h);
+/* Handle options (extension). BR_OPT_MAX_ITERS = k > 0: the reductions stop
+ * after their first k panels and return the raw working matrix (no
+ * finalize / band mask; the panels' own columns below the band hold R/L and
+ * scratch) - a partial reduction used to compare the trailing matrix with
+ * the reference after k iterations at sizes where a full CPU reference run
+ * is too slow; 0 (default) = full reduction. */
+#define BR_OPT_MAX_ITERS 1
+int br_set_option(br_handle_t h, int key, int64_t value);
 int br_trace_get(br_handle_t h, int64_t idx, char* id, int64_t idlen, int* stream, double* t0_us,
                  double* t1_us);
 
@@ -117,6 +160,8 @@ int br_sym_two_sided_update(br_handle_t h, int64_t j, int64_t b, double* A2, int
                             const double* Y, int64_t ldy, const double* W, int64_t ldw);
 
 /* ---- reductions --------------------------------------------------------- */
+/* Every reduction takes `factors` (nullable, see br_factors): when given,
+ * each panel's Y, T and tau are stored there as the panel is factored. */
 /* reduce_sym_band (sevp.py:287-324) on a device matrix, in place. Reads
  * only the lower triangle; on return A holds the finalized band (mirrored,
  * off-band exactly zero). lookahead: 0 = reference schedule, 1 = next panel
@@ -124,13 +169,14 @@ int br_sym_two_sided_update(br_handle_t h, int64_t j, int64_t b, double* A2, int
  * Q (nullable, n x n) receives the accumulated orthogonal factor
  * (accumulate_q, sevp.py:138-144). If n <= w+1 nothing is done. */
 int br_reduce_sym_band(br_handle_t h, int64_t n, int64_t w, int64_t b, int lookahead, double* A,
-                       int64_t lda, double* Q, int64_t ldq, br_stats* stats);
+                       int64_t lda, double* Q, int64_t ldq, const br_factors* factors,
+                       br_stats* stats);
 /* reduce_tri_band (svd.py:179-247) on a device m x n matrix, m >= n, in
  * place: upper triangular-band with bandwidth w, everything else exactly 0.
  * lookahead 1 overlaps the LQ / next QR panels with the rank-b updates
  * (extension: the reference schedule is sequential, results identical). */
 int br_reduce_tri_band(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b, int lookahead,
-                       double* A, int64_t lda, br_stats* stats);
+                       double* A, int64_t lda, const br_factors* factors, br_stats* stats);
 /* Host-buffer variants: copy A (host, lda) to the device, reduce, copy the
  * band back to `band` (host, ldb). Host buffers may be pageable or pinned.
  * Pinned buffers of 64 MiB and more are streamed: finished band column
@@ -140,10 +186,10 @@ int br_reduce_tri_band(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b
  * the staged copies. */
 int br_reduce_sym_band_host(br_handle_t h, int64_t n, int64_t w, int64_t b, int lookahead,
                             const double* A, int64_t lda, double* band, int64_t ldb, double* Q,
-                            int64_t ldq, br_stats* stats);
+                            int64_t ldq, const br_factors* factors, br_stats* stats);
 int br_reduce_tri_band_host(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b,
                             int lookahead, const double* A, int64_t lda, double* band,
-                            int64_t ldb, br_stats* stats);
+                            int64_t ldb, const br_factors* factors, br_stats* stats);
 
 /* Equal-bandwidth band form of the SVD (replaces the band branch of
  * reduce_band_svd, ref pkg/src/bandred/svd.py:515-589, task bodies
@@ -155,10 +201,11 @@ int br_reduce_tri_band_host(br_handle_t h, int64_t m, int64_t n, int64_t w, int6
  * static look-ahead (V1 / V2 schedules, svd.py:394-492): bitwise equal to
  * lookahead 0 with the same `simultaneous`. Needs 1 <= b <= w. */
 int br_reduce_band(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b, int simultaneous,
-                   int lookahead, double* A, int64_t lda, br_stats* stats);
+                   int lookahead, double* A, int64_t lda, const br_factors* factors,
+                   br_stats* stats);
 int br_reduce_band_host(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b,
                         int simultaneous, int lookahead, const double* A, int64_t lda,
-                        double* band, int64_t ldb, br_stats* stats);
+                        double* band, int64_t ldb, const br_factors* factors, br_stats* stats);
 
 #ifdef __cplusplus
 }

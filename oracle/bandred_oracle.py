@@ -15,6 +15,8 @@ from __future__ import annotations
 
 import numpy as np
 
+_BLK = 1024  # column block of the blocked SYMM / SYR2K restatements
+
 __all__ = [
     "house_gen",
     "qr_panel",
@@ -172,23 +174,33 @@ def apply_wy_left(A, Y, W):
     """A := A + Y (W^T A), in place (kernels.py:258-284)."""
     if A.shape[0] == 0 or A.shape[1] == 0:
         return A
-    A += Y @ (W.T @ A)
-    return A
+    Z = W.T @ A
+    A += (Z.T @ Y.T).T  # the product formed F-ordered, like A (a C-ordered
+    return A             # temporary makes the in-place add stride-bound)
 
 
 def apply_wy_right(A, Y, W):
     """A := A + (A W) Y^T, in place (kernels.py:287-309)."""
     if A.shape[0] == 0 or A.shape[1] == 0:
         return A
-    A += (A @ W) @ Y.T
+    AW = A @ W
+    A += (Y @ AW.T).T
     return A
 
 
 def symm_lower(A2, W):
     """sym(A2) W reading only A2's lower triangle (kernels.py:312-341)."""
-    L = np.tril(A2)
-    S = L + np.tril(A2, -1).T
-    return np.asfortranarray(S @ W)
+    j = A2.shape[0]
+    X1 = np.zeros((j, W.shape[1]), order="F")
+    for a in range(0, j, _BLK):  # column blocks: only lower-stored entries are read
+        e = min(j, a + _BLK)
+        D = np.tril(A2[a:e, a:e])
+        X1[a:e] += D @ W[a:e] + np.tril(D, -1).T @ W[a:e]
+        if e < j:
+            S = A2[e:, a:e]  # strictly below the diagonal block
+            X1[e:] += S @ W[a:e]
+            X1[a:e] += S.T @ W[e:]
+    return X1
 
 
 def syr2k_lower(A2, X3, Y, c0, c1):
@@ -199,12 +211,13 @@ def syr2k_lower(A2, X3, Y, c0, c1):
         raise ValueError("syr2k_lower bad column range")
     if c0 == c1:
         return A2
-    upd = X3[c0:, :] @ Y[c0:c1, :].T + Y[c0:, :] @ X3[c0:c1, :].T  # rows c0.. x cols c0..c1
-    r = np.arange(c0, j)[:, None]
-    c = np.arange(c0, c1)[None, :]
-    mask = r >= c
-    blk = A2[c0:, c0:c1]
-    blk[mask] += upd[mask]
+    for a in range(c0, c1, _BLK):  # column blocks; lower part of each only
+        e = min(c1, a + _BLK)
+        # rows a.. x cols a..e, formed F-ordered: (Y_b X3^T + X3_b Y^T)^T
+        upd = (Y[a:e] @ X3[a:].T + X3[a:e] @ Y[a:].T).T
+        d = np.tril(np.ones((e - a, e - a), dtype=bool))
+        A2[a:e, a:e][d] += upd[: e - a][d]
+        A2[e:, a:e] += upd[e - a :]
     return A2
 
 
@@ -250,31 +263,36 @@ def tri_schedule(m, n, b):
 
 def finalize_sym(A, n, w):
     """Mirror lower -> upper and zero off-band exactly (sevp.py:276-284)."""
-    i = np.arange(n)[:, None]
-    jj = np.arange(n)[None, :]
-    low = np.tril(A)
-    low[(i - jj) > w] = 0.0
-    out = low + low.T
-    out[i == jj] = np.diag(low)
-    return np.asfortranarray(out)
+    out = np.zeros((n, n), order="F")
+    for c in range(n):  # lower in-band entries kept, upper ones mirrored
+        lo = A[c : min(n, c + w + 1), c]
+        out[c : c + lo.size, c] = lo
+        out[c, c + 1 : c + lo.size] = lo[1:]
+    return out
 
 
 def mask_tri_band(A, w):
     """Zero i > j and j > i + w exactly (svd.py:237-239)."""
     m, n = A.shape
-    i = np.arange(m)[:, None]
-    jj = np.arange(n)[None, :]
-    A[(i > jj) | (jj > i + w)] = 0.0
+    for c in range(n):  # column by column (no m x n index masks)
+        A[c + 1 :, c] = 0.0
+        if c - w > 0:
+            A[: c - w, c] = 0.0
     return A
 
 
-def reduce_sym_band(A, n, w, b, inner_b=16, accumulate_q=False, max_iters=None):
+def reduce_sym_band(A, n, w, b, inner_b=16, accumulate_q=False, max_iters=None, finalize=True,
+                    factors=None):
     """Dense symmetric -> symmetric band, Reference schedule.
 
     Restates reduce_sym_band (sevp.py:287-324) with _run_reference
     (sevp.py:194-206) and the task bodies sevp.py:128-188. Reads only the
     lower triangle. Returns (band, q, iterations); n <= w+1 returns the
-    copied input unchanged (sevp.py:302-305).
+    copied input unchanged (sevp.py:302-305). Test hooks: `max_iters` stops
+    after that many panels, `finalize=False` returns the raw working matrix
+    (the partial-reduction comparison of BR_OPT_MAX_ITERS), `factors` (a
+    dict) receives k -> (Y, T, tau) of every panel (state.factors[k],
+    sevp.py:128-134).
     """
     if not (1 <= b <= w) or n < 1:
         raise ValueError("need n >= 1, 1 <= b <= w")
@@ -291,6 +309,8 @@ def reduce_sym_band(A, n, w, b, inner_b=16, accumulate_q=False, max_iters=None):
         bp = min(b, n - k - w)
         j = n - k - w
         Y, T, W, R, tau = qr_panel(A[k + w : n, k : k + bp], inner_b)
+        if factors is not None:
+            factors[k] = (Y, T, tau)
         if Q is not None:
             apply_wy_right(Q[:, k + w : n], Y, W)
         if bp < w:
@@ -300,14 +320,18 @@ def reduce_sym_band(A, n, w, b, inner_b=16, accumulate_q=False, max_iters=None):
         X2 = 0.5 * (X1.T @ W)
         X3 = X1 + Y @ X2
         syr2k_lower(A2, X3, Y, 0, j)
+    if not finalize:
+        return A, Q, len(ks)
     return finalize_sym(A, n, w), Q, len(ks)
 
 
-def reduce_tri_band(A, w, b, inner_b=16, max_iters=None):
+def reduce_tri_band(A, w, b, inner_b=16, max_iters=None, finalize=True, factors=None):
     """Dense general -> upper triangular-band (svd.py:179-247).
 
     Returns (band, lower_bw, upper_bw, iterations); m < n reduces A^T and
-    transposes back (svd.py:221-232).
+    transposes back (svd.py:221-232). Test hooks as in reduce_sym_band;
+    `factors` receives ("qr", k) / ("lq", k) -> (Y, T, tau) (fu / fv,
+    svd.py:185,195).
     """
     if w < 1 or not (1 <= b <= w):
         raise ValueError("need w >= 1, 1 <= b <= w")
@@ -323,14 +347,20 @@ def reduce_tri_band(A, w, b, inner_b=16, max_iters=None):
     if max_iters is not None:  # bounded CPU-baseline sample (bench.py)
         sched = sched[:max_iters]
     for k, bp in sched:
-        Yu, Tu, Wu, _, _ = qr_panel(A[k:m, k : k + bp], inner_b)
+        Yu, Tu, Wu, _, tu = qr_panel(A[k:m, k : k + bp], inner_b)
+        if factors is not None:
+            factors[("qr", k)] = (Yu, Tu, tu)
         apply_wy_left(A[k:m, k + bp : n], Yu, Wu)
         jr = n - k - w
         if jr >= 1:
             bq = min(bp, jr)
-            Yv, Tv, Wv, _, _ = lq_panel(A[k : k + bq, k + w : n], inner_b)
+            Yv, Tv, Wv, _, tv = lq_panel(A[k : k + bq, k + w : n], inner_b)
+            if factors is not None:
+                factors[("lq", k)] = (Yv, Tv, tv)
             apply_wy_right(A[k + bq : m, k + w : n], Yv, Wv)
         it += 1
+    if not finalize:
+        return A, 0, w, it
     return mask_tri_band(A, w), 0, w, it
 
 

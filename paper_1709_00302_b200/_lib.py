@@ -26,6 +26,18 @@ class BrStats(C.Structure):
     ]
 
 
+class BrFactors(C.Structure):
+    """br_factors (include/bandred_b200.h): packed per-panel Y / T / tau."""
+    _fields_ = [
+        ("yl", C.c_void_p), ("ldyl", C.c_int64), ("tl", C.c_void_p), ("ldtl", C.c_int64),
+        ("taul", C.c_void_p),
+        ("yr", C.c_void_p), ("ldyr", C.c_int64), ("tr", C.c_void_p), ("ldtr", C.c_int64),
+        ("taur", C.c_void_p),
+    ]
+
+
+BR_OPT_MAX_ITERS = 1
+
 # name -> (restype, argtypes); mirrors include/bandred_b200.h exactly
 SIGNATURES = {
     "br_version": (C.c_int, []),
@@ -53,21 +65,22 @@ SIGNATURES = {
     "br_symm_lower": (C.c_int, [C.c_void_p, i64, i64, dptr, i64, dptr, i64, dptr, i64]),
     "br_syr2k_lower": (C.c_int, [C.c_void_p, i64, i64, dptr, i64, dptr, i64, dptr, i64, i64, i64]),
     "br_sym_two_sided_update": (C.c_int, [C.c_void_p, i64, i64, dptr, i64, dptr, i64, dptr, i64]),
+    "br_set_option": (C.c_int, [C.c_void_p, C.c_int, i64]),
     "br_reduce_sym_band": (C.c_int, [C.c_void_p, i64, i64, i64, C.c_int, dptr, i64, dptr, i64,
-                                     C.POINTER(BrStats)]),
+                                     C.POINTER(BrFactors), C.POINTER(BrStats)]),
     "br_reduce_tri_band": (C.c_int, [C.c_void_p, i64, i64, i64, i64, C.c_int, dptr, i64,
-                                     C.POINTER(BrStats)]),
+                                     C.POINTER(BrFactors), C.POINTER(BrStats)]),
     "br_reduce_sym_band_host": (C.c_int, [C.c_void_p, i64, i64, i64, C.c_int, dptr, i64, dptr, i64,
-                                          dptr, i64, C.POINTER(BrStats)]),
+                                          dptr, i64, C.POINTER(BrFactors), C.POINTER(BrStats)]),
     "br_reduce_tri_band_host": (C.c_int, [C.c_void_p, i64, i64, i64, i64, C.c_int, dptr, i64, dptr,
-                                          i64, C.POINTER(BrStats)]),
+                                          i64, C.POINTER(BrFactors), C.POINTER(BrStats)]),
     "br_trace_count": (i64, [C.c_void_p]),
     "br_trace_get": (C.c_int, [C.c_void_p, i64, C.c_char_p, i64, C.POINTER(C.c_int),
                                C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "br_reduce_band": (C.c_int, [C.c_void_p, i64, i64, i64, i64, C.c_int, C.c_int, dptr, i64,
-                                 C.POINTER(BrStats)]),
+                                 C.POINTER(BrFactors), C.POINTER(BrStats)]),
     "br_reduce_band_host": (C.c_int, [C.c_void_p, i64, i64, i64, i64, C.c_int, C.c_int, dptr, i64,
-                                      dptr, i64, C.POINTER(BrStats)]),
+                                      dptr, i64, C.POINTER(BrFactors), C.POINTER(BrStats)]),
 }
 
 _lib = None

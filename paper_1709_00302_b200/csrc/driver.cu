@@ -222,6 +222,37 @@ int band_out_flush(Workspace& ws, BandOut* bo, int64_t upto) {
   bo->done = upto;
   return 0;
 }
+int store_factors(Workspace& ws, cudaStream_t st, int chain, int64_t k, int64_t r0, int64_t j,
+                  int64_t bp, const double* Y, int64_t ldy, const double* T, int64_t ldt,
+                  const double* tau) {
+  const br_factors* f = ws.fo;
+  if (!f || j <= 0 || bp <= 0) return 0;
+  double* y = chain ? f->yr : f->yl;
+  double* t = chain ? f->tr : f->tl;
+  double* ta = chain ? f->taur : f->taul;
+  const int64_t ldyo = chain ? f->ldyr : f->ldyl, ldto = chain ? f->ldtr : f->ldtl;
+  const size_t D = sizeof(double);
+  if (y)
+    BR_CUDA(cudaMemcpy2DAsync(y + r0 + k * ldyo, ldyo * D, Y, ldy * D, j * D, bp,
+                              cudaMemcpyDeviceToDevice, st));
+  if (t)
+    BR_CUDA(cudaMemcpy2DAsync(t + k * ldto, ldto * D, T, ldt * D, bp * D, bp,
+                              cudaMemcpyDeviceToDevice, st));
+  if (ta) BR_CUDA(cudaMemcpyAsync(ta + k, tau, bp * D, cudaMemcpyDeviceToDevice, st));
+  return 0;
+}
+
+int band_out_raw(Workspace& ws, BandOut* bo, int64_t cols) {
+  if (!bo) return 0;
+  cudaEvent_t ev = ws_event(ws);
+  BR_CUDA(cudaEventRecord(ev, ws.main));
+  BR_CUDA(cudaStreamWaitEvent(bo->st, ev, 0));
+  BR_CUDA(cudaMemcpy2DAsync(bo->host, bo->ldh * sizeof(double), bo->A, bo->lda * sizeof(double),
+                            bo->rows * sizeof(double), cols, cudaMemcpyDeviceToHost, bo->st));
+  bo->done = cols;
+  return 0;
+}
+
 int zero_fill(cudaStream_t st, MatView V) {
   if (V.rows <= 0 || V.cols <= 0) return 0;
   const int64_t r = V.trans ? V.cols : V.rows, c = V.trans ? V.rows : V.cols;
@@ -265,6 +296,8 @@ int timed_reduction(Workspace& ws, br_stats* stats, double nominal, Workspace::G
     return 1000 + (int)e;
   };
   key.gen = alloc_generation();
+  key.max_iters = ws.max_iters;
+  if (ws.fo) key.fo = *ws.fo;
   key.main = ws.main;
   key.panel = ws.panel;
   key.timing = ws.timing;
@@ -385,6 +418,10 @@ struct br_handle_s {
 // Stream (and its split-K scratch) used by kernel-level calls: br_stream_select.
 static cudaStream_t cur_stream(Workspace& ws) { return ws.active ? ws.panel : ws.main; }
 static Scratch& cur_sk(Workspace& ws) { return ws.active ? ws.sk_panel : ws.sk_main; }
+// Temporaries and panel scratch of kernel-level calls are per stream too, so
+// calls issued concurrently on the two streams never share a buffer.
+static DevBuf& cur_tmp(Workspace& ws) { return ws.active ? ws.tmp_panel : ws.tmp; }
+static DevBuf& cur_pscr(Workspace& ws) { return ws.active ? ws.pscratch_panel : ws.pscratch; }
 
 #define ARG(cond, i)                                   \
   do {                                                 \
@@ -405,7 +442,7 @@ static int ensure_scratch(Workspace& ws, int64_t main_doubles, int64_t panel_dou
   BR_CHECK(devbuf_reserve(ws.skbuf_main, both));
   BR_CHECK(devbuf_reserve(ws.skbuf_panel, both));
   BR_CHECK(devbuf_reserve(ws.skbuf_aux, both));
-  BR_CHECK(devbuf_reserve(ws.pscratch, pscr));
+  BR_CHECK(devbuf_reserve(cur_pscr(ws), pscr));
   ws.sk_main.p = ws.skbuf_main.p;
   ws.sk_main.cap = ws.skbuf_main.cap;
   ws.sk_panel.p = ws.skbuf_panel.p;
@@ -478,8 +515,11 @@ int br_destroy(br_handle_t h) {
   devbuf_free(ws.pscratch);
   devbuf_free(ws.factors);
   devbuf_free(ws.tmp);
+  devbuf_free(ws.tmp_panel);
+  devbuf_free(ws.pscratch_panel);
   devbuf_free(ws.stageA);
   devbuf_free(ws.stageQ);
+  devbuf_free(ws.stageF);
   devbuf_free(ws.skbuf_aux);
   if (ws.flags) cudaFree(ws.flags);
   if (ws.ev_aux0) cudaEventDestroy(ws.ev_aux0);
@@ -564,7 +604,7 @@ static int qr_common(br_handle_t h, MatView P, double* Y, int64_t ldy, double* T
   BR_CHECK(ensure_scratch(ws, 4 * std::max<int64_t>(j, 1) * b + (1 << 20), (1 << 20) + 4 * j * b,
                           panel_scratch_doubles(b)));
   MatView Yv(Y, ldy, j, b), Tv(T, ldt, b, b), Wv(W, ldw, j, b);
-  return panel_qr(cur_stream(ws), cur_sk(ws), ws.pscratch, P, Yv, tau, Tv, W ? &Wv : nullptr, 0,
+  return panel_qr(cur_stream(ws), cur_sk(ws), cur_pscr(ws), P, Yv, tau, Tv, W ? &Wv : nullptr, 0,
                   &ws);
 }
 
@@ -626,8 +666,9 @@ int br_apply_wy_left(br_handle_t h, int64_t rows, int64_t cols, double* A, int64
   Workspace& ws = h->ws;
   BR_CHECK(ensure_scratch(ws, 4 * std::max(rows, cols) * b + (1 << 20), 1 << 20,
                           panel_scratch_doubles(1)));
-  BR_CHECK(devbuf_reserve(ws.tmp, b * cols));
-  MatView Z(ws.tmp.p, b, b, cols), Av(A, lda, rows, cols);
+  DevBuf& tmp = cur_tmp(ws);
+  BR_CHECK(devbuf_reserve(tmp, b * cols));
+  MatView Z(tmp.p, b, b, cols), Av(A, lda, rows, cols);
   BR_CHECK(gemm(cur_stream(ws), cur_sk(ws), Z, MatView((double*)W, ldw, rows, b).T(), Av, 1.0, 0.0));
   return gemm(cur_stream(ws), cur_sk(ws), Av, MatView((double*)Y, ldy, rows, b), Z, 1.0, 1.0);
 }
@@ -646,8 +687,9 @@ int br_apply_wy_right(br_handle_t h, int64_t rows, int64_t cols, double* A, int6
   Workspace& ws = h->ws;
   BR_CHECK(ensure_scratch(ws, 4 * std::max(rows, cols) * b + (1 << 20), 1 << 20,
                           panel_scratch_doubles(1)));
-  BR_CHECK(devbuf_reserve(ws.tmp, rows * b));
-  MatView Z(ws.tmp.p, rows, rows, b), Av(A, lda, rows, cols);
+  DevBuf& tmp = cur_tmp(ws);
+  BR_CHECK(devbuf_reserve(tmp, rows * b));
+  MatView Z(tmp.p, rows, rows, b), Av(A, lda, rows, cols);
   BR_CHECK(gemm(cur_stream(ws), cur_sk(ws), Z, Av, MatView((double*)W, ldw, cols, b), 1.0, 0.0));
   return gemm(cur_stream(ws), cur_sk(ws), Av, Z, MatView((double*)Y, ldy, cols, b).T(), 1.0, 1.0);
 }
@@ -720,8 +762,11 @@ int br_gemm(br_handle_t h, int transa, int transb, int64_t m, int64_t n, int64_t
   DEV(h);
   if (m == 0 || n == 0) return 0;
   Workspace& ws = h->ws;
-  BR_CHECK(ensure_scratch(ws, 4 * std::max(m, n) * std::max<int64_t>(std::min(m, n), 1) + (1 << 20),
-                          1 << 20, panel_scratch_doubles(1)));
+  // split-K partials: S * m * n doubles for S splits; pick_kps only splits
+  // products whose partials fit, so a large C is simply not split (the
+  // budget stays <= 4 m n and <= 64 Mi doubles instead of growing with C)
+  BR_CHECK(ensure_scratch(ws, std::min<int64_t>(4 * m * n, (int64_t)1 << 26) + (1 << 20), 1 << 20,
+                          panel_scratch_doubles(1)));
   MatView Av = transa ? MatView((double*)A, lda, k, m).T() : MatView((double*)A, lda, m, k);
   MatView Bv = transb ? MatView((double*)B, ldb, n, k).T() : MatView((double*)B, ldb, k, n);
   return gemm(cur_stream(ws), cur_sk(ws), MatView(C, ldc, m, n), Av, Bv, alpha, beta);
@@ -756,8 +801,9 @@ int br_sym_two_sided_update(br_handle_t h, int64_t j, int64_t b, double* A2, int
   if (j == 0 || b == 0) return 0;
   Workspace& ws = h->ws;
   BR_CHECK(ensure_scratch(ws, 4 * j * b + (1 << 20), 1 << 20, panel_scratch_doubles(1)));
-  BR_CHECK(devbuf_reserve(ws.tmp, 2 * j * b + b * b));
-  MatView X1(ws.tmp.p, j, j, b), X3(ws.tmp.p + j * b, j, j, b), X2(ws.tmp.p + 2 * j * b, b, b, b);
+  DevBuf& tmp = cur_tmp(ws);
+  BR_CHECK(devbuf_reserve(tmp, 2 * j * b + b * b));
+  MatView X1(tmp.p, j, j, b), X3(tmp.p + j * b, j, j, b), X2(tmp.p + 2 * j * b, b, b, b);
   MatView A2v(A2, lda, j, j), Yv((double*)Y, ldy, j, b), Wv((double*)W, ldw, j, b);
   BR_CHECK(symm_lower(cur_stream(ws), cur_sk(ws), X1, A2v, Wv));
   BR_CHECK(gemm(cur_stream(ws), cur_sk(ws), X2, X1.T(), Wv, 0.5, 0.0));
@@ -770,8 +816,37 @@ static double svd_nominal(int64_t m, int64_t n) {
   return 4.0 * ((double)m * n * n - (double)n * n * n / 3.0);
 }
 
+// Factor output checks: leading dimensions cover the packed layout.
+static bool factors_ok(const br_factors* f, int64_t m, int64_t n, int64_t b, bool right) {
+  if (!f) return true;
+  if (f->yl && f->ldyl < std::max<int64_t>(m, 1)) return false;
+  if (f->tl && f->ldtl < b) return false;
+  if (right && f->yr && f->ldyr < std::max<int64_t>(n, 1)) return false;
+  if (right && f->tr && f->ldtr < b) return false;
+  return true;
+}
+
+// Sets the handle's per-call state (factor output) for the duration of one
+// reduction call.
+struct CallState {
+  Workspace& ws;
+  CallState(Workspace& w, const br_factors* f) : ws(w) {
+    ws.fo = (f && (f->yl || f->tl || f->taul || f->yr || f->tr || f->taur)) ? f : nullptr;
+  }
+  ~CallState() { ws.fo = nullptr; }
+};
+
+int br_set_option(br_handle_t h, int key, int64_t value) {
+  ARG(h != nullptr, 1);
+  ARG(key == BR_OPT_MAX_ITERS, 2);
+  ARG(value >= 0, 3);
+  h->ws.max_iters = value;
+  return 0;
+}
+
 int br_reduce_sym_band(br_handle_t h, int64_t n, int64_t w, int64_t b, int lookahead, double* A,
-                       int64_t lda, double* Q, int64_t ldq, br_stats* stats) {
+                       int64_t lda, double* Q, int64_t ldq, const br_factors* factors,
+                       br_stats* stats) {
   ARG(h != nullptr, 1);
   ARG(n >= 1, 2);
   ARG(w >= 1, 3);
@@ -779,7 +854,9 @@ int br_reduce_sym_band(br_handle_t h, int64_t n, int64_t w, int64_t b, int looka
   ARG(lookahead == 0 || lookahead == 1, 5);
   ARG(A != nullptr && lda >= n, 6);
   ARG(Q == nullptr || ldq >= n, 9);
+  ARG(factors_ok(factors, n, n, b, false), 10);
   DEV(h);
+  CallState cs(h->ws, factors);
   Workspace::GraphKey key;
   key.kind = 0;
   key.n = n;
@@ -798,7 +875,7 @@ int br_reduce_sym_band(br_handle_t h, int64_t n, int64_t w, int64_t b, int looka
 }
 
 int br_reduce_tri_band(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b, int lookahead,
-                       double* A, int64_t lda, br_stats* stats) {
+                       double* A, int64_t lda, const br_factors* factors, br_stats* stats) {
   ARG(h != nullptr, 1);
   ARG(m >= 1 && m >= n, 2);
   ARG(n >= 1, 3);
@@ -806,7 +883,9 @@ int br_reduce_tri_band(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b
   ARG(b >= 1 && b <= w, 5);
   ARG(lookahead == 0 || lookahead == 1, 6);
   ARG(A != nullptr && lda >= m, 7);
+  ARG(factors_ok(factors, m, n, b, true), 9);
   DEV(h);
+  CallState cs(h->ws, factors);
   Workspace::GraphKey key;
   key.kind = 1;
   key.m = m;
@@ -824,7 +903,8 @@ int br_reduce_tri_band(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b
 }
 
 int br_reduce_band(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b, int simultaneous,
-                   int lookahead, double* A, int64_t lda, br_stats* stats) {
+                   int lookahead, double* A, int64_t lda, const br_factors* factors,
+                   br_stats* stats) {
   ARG(h != nullptr, 1);
   ARG(m >= 1 && m >= n, 2);
   ARG(n >= 1, 3);
@@ -833,7 +913,9 @@ int br_reduce_band(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b, in
   ARG(simultaneous == 0 || simultaneous == 1, 6);
   ARG(lookahead == 0 || lookahead == 1, 7);
   ARG(A != nullptr && lda >= m, 8);
+  ARG(factors_ok(factors, m, n, b, true), 10);
   DEV(h);
+  CallState cs(h->ws, factors);
   Workspace::GraphKey key;
   key.kind = 2;
   key.m = m;
@@ -881,6 +963,59 @@ static bool setup_band_out(Workspace& ws, BandOut& bo, double* band, int64_t ldb
   return true;
 }
 
+// Host factor output: device staging buffers (zeroed; the packed layout with
+// leading dimensions m / b / n) and the copy back into the caller's arrays.
+struct FactorStage {
+  br_factors dev{};
+  const br_factors* host = nullptr;
+  int64_t m = 0, n = 0, b = 0;
+};
+static int factors_stage(Workspace& ws, const br_factors* hf, int64_t m, int64_t n, int64_t b,
+                         bool right, FactorStage& fs) {
+  fs.host = nullptr;
+  if (!hf || !(hf->yl || hf->tl || hf->taul || (right && (hf->yr || hf->tr || hf->taur))))
+    return 0;
+  fs.host = hf;
+  fs.m = m;
+  fs.n = n;
+  fs.b = b;
+  const int64_t need = m * n + b * n + n + (right ? n * n + b * n + n : 0);
+  BR_CHECK(devbuf_reserve(ws.stageF, need));
+  BR_CUDA(cudaMemsetAsync(ws.stageF.p, 0, need * sizeof(double), ws.main));
+  double* p = ws.stageF.p;
+  br_factors& d = fs.dev;
+  d.yl = hf->yl ? p : nullptr, d.ldyl = m;
+  p += m * n;
+  d.tl = hf->tl ? p : nullptr, d.ldtl = b;
+  p += b * n;
+  d.taul = hf->taul ? p : nullptr;
+  p += n;
+  if (right) {
+    d.yr = hf->yr ? p : nullptr, d.ldyr = n;
+    p += n * n;
+    d.tr = hf->tr ? p : nullptr, d.ldtr = b;
+    p += b * n;
+    d.taur = hf->taur ? p : nullptr;
+  }
+  return 0;
+}
+static int factors_unstage(Workspace& ws, const FactorStage& fs) {
+  if (!fs.host) return 0;
+  const br_factors &h = *fs.host, &d = fs.dev;
+  const size_t D = sizeof(double);
+  auto mat = [&](double* dst, int64_t ldd, const double* src, int64_t lds, int64_t r, int64_t c) {
+    if (!dst || !src) return cudaSuccess;
+    return cudaMemcpy2DAsync(dst, ldd * D, src, lds * D, r * D, c, cudaMemcpyDeviceToHost, ws.main);
+  };
+  BR_CUDA(mat(h.yl, h.ldyl, d.yl, d.ldyl, fs.m, fs.n));
+  BR_CUDA(mat(h.tl, h.ldtl, d.tl, d.ldtl, fs.b, fs.n));
+  BR_CUDA(mat(h.taul, 1, d.taul, 1, 1, fs.n));
+  BR_CUDA(mat(h.yr, h.ldyr, d.yr, d.ldyr, fs.n, fs.n));
+  BR_CUDA(mat(h.tr, h.ldtr, d.tr, d.ldtr, fs.b, fs.n));
+  BR_CUDA(mat(h.taur, 1, d.taur, 1, 1, fs.n));
+  return 0;
+}
+
 static int host_stage_in(Workspace& ws, int64_t m, int64_t n, const double* A, int64_t lda,
                          DevBuf& dev, int64_t& ldd) {
   ldd = (m + 31) / 32 * 32;
@@ -892,13 +1027,18 @@ static int host_stage_in(Workspace& ws, int64_t m, int64_t n, const double* A, i
 
 int br_reduce_sym_band_host(br_handle_t h, int64_t n, int64_t w, int64_t b, int lookahead,
                             const double* A, int64_t lda, double* band, int64_t ldb, double* Q,
-                            int64_t ldq, br_stats* stats) {
+                            int64_t ldq, const br_factors* factors, br_stats* stats) {
   ARG(h != nullptr, 1);
   ARG(n >= 1, 2);
+  ARG(w >= 1, 3);
+  ARG(b >= 1 && b <= w, 4);
   ARG(A != nullptr && lda >= n, 6);
   ARG(band != nullptr && ldb >= n, 8);
   ARG(Q == nullptr || ldq >= n, 11);
+  ARG(factors_ok(factors, n, n, b, false), 12);
   DEV(h);
+  FactorStage fs;
+  BR_CHECK(factors_stage(h->ws, factors, n, n, b, false, fs));
   Workspace& ws = h->ws;
   DevBuf& dA = ws.stageA;
   DevBuf& dQ = ws.stageQ;
@@ -913,10 +1053,12 @@ int br_reduce_sym_band_host(br_handle_t h, int64_t n, int64_t w, int64_t b, int 
   bo.sym = true;
   bo.w = w;
   const bool streamed = setup_band_out(ws, bo, band, ldb, dA.p, ldd, n, n);
-  const int rc = br_reduce_sym_band(h, n, w, b, lookahead, dA.p, ldd, qd, ldd, stats);
+  const int rc = br_reduce_sym_band(h, n, w, b, lookahead, dA.p, ldd, qd, ldd,
+                                    fs.host ? &fs.dev : nullptr, stats);
   ws.band_out = nullptr;
   if (streamed) BR_CUDA(cudaStreamSynchronize(ws.copy));
   BR_CHECK(rc);
+  BR_CHECK(factors_unstage(ws, fs));
   if (!streamed)
     BR_CUDA(cudaMemcpy2DAsync(band, ldb * sizeof(double), dA.p, ldd * sizeof(double),
                               n * sizeof(double), n, cudaMemcpyDeviceToHost, ws.main));
@@ -929,13 +1071,18 @@ int br_reduce_sym_band_host(br_handle_t h, int64_t n, int64_t w, int64_t b, int 
 
 int br_reduce_tri_band_host(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b,
                             int lookahead, const double* A, int64_t lda, double* band,
-                            int64_t ldb, br_stats* stats) {
+                            int64_t ldb, const br_factors* factors, br_stats* stats) {
   ARG(h != nullptr, 1);
   ARG(m >= 1 && m >= n, 2);
   ARG(n >= 1, 3);
+  ARG(w >= 1, 4);
+  ARG(b >= 1 && b <= w, 5);
   ARG(A != nullptr && lda >= m, 7);
   ARG(band != nullptr && ldb >= m, 9);
+  ARG(factors_ok(factors, m, n, b, true), 10);
   DEV(h);
+  FactorStage fs;
+  BR_CHECK(factors_stage(h->ws, factors, m, n, b, true, fs));
   Workspace& ws = h->ws;
   DevBuf& dA = ws.stageA;
   int64_t ldd = 0;
@@ -970,12 +1117,14 @@ int br_reduce_tri_band_host(br_handle_t h, int64_t m, int64_t n, int64_t w, int6
   bo.lo = 0;
   bo.up = w;
   const bool streamed = setup_band_out(ws, bo, band, ldb, dA.p, ldd, m, n);
-  const int rc = br_reduce_tri_band(h, m, n, w, b, lookahead, dA.p, ldd, stats);
+  const int rc = br_reduce_tri_band(h, m, n, w, b, lookahead, dA.p, ldd,
+                                    fs.host ? &fs.dev : nullptr, stats);
   ws.band_out = nullptr;
   ws.band_in = nullptr;
   if (stream_in) BR_CUDA(cudaStreamSynchronize(ws.copy_in));
   if (streamed) BR_CUDA(cudaStreamSynchronize(ws.copy));
   BR_CHECK(rc);
+  BR_CHECK(factors_unstage(ws, fs));
   if (!streamed)
     BR_CUDA(cudaMemcpy2DAsync(band, ldb * sizeof(double), dA.p, ldd * sizeof(double),
                               m * sizeof(double), n, cudaMemcpyDeviceToHost, ws.main));
@@ -985,13 +1134,18 @@ int br_reduce_tri_band_host(br_handle_t h, int64_t m, int64_t n, int64_t w, int6
 
 int br_reduce_band_host(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b,
                         int simultaneous, int lookahead, const double* A, int64_t lda,
-                        double* band, int64_t ldb, br_stats* stats) {
+                        double* band, int64_t ldb, const br_factors* factors, br_stats* stats) {
   ARG(h != nullptr, 1);
   ARG(m >= 1 && m >= n, 2);
   ARG(n >= 1, 3);
+  ARG(w >= 1, 4);
+  ARG(b >= 1 && b <= w, 5);
   ARG(A != nullptr && lda >= m, 8);
   ARG(band != nullptr && ldb >= m, 10);
+  ARG(factors_ok(factors, m, n, b, true), 11);
   DEV(h);
+  FactorStage fs;
+  BR_CHECK(factors_stage(h->ws, factors, m, n, b, true, fs));
   Workspace& ws = h->ws;
   DevBuf& dA = ws.stageA;
   int64_t ldd = 0;
@@ -1000,10 +1154,12 @@ int br_reduce_band_host(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t 
   bo.lo = w;
   bo.up = w;
   const bool streamed = setup_band_out(ws, bo, band, ldb, dA.p, ldd, m, n);
-  const int rc = br_reduce_band(h, m, n, w, b, simultaneous, lookahead, dA.p, ldd, stats);
+  const int rc = br_reduce_band(h, m, n, w, b, simultaneous, lookahead, dA.p, ldd,
+                                fs.host ? &fs.dev : nullptr, stats);
   ws.band_out = nullptr;
   if (streamed) BR_CUDA(cudaStreamSynchronize(ws.copy));
   BR_CHECK(rc);
+  BR_CHECK(factors_unstage(ws, fs));
   if (!streamed)
     BR_CUDA(cudaMemcpy2DAsync(band, ldb * sizeof(double), dA.p, ldd * sizeof(double),
                               m * sizeof(double), n, cudaMemcpyDeviceToHost, ws.main));

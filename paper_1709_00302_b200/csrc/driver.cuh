@@ -2,6 +2,7 @@
 #pragma once
 #include <vector>
 
+#include "../../include/bandred_b200.h"
 #include "common.cuh"
 #include "gemm.cuh"
 
@@ -29,10 +30,12 @@ struct Workspace {
   cudaStream_t own_main = nullptr, own_panel = nullptr;
   Scratch sk_main, sk_panel;  // split-K partials, one per stream
   DevBuf skbuf_main, skbuf_panel;
-  DevBuf pscratch;  // panel_qr internal scratch (panel stream)
+  DevBuf pscratch;  // panel_qr internal scratch (reductions; kernel-level calls on main)
+  DevBuf pscratch_panel;  // panel_qr scratch of kernel-level calls on the panel stream
   DevBuf factors;   // reduction buffers
-  DevBuf tmp;       // kernel-level API temporaries
+  DevBuf tmp, tmp_panel;  // kernel-level API temporaries, one per stream
   DevBuf stageA, stageQ;  // host-buffer entry points
+  DevBuf stageF;          // host-buffer entry points: device copy of the factor output
   // auxiliary stream of the persistent panel: the block updates between
   // leaves run there while the leaf cluster stays resident
   cudaStream_t aux = nullptr;
@@ -45,15 +48,19 @@ struct Workspace {
   // same reduction (sizes, pointers, streams, workspace generation) repeats
   struct GraphKey {
     int kind = -1, fused = 0, la = 0, timing = 0;
-    int64_t m = 0, n = 0, w = 0, b = 0, lda = 0, ldq = 0, gen = -1;
+    int64_t m = 0, n = 0, w = 0, b = 0, lda = 0, ldq = 0, gen = -1, max_iters = 0;
     const void* A = nullptr;
     const void* Q = nullptr;
+    br_factors fo{};  // factor output pointers (all NULL when none)
     cudaStream_t main = nullptr, panel = nullptr;
     bool operator==(const GraphKey& o) const {
       return kind == o.kind && fused == o.fused && la == o.la && timing == o.timing && m == o.m &&
-             n == o.n &&
-             w == o.w && b == o.b && lda == o.lda && ldq == o.ldq && gen == o.gen && A == o.A &&
-             Q == o.Q && main == o.main && panel == o.panel;
+             n == o.n && w == o.w && b == o.b && lda == o.lda && ldq == o.ldq && gen == o.gen &&
+             max_iters == o.max_iters && A == o.A && Q == o.Q && main == o.main &&
+             panel == o.panel && fo.yl == o.fo.yl && fo.ldyl == o.fo.ldyl && fo.tl == o.fo.tl &&
+             fo.ldtl == o.fo.ldtl && fo.taul == o.fo.taul && fo.yr == o.fo.yr &&
+             fo.ldyr == o.fo.ldyr && fo.tr == o.fo.tr && fo.ldtr == o.fo.ldtr &&
+             fo.taur == o.fo.taur;
     }
   };
   GraphKey gkey;
@@ -92,7 +99,20 @@ struct Workspace {
   int64_t t_launches[TC_COUNT] = {0, 0, 0, 0};
   int64_t launches = 0;
   int active = 0;  // stream used by kernel-level C-ABI calls: 0 main, 1 panel
+  // factor output of the reduction in progress (device pointers; nullable)
+  const br_factors* fo = nullptr;
+  int64_t max_iters = 0;  // BR_OPT_MAX_ITERS: partial reduction (0 = full)
 };
+
+// Store one panel's factors into the reduction's factor output (on the
+// panel's stream, right after it was factored). chain 0 = left (QR), 1 =
+// right (LQ); r0 = first row of Y_k in the packed layout (br_factors).
+int store_factors(Workspace& ws, cudaStream_t st, int chain, int64_t k, int64_t r0, int64_t j,
+                  int64_t bp, const double* Y, int64_t ldy, const double* T, int64_t ldt,
+                  const double* tau);
+// Copy the raw working matrix of a partial reduction (BR_OPT_MAX_ITERS) to a
+// streamed host destination.
+int band_out_raw(Workspace& ws, BandOut* bo, int64_t cols);
 
 // Kernels launched by this library in this process (stats / bench evidence).
 int64_t launch_count();

@@ -70,6 +70,11 @@ int sevp_reduce(Workspace& ws, int64_t n, int64_t w, int64_t b, int lookahead, d
                 int64_t lda, double* Q, int64_t ldq, int64_t* iterations, BandOut* bo) {
   std::vector<int64_t> ks;
   for (int64_t k = 0; n - k - w >= 2; k += std::min(b, n - k - w)) ks.push_back(k);
+  // partial reduction (BR_OPT_MAX_ITERS): the first max_iters panels only,
+  // raw working matrix out (no finalize, no streamed finalized blocks)
+  const bool partial = ws.max_iters > 0 && ws.max_iters < (int64_t)ks.size();
+  if (partial) ks.resize((size_t)ws.max_iters);
+  BandOut* bof = partial ? nullptr : bo;
   *iterations = (int64_t)ks.size();
   if (ks.empty()) {  // n <= w + 1: input returned unchanged (sevp.py:302-305)
     if (bo) {
@@ -119,7 +124,8 @@ int sevp_reduce(Workspace& ws, int64_t n, int64_t w, int64_t b, int lookahead, d
     MatView P(Aat(k + w, k), lda, j, bp);
     MatView Y(Yb[par], jmax, j, bp), T(Tb[par], b, bp, bp), W(Wb[par], jmax, j, bp);
     TimeScope ts(ws, st, TC_PANEL, panel_flops(j, bp), "qr", k);
-    return panel_qr(st, sk, ws.pscratch, P, Y, taub[par], T, &W, panel_cap(j), &ws);
+    BR_CHECK(panel_qr(st, sk, ws.pscratch, P, Y, taub[par], T, &W, panel_cap(j), &ws));
+    return store_factors(ws, st, 0, k, k + w, j, bp, Yb[par], jmax, Tb[par], b, taub[par]);
   };
 
   cudaEvent_t ev_panel = nullptr;
@@ -214,7 +220,12 @@ int sevp_reduce(Workspace& ws, int64_t n, int64_t w, int64_t b, int lookahead, d
       BR_CHECK(accq());
       if (has_next) BR_CHECK(do_panel(ws.main, ws.sk_main, kn, par ^ 1));
     }
-    BR_CHECK(band_out_flush(ws, bo, k + bp));  // columns [0, k + bp) are final
+    BR_CHECK(band_out_flush(ws, bof, k + bp));  // columns [0, k + bp) are final
+  }
+  if (partial) {
+    BR_CHECK(band_out_raw(ws, bo, n));
+    ws_events_reset(ws);
+    return 0;
   }
   if (bo) {
     BR_CHECK(band_out_flush(ws, bo, n));
@@ -239,7 +250,11 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
     its.push_back({k, bp});
     k += bp;
   }
+  const bool partial = ws.max_iters > 0 && ws.max_iters < (int64_t)its.size();
+  if (partial) its.resize((size_t)ws.max_iters);
   *iterations = (int64_t)its.size();
+  BandOut* const bo_full = bo;
+  if (partial) bo = nullptr;
   BandIn* bi = ws.band_in;
   if (bi) BR_CHECK(band_in_start(ws, bi));
   if (its.empty()) {
@@ -286,16 +301,18 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
     MatView P(Aat(k, k), lda, i, bp);
     MatView Y(Yu[par], m, i, bp), T(Tu[par], b, bp, bp), W(Wu[par], m, i, bp);
     TimeScope ts(ws, st, TC_PANEL, panel_flops(i, bp), "qr", k);
-    return panel_qr(st, sk, ws.pscratch, P, Y, tauu[par], T, &W, panel_cap(i), &ws,
-                    pz_rows() > 0 ? &mk_qr[par] : nullptr);
+    BR_CHECK(panel_qr(st, sk, ws.pscratch, P, Y, tauu[par], T, &W, panel_cap(i), &ws,
+                      pz_rows() > 0 ? &mk_qr[par] : nullptr));
+    return store_factors(ws, st, 0, k, k, i, bp, Yu[par], m, Tu[par], b, tauu[par]);
   };
   auto lq = [&](cudaStream_t st, Scratch& sk, int64_t k, int64_t bq) -> int {
     const int64_t jr = n - k - w;
     MatView P(Aat(k, k + w), lda, jr, bq, true);  // transposed view of the bq x jr rows
     MatView Y(Yv, n, jr, bq), T(Tv, b, bq, bq), W(Wv, n, jr, bq);
     TimeScope ts(ws, st, TC_PANEL, panel_flops(jr, bq), "lq", k);
-    return panel_qr(st, sk, ws.pscratch, P, Y, tauv, T, &W, panel_cap(jr), &ws,
-                    pz_rows() > 0 ? &mk_lq : nullptr);
+    BR_CHECK(panel_qr(st, sk, ws.pscratch, P, Y, tauv, T, &W, panel_cap(jr), &ws,
+                      pz_rows() > 0 ? &mk_lq : nullptr));
+    return store_factors(ws, st, 1, k, k + w, jr, bq, Yv, n, Tv, b, tauv);
   };
   auto handoff = [&]() -> int {  // main -> panel ordering point
     cudaEvent_t ev = ws_event(ws);
@@ -475,6 +492,11 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
   }
   if (ev_qr) BR_CHECK(join(ev_qr));
   BR_CHECK(band_in_wait(ws, bi, n));
+  if (partial) {
+    BR_CHECK(band_out_raw(ws, bo_full, n));
+    ws_events_reset(ws);
+    return 0;
+  }
   if (bo) {
     BR_CHECK(band_out_flush(ws, bo, n));
     ws_events_reset(ws);
@@ -515,6 +537,10 @@ int band_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int f
     its.push_back({k, bp, jr, jr >= 1 ? std::min(bp, jr) : 0});
     k += bp;
   }
+  const bool partial = ws.max_iters > 0 && ws.max_iters < (int64_t)its.size();
+  if (partial) its.resize((size_t)ws.max_iters);
+  BandOut* const bo_full = bo;
+  if (partial) bo = nullptr;
   *iterations = (int64_t)its.size();
   if (its.empty()) {  // m <= w + 1: returned unchanged (ref svd.py:561-564)
     if (bo) {
@@ -558,13 +584,15 @@ int band_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int f
     MatView P(Aat(t.k + w, t.k), lda, i, t.bp);
     MatView Y(Yu[par], m, i, t.bp), T(Tu[par], b, t.bp, t.bp), W(Wu[par], m, i, t.bp);
     TimeScope ts(ws, st, TC_PANEL, panel_flops(i, t.bp), "qr", t.k);
-    return panel_qr(st, sk, ws.pscratch, P, Y, tauu[par], T, &W, panel_cap(i), &ws);
+    BR_CHECK(panel_qr(st, sk, ws.pscratch, P, Y, tauu[par], T, &W, panel_cap(i), &ws));
+    return store_factors(ws, st, 0, t.k, t.k + w, i, t.bp, Yu[par], m, Tu[par], b, tauu[par]);
   };
   auto lq = [&](cudaStream_t st, Scratch& sk, const It& t, int par) -> int {
     MatView P(Aat(t.k, t.k + w), lda, t.jr, t.bq, true);  // transposed view of the bq x jr rows
     MatView Y(Yv[par], n, t.jr, t.bq), T(Tv[par], b, t.bq, t.bq), W(Wv[par], n, t.jr, t.bq);
     TimeScope ts(ws, st, TC_PANEL, panel_flops(t.jr, t.bq), "lq", t.k);
-    return panel_qr(st, sk, ws.pscratch, P, Y, tauv[par], T, &W, panel_cap(t.jr), &ws);
+    BR_CHECK(panel_qr(st, sk, ws.pscratch, P, Y, tauv[par], T, &W, panel_cap(t.jr), &ws));
+    return store_factors(ws, st, 1, t.k, t.k + w, t.jr, t.bq, Yv[par], n, Tv[par], b, tauv[par]);
   };
   auto panels = [&](cudaStream_t st, Scratch& sk, const It& t, int par) -> int {
     BR_CHECK(qr(st, sk, t, par));
@@ -723,6 +751,11 @@ int band_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int f
     BR_CHECK(band_out_flush(ws, bo, std::min(n, t.k + t.bp)));  // columns [0, k + bp) are final
   }
   if (ev_panels) BR_CUDA(cudaStreamWaitEvent(ws.main, ev_panels, 0));
+  if (partial) {
+    BR_CHECK(band_out_raw(ws, bo_full, n));
+    ws_events_reset(ws);
+    return 0;
+  }
   if (bo) {
     BR_CHECK(band_out_flush(ws, bo, n));
     ws_events_reset(ws);

@@ -9,7 +9,9 @@ validation, result type and edge semantics (ref sevp.py:287-324):
 Schedules: REFERENCE -> look-ahead depth 0; V1 / V2 -> depth 1 (the next
 panel is factored on the panel stream while the trailing update finishes).
 Both are bitwise identical on the GPU. Extensions (keyword-only):
-`lookahead` overrides the depth, `device` selects the GPU.
+`lookahead` overrides the depth, `device` selects the GPU, `return_factors`
+returns every panel's Householder factors (`result.factors`, see factors.py;
+the reference keeps them only in private state, ref sevp.py:106,128-134).
 """
 from __future__ import annotations
 
@@ -20,6 +22,7 @@ from enum import Enum
 import numpy as np
 
 from . import _dev, _lib
+from . import factors as _factors
 from .flops import FLOPS, sevp_counted_flops, sevp_nominal_flops  # noqa: F401
 
 
@@ -69,6 +72,7 @@ class SevpResult:
     q: np.ndarray | None
     flops: dict
     iterations: int
+    factors: "_factors.BandFactors | None" = None  # extension: return_factors=True
 
 
 def _schedule(n, w, b):
@@ -91,7 +95,8 @@ def _depth(cfg, groups, lookahead):
     return 0 if cfg.variant == SevpVariant.REFERENCE else 1
 
 
-def reduce_sym_band(A, cfg, groups=None, *, lookahead=None, device=None, stats=None):
+def reduce_sym_band(A, cfg, groups=None, *, lookahead=None, device=None, stats=None,
+                    return_factors=False):
     """Reduce symmetric A to a symmetric band matrix of bandwidth cfg.w."""
     cfg.validate()
     A = np.array(A, dtype=np.float64, order="F")
@@ -108,10 +113,11 @@ def reduce_sym_band(A, cfg, groups=None, *, lookahead=None, device=None, stats=N
     n = cfg.n
     band = np.empty((n, n), order="F")
     Q = np.empty((n, n), order="F") if cfg.accumulate_q else None
+    fo, arrs = _factors.alloc_host(n, n, cfg.b, False) if return_factors else (None, None)
     st = _lib.BrStats()
     rc = _dev.run_traced(h, groups, lambda: lib.br_reduce_sym_band_host(
         h, n, cfg.w, cfg.b, depth, A.ctypes.data, n, band.ctypes.data, n,
-        Q.ctypes.data if Q is not None else None, n, st))
+        Q.ctypes.data if Q is not None else None, n, fo, st))
     _lib.check(rc, "reduce_sym_band")
     variant = {SevpVariant.REFERENCE: "reference", SevpVariant.V1: "v1", SevpVariant.V2: "v2"}[cfg.variant]
     flops, iters = sevp_counted_flops(n, cfg.w, cfg.b, variant, cfg.accumulate_q, cfg.inner_b)
@@ -120,4 +126,8 @@ def reduce_sym_band(A, cfg, groups=None, *, lookahead=None, device=None, stats=N
             FLOPS.add(key, val)
     if stats is not None:
         stats.update(device_ms=st.device_ms, launches=st.launches, iterations=st.iterations)
-    return SevpResult(band=band, q=Q, flops=flops, iterations=int(st.iterations))
+    fac = None
+    if return_factors:
+        fac = _factors.BandFactors(left=_factors.ChainFactors(
+            arrs["yl"], arrs["tl"], arrs["taul"], _factors.sevp_panels(n, cfg.w, cfg.b), n))
+    return SevpResult(band=band, q=Q, flops=flops, iterations=int(st.iterations), factors=fac)

@@ -25,6 +25,7 @@ from enum import Enum
 import numpy as np
 
 from . import _dev, _lib
+from . import factors as _factors
 from .flops import FLOPS, band_counted_flops, svd_nominal_flops, tri_counted_flops  # noqa: F401
 from .sevp import V2Mapping
 
@@ -82,6 +83,7 @@ class SvdResult:
     lower_bw: int
     upper_bw: int
     iterations: int
+    factors: "_factors.BandFactors | None" = None  # extension: return_factors=True
 
 
 def _depth(groups, lookahead):
@@ -94,9 +96,17 @@ def _depth(groups, lookahead):
     return 1
 
 
+def _swap(fac):
+    # factors of A^T: its left chain is A's right chain and vice versa
+    return None if fac is None else _factors.BandFactors(left=fac.right, right=fac.left)
+
+
 def reduce_tri_band(A, w, b, groups=None, range_log=None, inner_b=16, *, lookahead=None,
-                    device=None, stats=None):
-    """Reduce A to upper triangular-band form (band[i,j] = 0 for i > j or j > i + w)."""
+                    device=None, stats=None, return_factors=False):
+    """Reduce A to upper triangular-band form (band[i,j] = 0 for i > j or j > i + w).
+
+    return_factors=True (extension) adds `factors`: the QR chain (left, U)
+    and the LQ chain (right, V) with A = U B V^T (see factors.py)."""
     if w < 1:
         raise ValueError("w >= 1")
     if not (1 <= b <= w):
@@ -113,14 +123,16 @@ def reduce_tri_band(A, w, b, groups=None, range_log=None, inner_b=16, *, lookahe
     m, n = A.shape
     if m < n:
         inner = reduce_tri_band(np.asfortranarray(A.T), w, b, groups, None, inner_b,
-                                lookahead=lookahead, device=device, stats=stats)
+                                lookahead=lookahead, device=device, stats=stats,
+                                return_factors=return_factors)
         return SvdResult(band=np.asfortranarray(inner.band.T), flops=inner.flops,
                          form=SvdForm.TRIANGULAR_BAND, lower_bw=w, upper_bw=0,
-                         iterations=inner.iterations)
+                         iterations=inner.iterations, factors=_swap(inner.factors))
     band = np.empty((m, n), order="F")
+    fo, arrs = _factors.alloc_host(m, n, b, True) if return_factors else (None, None)
     st = _lib.BrStats()
     rc = _dev.run_traced(h, groups, lambda: lib.br_reduce_tri_band_host(
-        h, m, n, w, b, depth, A.ctypes.data, m, band.ctypes.data, m, st))
+        h, m, n, w, b, depth, A.ctypes.data, m, band.ctypes.data, m, fo, st))
     _lib.check(rc, "reduce_tri_band")
     flops, _ = tri_counted_flops(m, n, w, b, inner_b)
     for key, val in flops.items():
@@ -129,11 +141,21 @@ def reduce_tri_band(A, w, b, groups=None, range_log=None, inner_b=16, *, lookahe
     if stats is not None:
         stats.update(device_ms=st.device_ms, launches=st.launches, iterations=st.iterations)
     return SvdResult(band=band, flops=flops, form=SvdForm.TRIANGULAR_BAND, lower_bw=0, upper_bw=w,
-                     iterations=int(st.iterations))
+                     iterations=int(st.iterations),
+                     factors=_chains(arrs, _factors.tri_panels(m, n, w, b), m, n))
+
+
+def _chains(arrs, panels, m, n):
+    if arrs is None:
+        return None
+    left, right = panels
+    return _factors.BandFactors(
+        left=_factors.ChainFactors(arrs["yl"], arrs["tl"], arrs["taul"], left, m),
+        right=_factors.ChainFactors(arrs["yr"], arrs["tr"], arrs["taur"], right, n))
 
 
 def reduce_band_svd(A, cfg, groups=None, range_log=None, *, lookahead=None, device=None,
-                    stats=None):
+                    stats=None, return_factors=False):
     """Dispatch on cfg.form (ref svd.py:515-589); m < n reduces A^T and swaps
     the bandwidth tags (ref svd.py:530-550); m <= w + 1 returns A unchanged."""
     cfg.validate()
@@ -148,13 +170,15 @@ def reduce_band_svd(A, cfg, groups=None, range_log=None, *, lookahead=None, devi
             tcfg = SvdConfig(m=cfg.n, n=cfg.m, w=cfg.w, b=cfg.b, form=cfg.form,
                              variant=cfg.variant, v2_mapping=cfg.v2_mapping, inner_b=cfg.inner_b)
             inner = reduce_band_svd(np.asfortranarray(A.T), tcfg, groups, range_log,
-                                    lookahead=lookahead, device=device, stats=stats)
+                                    lookahead=lookahead, device=device, stats=stats,
+                                    return_factors=return_factors)
         return SvdResult(band=np.asfortranarray(inner.band.T), flops=inner.flops, form=cfg.form,
                          lower_bw=inner.upper_bw, upper_bw=inner.lower_bw,
-                         iterations=inner.iterations)
+                         iterations=inner.iterations, factors=_swap(inner.factors))
     if cfg.form == SvdForm.TRIANGULAR_BAND:
         return reduce_tri_band(A, cfg.w, cfg.b, groups, range_log, cfg.inner_b,
-                               lookahead=lookahead, device=device, stats=stats)
+                               lookahead=lookahead, device=device, stats=stats,
+                               return_factors=return_factors)
     if range_log is not None:
         if cfg.variant != SvdVariant.REFERENCE:
             raise ValueError("range logging is defined for the reference schedule")
@@ -172,9 +196,10 @@ def reduce_band_svd(A, cfg, groups=None, range_log=None, *, lookahead=None, devi
     lib = _lib.load()
     h, _ = _dev.ctx(device)
     band = np.empty((m, n), order="F")
+    fo, arrs = _factors.alloc_host(m, n, b, True) if return_factors else (None, None)
     st = _lib.BrStats()
     rc = _dev.run_traced(h, groups, lambda: lib.br_reduce_band_host(
-        h, m, n, w, b, int(simultaneous), depth, A.ctypes.data, m, band.ctypes.data, m, st))
+        h, m, n, w, b, int(simultaneous), depth, A.ctypes.data, m, band.ctypes.data, m, fo, st))
     _lib.check(rc, "reduce_band_svd")
     if st.iterations == 0:
         flops = {"total": 0}
@@ -186,4 +211,5 @@ def reduce_band_svd(A, cfg, groups=None, range_log=None, *, lookahead=None, devi
     if stats is not None:
         stats.update(device_ms=st.device_ms, launches=st.launches, iterations=st.iterations)
     return SvdResult(band=band, flops=flops, form=SvdForm.BAND, lower_bw=w, upper_bw=w,
-                     iterations=int(st.iterations))
+                     iterations=int(st.iterations),
+                     factors=_chains(arrs, _factors.band_panels(m, n, w, b), m, n))

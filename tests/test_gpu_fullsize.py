@@ -1,8 +1,20 @@
-"""BASELINE.json configurations at full size on the GPU: c3 against the
-oracle, and size-independent properties for c3-c5 (exact band pattern and
-symmetry, Frobenius norm and trace preserved by the orthogonal two-sided
-transforms, look-ahead bitwise equal to the sequential schedule, run-to-run
-determinism)."""
+"""BASELINE.json configurations at full size on the GPU.
+
+c1/c2 are compared with the oracle whole in test_gpu_parity.py; here:
+  * c3 whole against the oracle, plus its graded spectrum;
+  * c4 (the bench workload) and c5 against the oracle through a PARTIAL
+    reduction (BR_OPT_MAX_ITERS: the first panels, raw working matrix - the
+    full CPU run is minutes to tens of minutes): the trailing matrix and the
+    finished band entries after k iterations, <= 1e-12 sqrt(n) ||A||_F;
+  * spectra of the full c4/c5 bands against A's on the GPU (cuSOLVER as the
+    checker), normwise <= 1e-10 ||A||_2 (SURVEY finding 6);
+  * the north-star backward error ||A - Q B Q^T||_F / (n eps ||A||_F) (c1,
+    c3, c5 through accumulate_q) and ||A - U B V^T|| (c4 through the returned
+    factors), asserted <= 10;
+  * size-independent properties: exact band pattern and symmetry, Frobenius
+    norm and trace preserved, look-ahead bitwise equal to the sequential
+    schedule, run-to-run determinism.
+"""
 import ctypes as C
 
 import numpy as np
@@ -11,21 +23,34 @@ import pytest
 import oracle as O
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+EPS = np.finfo(np.float64).eps
 
 
-def _run(kind, A, w, b, la, h, lib, torch):
-    from paper_1709_00302_b200 import _lib
-
+def _dev_matrix(A, torch):
     n = A.shape[0]
     ld = (n + 31) // 32 * 32
-    d = torch.empty((n, ld), dtype=torch.float64, device="cuda")
+    d = torch.empty((A.shape[1], ld), dtype=torch.float64, device="cuda")
     d[:, :n].copy_(torch.from_numpy(np.asfortranarray(A).T))
+    return d, ld
+
+
+def _run(kind, A0d, ld, n, w, b, la, h, lib, torch, Q=None, factors=None, max_iters=0):
+    """One reduction on a device copy of A0d (column-major, ld); returns it."""
+    from paper_1709_00302_b200 import _lib
+
+    d = A0d.clone()
     st = _lib.BrStats()
-    if kind == "sevp":
-        rc = lib.br_reduce_sym_band(h, n, w, b, la, d.data_ptr(), ld, None, 0, st)
-    else:
-        rc = lib.br_reduce_tri_band(h, n, n, w, b, la, d.data_ptr(), ld, st)
-    _lib.check(rc, "reduce")
+    _lib.check(lib.br_set_option(h, _lib.BR_OPT_MAX_ITERS, max_iters), "option")
+    try:
+        if kind == "sevp":
+            rc = lib.br_reduce_sym_band(h, n, w, b, la, d.data_ptr(), ld,
+                                        Q.data_ptr() if Q is not None else None, ld, factors, st)
+        else:
+            rc = lib.br_reduce_tri_band(h, n, n, w, b, la, d.data_ptr(), ld, factors, st)
+        _lib.check(rc, "reduce")
+    finally:
+        lib.br_set_option(h, _lib.BR_OPT_MAX_ITERS, 0)
+    torch.cuda.synchronize()
     return d, st
 
 
@@ -41,44 +66,198 @@ def env():
     return torch, lib, h
 
 
-def test_c3_full_vs_oracle(env):
-    torch, lib, h = env
-    A = O.gen_c3()
-    d, st = _run("sevp", A, 128, 128, 1, h, lib, torch)
-    band = d[:, :8192].cpu().numpy().T
-    ref, _, it = O.reduce_sym_band(A, 8192, 128, 128)
-    assert st.iterations == it
-    assert O.band_check(band, 128, 128) == 0.0
-    assert np.linalg.norm(band - ref) / np.linalg.norm(A) <= 1e-12 * np.sqrt(8192)
-    ev_a = np.linalg.eigvalsh(A)
-    ev_b = torch.linalg.eigvalsh(torch.from_numpy(band).cuda()).cpu().numpy()
-    assert np.max(np.abs(ev_a - ev_b)) <= 1e-10 * np.max(np.abs(ev_a))
+def _fro(x, torch):
+    return float(torch.linalg.norm(x))
 
 
-@pytest.mark.parametrize("cfg", ["c4", "c5"])
-def test_large_configs_properties(env, cfg):
-    torch, lib, h = env
-    kind, n, w, b = {"c4": ("tri", 16384, 256, 256), "c5": ("sevp", 32768, 256, 256)}[cfg]
-    A = O.gen_config(cfg)
-    nA = float(np.linalg.norm(A))  # c5's generator is exactly symmetric
-    trA = float(np.trace(A))
-    d1, st = _run(kind, A, w, b, 1, h, lib, torch)
-    band = d1[:, :n]  # row-major view of the column-major band: band^T
-    # exact zeros off the band, on the device
+def _eig(M, torch):
+    return torch.linalg.eigvalsh(M).double()
+
+
+def _sing(M, torch):
+    """Singular values of a square M: the nonnegative eigenvalues of the
+    augmented [[0, M], [M^T, 0]] (symmetric eigensolver, normwise stable)."""
+    n = M.shape[0]
+    Z = torch.zeros((2 * n, 2 * n), dtype=torch.float64, device=M.device)
+    Z[:n, n:] = M
+    Z[n:, :n] = M.T
+    ev = torch.linalg.eigvalsh(Z)
+    del Z
+    return ev[n:]
+
+
+def _partial_vs_oracle(kind, A, d, n, w, b, iters, torch):
+    """Compare the raw GPU matrix after `iters` panels with the oracle's: the
+    trailing block (lower triangle for SEVP) and the finished band entries."""
+    if kind == "sevp":
+        ref, _, it = O.reduce_sym_band(A, n, w, b, max_iters=iters, finalize=False)
+        kn = O.sevp_schedule(n, w, b)[iters]
+    else:
+        ref, _, _, it = O.reduce_tri_band(A, w, b, max_iters=iters, finalize=False)
+        kn = O.tri_schedule(n, n, b)[iters][0]
+    assert it == iters
+    R = torch.from_numpy(np.asfortranarray(ref).T).cuda()  # (col, row) like d
+    del ref
+    G = d[:, :n]
+    num = 0.0
+    i = torch.arange(n, device="cuda")
+    for c0 in range(0, n, 2048):  # column blocks: (col, row) index grids stay small
+        c1 = min(n, c0 + 2048)
+        col = torch.arange(c0, c1, device="cuda")[:, None]
+        row = i[None, :]
+        if kind == "sevp":
+            keep = ((row - col >= 0) & (row - col <= w)) | ((col >= kn) & (row >= col))
+        else:
+            keep = ((col - row >= 0) & (col - row <= w)) | ((col >= kn) & (row >= kn))
+        diff = torch.where(keep, G[c0:c1] - R[c0:c1], torch.zeros((), dtype=torch.float64, device="cuda"))
+        num += float((diff * diff).sum())
+    err = np.sqrt(num) / float(np.linalg.norm(A))
+    print(f"{kind} n={n}: partial ({iters} panels) rel diff vs oracle {err:.2e}")
+    assert err <= 1e-12 * np.sqrt(n)
+
+
+def _pattern(band, n, w, kind, torch):
     i = torch.arange(n, device="cuda")
     r = i[None, :]  # row index of element (c, r) of the transposed view
     c = i[:, None]
     off = ((r - c) > (w if kind == "sevp" else 0)) | ((c - r) > w)
-    assert float(band[off].abs().max()) == 0.0
-    if kind == "sevp":
-        assert torch.equal(band, band.T)
-        assert abs(float(torch.trace(band)) - trA) <= 1e-10 * nA
-    fro = float(torch.linalg.norm(band))
-    assert abs(fro - nA) <= 1e-12 * np.sqrt(n) * nA
-    del off, r, c, i
-    # depth 1 == depth 0 bitwise, and run-to-run determinism
-    d0, _ = _run(kind, A, w, b, 0, h, lib, torch)
+    return float(band[off].abs().max())
+
+
+def _apply_chain(Mt, yl, tl, panels, torch):
+    """M := M Q_0 Q_1 ... for the packed chain (test-side, cuBLAS): Mt is the
+    (col, row) view of M, i.e. M^T row-major; Q_k = I + W Y^T on cols r0.."""
+    for k, r0, rows, cols in panels:
+        Y = yl[k:k + cols, r0:r0 + rows].T  # column-major packed -> (rows, cols)
+        T = tl[k:k + cols, :cols].T
+        W = Y @ T
+        Mr = Mt[r0:r0 + rows, :].T  # M[:, r0:r0+rows]
+        upd = (Mr @ W) @ Y.T
+        Mt[r0:r0 + rows, :] += upd.T
+    return Mt
+
+
+def test_c1_backward_error(env):
+    torch, lib, h = env
+    A = O.gen_c1()
+    n = 2048
+    A0d, ld = _dev_matrix(A, torch)
+    Q = torch.empty_like(A0d)
+    d, _ = _run("sevp", A0d, ld, n, 32, 32, 1, h, lib, torch, Q=Q)
+    B, Qm, Ad = d[:, :n].T, Q[:, :n].T, A0d[:, :n].T
+    be = _fro(Ad - Qm @ B @ Qm.T, torch) / (n * EPS * _fro(Ad, torch))
+    print(f"c1 backward error {be:.3f}")
+    assert be <= 10.0
+
+
+def test_c3_full_vs_oracle(env):
+    torch, lib, h = env
+    A = O.gen_c3()
+    n = 8192
+    A0d, ld = _dev_matrix(A, torch)
+    Q = torch.empty_like(A0d)
+    d, st = _run("sevp", A0d, ld, n, 128, 128, 1, h, lib, torch, Q=Q)
+    band = d[:, :n].cpu().numpy().T
+    ref, _, it = O.reduce_sym_band(A, n, 128, 128)
+    assert st.iterations == it
+    assert O.band_check(band, 128, 128) == 0.0
+    assert np.linalg.norm(band - ref) / np.linalg.norm(A) <= 1e-12 * np.sqrt(n)
+    ev_a = np.linalg.eigvalsh(A)
+    ev_b = torch.linalg.eigvalsh(torch.from_numpy(band).cuda()).cpu().numpy()
+    assert np.max(np.abs(ev_a - ev_b)) <= 1e-10 * np.max(np.abs(ev_a))
+    B, Qm, Ad = d[:, :n].T, Q[:, :n].T, A0d[:, :n].T
+    be = _fro(Ad - Qm @ B @ Qm.T, torch) / (n * EPS * _fro(Ad, torch))
+    print(f"c3 backward error {be:.3f}")
+    assert be <= 10.0
+
+
+def test_c4_full(env):
+    """The bench workload: partial vs oracle, properties, factors-based
+    backward error, singular values."""
+    torch, lib, h = env
+    from paper_1709_00302_b200 import _lib
+    from paper_1709_00302_b200.factors import tri_panels
+
+    n, w, b = 16384, 256, 256
+    A = O.gen_c4()
+    nA = float(np.linalg.norm(A))
+    A0d, ld = _dev_matrix(A, torch)
+    # partial reduction vs the oracle (first 3 panels)
+    dp, st = _run("tri", A0d, ld, n, w, b, 1, h, lib, torch, max_iters=3)
+    assert st.iterations == 3
+    _partial_vs_oracle("tri", A, dp, n, w, b, 3, torch)
+    del dp
+    # full reduction with factors
+    yl = torch.zeros((n, n), dtype=torch.float64, device="cuda")
+    yr = torch.zeros((n, n), dtype=torch.float64, device="cuda")
+    tl = torch.zeros((n, b), dtype=torch.float64, device="cuda")
+    tr = torch.zeros((n, b), dtype=torch.float64, device="cuda")
+    taul = torch.zeros(n, dtype=torch.float64, device="cuda")
+    taur = torch.zeros(n, dtype=torch.float64, device="cuda")
+    f = _lib.BrFactors(yl.data_ptr(), n, tl.data_ptr(), b, taul.data_ptr(),
+                       yr.data_ptr(), n, tr.data_ptr(), b, taur.data_ptr())
+    d1, st = _run("tri", A0d, ld, n, w, b, 1, h, lib, torch, factors=f)
+    band = d1[:, :n]
+    assert _pattern(band, n, w, "tri", torch) == 0.0
+    assert abs(_fro(band, torch) - nA) <= 1e-12 * np.sqrt(n) * nA
+    # look-ahead == sequential, bitwise; run-to-run determinism; factors change nothing
+    d0, _ = _run("tri", A0d, ld, n, w, b, 0, h, lib, torch)
     assert torch.equal(d0[:, :n], band)
     del d0
-    d2, _ = _run(kind, A, w, b, 1, h, lib, torch)
+    d2, _ = _run("tri", A0d, ld, n, w, b, 1, h, lib, torch)
     assert torch.equal(d2[:, :n], band)
+    del d2
+    # backward error: U = Q_U0 Q_U1 ..., V likewise, A = U B V^T
+    left, right = tri_panels(n, n, w, b)
+    Ut = _apply_chain(torch.eye(n, dtype=torch.float64, device="cuda"), yl, tl, left, torch)
+    Vt = _apply_chain(torch.eye(n, dtype=torch.float64, device="cuda"), yr, tr, right, torch)
+    del yl, yr
+    U, V, B, Ad = Ut.T, Vt.T, band.T, A0d[:, :n].T
+    orth_u = _fro(U.T @ U - torch.eye(n, dtype=torch.float64, device="cuda"), torch) / (n * EPS)
+    be = _fro(Ad - U @ B @ V.T, torch) / (n * EPS * _fro(Ad, torch))
+    print(f"c4 backward error {be:.3f}, U orthogonality {orth_u:.3f}")
+    assert be <= 10.0 and orth_u <= 10.0
+    del U, V, Ut, Vt
+    torch.cuda.empty_cache()
+    # singular values, normwise
+    sa = _sing(Ad.contiguous(), torch)
+    sb = _sing(B.contiguous(), torch)
+    err = float((sa - sb).abs().max()) / float(sa.max())
+    print(f"c4 singular values: max |diff| / ||A||_2 = {err:.2e}")
+    assert err <= 1e-10
+
+
+def test_c5_full(env):
+    """SEVP n=32768: partial vs oracle, properties, accumulate_q backward
+    error, eigenvalues."""
+    torch, lib, h = env
+    n, w, b = 32768, 256, 256
+    A = O.gen_c5()
+    nA = float(np.linalg.norm(A))
+    trA = float(np.trace(A))
+    A0d, ld = _dev_matrix(A, torch)
+    dp, st = _run("sevp", A0d, ld, n, w, b, 1, h, lib, torch, max_iters=2)
+    assert st.iterations == 2
+    _partial_vs_oracle("sevp", A, dp, n, w, b, 2, torch)
+    del dp, A
+    Q = torch.empty_like(A0d)
+    d1, _ = _run("sevp", A0d, ld, n, w, b, 1, h, lib, torch, Q=Q)
+    band = d1[:, :n]
+    assert _pattern(band, n, w, "sevp", torch) == 0.0
+    assert torch.equal(band, band.T)
+    assert abs(float(torch.trace(band)) - trA) <= 1e-10 * nA
+    assert abs(_fro(band, torch) - nA) <= 1e-12 * np.sqrt(n) * nA
+    d0, _ = _run("sevp", A0d, ld, n, w, b, 0, h, lib, torch)
+    assert torch.equal(d0[:, :n], band)
+    del d0
+    B, Qm, Ad = band.T, Q[:, :n].T, A0d[:, :n].T
+    be = _fro(Ad - Qm @ B @ Qm.T, torch) / (n * EPS * nA)
+    print(f"c5 backward error {be:.3f}")
+    assert be <= 10.0
+    del Q, Qm
+    torch.cuda.empty_cache()
+    ea = _eig(Ad.contiguous(), torch)
+    eb = _eig(B.contiguous(), torch)
+    err = float((ea - eb).abs().max()) / float(ea.abs().max())
+    print(f"c5 eigenvalues: max |diff| / ||A||_2 = {err:.2e}")
+    assert err <= 1e-10

@@ -463,11 +463,11 @@ def test_streamed_band_output_matches(br, kind):
         st = _lib.BrStats()
         if kind == "sevp":
             rc = lib.br_reduce_sym_band_host(h, n, w, b, 1, Ah.data_ptr(), n, Bt.data_ptr(), n,
-                                             None, 0, st)
+                                             None, 0, None, st)
         elif kind == "tri":
-            rc = lib.br_reduce_tri_band_host(h, n, n, w, b, 1, Ah.data_ptr(), n, Bt.data_ptr(), n, st)
+            rc = lib.br_reduce_tri_band_host(h, n, n, w, b, 1, Ah.data_ptr(), n, Bt.data_ptr(), n, None, st)
         else:
-            rc = lib.br_reduce_band_host(h, n, n, w, b, 1, 1, Ah.data_ptr(), n, Bt.data_ptr(), n, st)
+            rc = lib.br_reduce_band_host(h, n, n, w, b, 1, 1, Ah.data_ptr(), n, Bt.data_ptr(), n, None, st)
         _lib.check(rc, kind)
         outs.append(Bt.numpy().T.copy())
     assert np.array_equal(outs[0], outs[1])
@@ -479,7 +479,7 @@ def test_streamed_band_output_matches(br, kind):
         Ap = torch.from_numpy(np.asfortranarray(A).T.copy())
         Bt = torch.empty((n, n), dtype=torch.float64).pin_memory()
         _lib.check(lib.br_reduce_tri_band_host(h, n, n, w, b, 1, Ap.data_ptr(), n, Bt.data_ptr(), n,
-                                               _lib.BrStats()), kind)
+                                               None, _lib.BrStats()), kind)
         assert np.array_equal(Bt.numpy().T, outs[0])
 
 
@@ -583,3 +583,56 @@ def test_tuning_modes_agree(tmp_path, env):
     assert np.array_equal(mode[0], mode[2]) and np.array_equal(mode[1], mode[3])
     for a, b in zip(base, mode):
         assert np.linalg.norm(a - b) <= 1e-12 * np.sqrt(900) * np.linalg.norm(a)
+
+
+# --- partial reductions (BR_OPT_MAX_ITERS, the full-size parity hook) ------------
+
+@pytest.mark.parametrize("kind,n,w,b,iters", [("sevp", 300, 24, 24, 3), ("sevp", 300, 24, 8, 5),
+                                              ("tri", 280, 20, 20, 4), ("tri", 280, 20, 10, 7)])
+@pytest.mark.parametrize("la", [0, 1])
+def test_partial_reduction_vs_oracle(br, kind, n, w, b, iters, la):
+    import torch
+
+    from paper_1709_00302_b200 import _lib
+
+    lib = _lib.load()
+    h = _lib.handle(0)
+    A = sym(n, 5) if kind == "sevp" else rand(n, n, 5)
+    ld = (n + 31) // 32 * 32
+    d = torch.zeros((n, ld), dtype=torch.float64, device="cuda")
+    d[:, :n].copy_(torch.from_numpy(A.T.copy()))
+    torch.cuda.synchronize()
+    st = _lib.BrStats()
+    _lib.check(lib.br_set_option(h, _lib.BR_OPT_MAX_ITERS, iters), "opt")
+    try:
+        if kind == "sevp":
+            rc = lib.br_reduce_sym_band(h, n, w, b, la, d.data_ptr(), ld, None, 0, None, st)
+        else:
+            rc = lib.br_reduce_tri_band(h, n, n, w, b, la, d.data_ptr(), ld, None, st)
+        _lib.check(rc, kind)
+    finally:
+        lib.br_set_option(h, _lib.BR_OPT_MAX_ITERS, 0)
+    assert st.iterations == iters
+    G = d[:, :n].cpu().numpy().T
+    r = np.arange(n)[:, None]
+    c = np.arange(n)[None, :]
+    if kind == "sevp":
+        ref, _, it = O.reduce_sym_band(A, n, w, b, max_iters=iters, finalize=False)
+        kn = O.sevp_schedule(n, w, b)[iters]
+        keep = ((r - c >= 0) & (r - c <= w)) | ((c >= kn) & (r >= c))
+    else:
+        ref, _, _, it = O.reduce_tri_band(A, w, b, max_iters=iters, finalize=False)
+        kn = O.tri_schedule(n, n, b)[iters][0]
+        keep = ((c - r >= 0) & (c - r <= w)) | ((c >= kn) & (r >= kn))
+    assert it == iters
+    assert np.linalg.norm((G - ref)[keep]) <= 1e-13 * np.linalg.norm(A)
+
+
+def test_set_option_validation(br):
+    from paper_1709_00302_b200 import _lib
+
+    lib = _lib.load()
+    h = _lib.handle(0)
+    assert lib.br_set_option(h, 99, 1) == -2
+    assert lib.br_set_option(h, _lib.BR_OPT_MAX_ITERS, -1) == -3
+    assert lib.br_set_option(None, _lib.BR_OPT_MAX_ITERS, 0) == -1

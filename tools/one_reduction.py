@@ -25,10 +25,10 @@ A[:, :n].copy_(torch.from_numpy(np.asfortranarray(A_host).T))
 torch.cuda.synchronize()
 st = _lib.BrStats()
 if kind == "sevp":
-    rc = lib.br_reduce_sym_band(h, n, w, b, 1, A.data_ptr(), ld, None, 0, st)
+    rc = lib.br_reduce_sym_band(h, n, w, b, 1, A.data_ptr(), ld, None, 0, None, st)
 elif kind == "band":
-    rc = lib.br_reduce_band(h, n, n, w, b, 1, 1, A.data_ptr(), ld, st)
+    rc = lib.br_reduce_band(h, n, n, w, b, 1, 1, A.data_ptr(), ld, None, st)
 else:
-    rc = lib.br_reduce_tri_band(h, n, n, w, b, 1, A.data_ptr(), ld, st)
+    rc = lib.br_reduce_tri_band(h, n, n, w, b, 1, A.data_ptr(), ld, None, st)
 _lib.check(rc, "reduce")
 print(f"{cfg}: {st.device_ms:.2f} ms, {st.launches} launches", flush=True)

@@ -53,9 +53,9 @@ for name in args.cfgs:
         st = _lib.BrStats()
         t0 = time.perf_counter()
         if kind == "sevp":
-            rc = lib.br_reduce_sym_band(h, n, w, b, args.la, A.data_ptr(), ld, None, 0, st)
+            rc = lib.br_reduce_sym_band(h, n, w, b, args.la, A.data_ptr(), ld, None, 0, None, st)
         else:
-            rc = lib.br_reduce_tri_band(h, n, n, w, b, args.la, A.data_ptr(), ld, st)
+            rc = lib.br_reduce_tri_band(h, n, n, w, b, args.la, A.data_ptr(), ld, None, st)
         t1 = time.perf_counter()
         _lib.check(rc, name)
         gf = st.nominal_flops / (st.device_ms * 1e-3) / 1e9
