@@ -113,32 +113,76 @@ def make_input(cfg):
     return O.gen_config({"b4": "c4"}.get(cfg, cfg))
 
 
-def cpu_sample(cfg, A, seconds_hint=20.0):
-    """Time the oracle port (NumPy + multithreaded BLAS) on the first iterations
-    of the same workload; returns (gflops, iterations, seconds, cores)."""
-    import oracle as O
-    from paper_1709_00302_b200.flops import sevp_counted_flops, tri_counted_flops
+def _blas_threads():
+    try:
+        import threadpoolctl
+
+        return max((i.get("num_threads", 1) for i in threadpoolctl.threadpool_info()
+                    if i.get("user_api") == "blas"), default=os.cpu_count())
+    except Exception:
+        return os.cpu_count()
+
+
+def cpu_sample(cfg, A, seconds_hint=20.0, tasks=None):
+    """Time the reference's CPU implementation on the first panel tasks of the
+    same workload (a bounded sample). Prefers the reference package itself
+    (baseline/_ref, installed offline; its matmul rebound to multithreaded
+    BLAS = SURVEY tier B, see baseline/ref_driver.py), else the oracle port.
+    Returns a dict: value (GFLOP/s over the sampled tasks' counted flops),
+    kind, tasks, seconds, cores, sample text."""
+    from baseline import ref_driver as R
 
     kind, n, w, b, _ = CONFIGS[cfg]
-    iters = 1
-    t_total = 0.0
-    best = None
-    while True:
-        t0 = time.perf_counter()
-        if kind == "sevp":
-            O.reduce_sym_band(A, n, w, b, max_iters=iters)
-            fl = sevp_counted_flops(n, w, b, "v2", max_iters=iters)[0]["total"]
-        else:
-            O.reduce_tri_band(A, w, b, max_iters=iters)
-            fl = tri_counted_flops(n, n, w, b, max_iters=iters)[0]["total"]
-        dt = time.perf_counter() - t0
-        t_total += dt
-        best = (fl / dt / 1e9, iters, dt)
-        full = len(O.sevp_schedule(n, w, b)) if kind == "sevp" else len(O.tri_schedule(n, n, b))
-        if t_total > seconds_hint or iters >= full or dt * 2.2 > seconds_hint:
-            break
-        iters = min(full, iters * 2)
-    return best[0], best[1], best[2], os.cpu_count()
+    full = 2 * len(__import__("oracle").tri_schedule(n, n, b)) if kind == "tri" else \
+        len(__import__("oracle").sevp_schedule(n, w, b))
+    if R.available():
+        mod = R.load("blas")
+
+        def run(k):
+            fl, dt, done = R.sample(mod, kind, A, n, w, b, k)
+            return fl, dt, done
+
+        label = ("reference package (baseline/_ref) with its matmul rebound to multithreaded "
+                 "BLAS (SURVEY tier B)")
+        kind_out = "reference"
+    else:
+        import oracle as O
+        from paper_1709_00302_b200.flops import sevp_counted_flops, tri_counted_flops
+
+        def run(k):
+            t0 = time.perf_counter()
+            if kind == "sevp":
+                O.reduce_sym_band(A, n, w, b, max_iters=k, finalize=False)
+                fl = sevp_counted_flops(n, w, b, "reference", max_iters=k)[0]["total"]
+            else:
+                it = (k + 1) // 2
+                O.reduce_tri_band(A, w, b, max_iters=it, finalize=False)
+                fl = tri_counted_flops(n, n, w, b, max_iters=it)[0]["total"]
+                k = 2 * it
+            return fl, time.perf_counter() - t0, k
+
+        label = "oracle/ NumPy port + multithreaded OpenBLAS (reference package not installed)"
+        kind_out = "port"
+    if tasks is None:
+        fl, dt, done = run(1)
+        tasks = max(1, min(full, int(seconds_hint / max(dt, 1e-3))))
+        if tasks > 1:
+            fl, dt, done = run(tasks)
+    else:
+        fl, dt, done = run(tasks)
+    unit = "iterations" if kind == "sevp" else "panel tasks (QR or LQ panel + its one-sided update)"
+    return {"value": fl / dt / 1e9, "unit": "GFLOP/s", "cores": _blas_threads(), "kind": kind_out,
+            "tasks": done, "seconds": dt,
+            "sample": f"first {done} of {full} {unit} of the same {n}x{n} reduction on the same "
+                      f"input, {dt:.1f} s, rate = counted flops of the sample / its time; {label}"}
+
+
+def same_config(cfg, la, world):
+    kind, n, w, b, desc = CONFIGS[cfg]
+    return {"workload": cfg, "desc": desc, "kind": kind, "n": n, "w": w, "b": b, "lookahead": la,
+            "parallelism": "1 GPU" if world == 1 else f"1D block-cyclic columns x{world} (NCCL)",
+            "l2": f"input {n * n * 8 / 2**30:.2f} GiB vs 126 MB L2 (no flush needed)"
+            if n * n * 8 > 126e6 else "input fits L2; restored from a separate copy each step"}
 
 
 def dgemm_peak(dev):
@@ -179,19 +223,20 @@ def load_traffic(cfg):
 # arms
 # --------------------------------------------------------------------------
 def run_reference(args, rank, world):
+    """The reference's CPU implementation on the host cores (rank 0 only),
+    each step one bounded sample (the first panel tasks) of the workload."""
     kind, n, w, b, desc = CONFIGS[args.config]
     if rank != 0:
         return
     A = make_input(args.config)
-    for _ in range(args.warmup):
-        pass  # the port has no warm-up state; a sample run below is timed per step
-    vals = []
-    sample = None
+    first = cpu_sample(args.config, A, min(args.cpu_seconds, 8.0))  # sizing run (= warm-up)
+    vals, secs = [], []
     for _ in range(args.steps):
-        gf, iters, dt, cores = cpu_sample(args.config, A, args.cpu_seconds)
-        vals.append(gf)
-        sample = (iters, dt, cores)
+        r = cpu_sample(args.config, A, tasks=first["tasks"])
+        vals.append(r["value"])
+        secs.append(r["seconds"])
     v = float(np.median(vals))
+    cb = dict(r, value=v, seconds=float(np.median(secs)))
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -200,17 +245,18 @@ def run_reference(args, rank, world):
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": sample[1] * 1e3,
+        "ms_per_step": float(np.median(secs)) * 1e3,
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": args.config, "desc": desc, "kind": kind, "n": n, "w": w, "b": b},
-        "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": sample[2], "kind": "port",
-                         "sample": f"first {sample[0]} of the reduction's iterations on the full "
-                                   f"{n}x{n} input (oracle/ NumPy port, multithreaded OpenBLAS)"},
+        "config": same_config(args.config, args.lookahead, world),
+        "cpu_baseline": cb,
         "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "each step = the reference's first panel tasks on the full input (CPU has no "
+                "warm-up state: one sizing sample replaces the warm-up steps); ms_per_step is "
+                "one sample, not a whole reduction",
     }
     print(json.dumps(line), flush=True)
 
@@ -345,10 +391,7 @@ def run_ours(args, rank, world, local_rank):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and kind != "band":
-        gf, iters, dt, cores = cpu_sample(args.config, A_host, args.cpu_seconds)
-        cpu = {"value": gf, "unit": "GFLOP/s", "cores": cores, "kind": "port",
-               "sample": f"first {iters} iterations of the same {n}x{n} reduction "
-                         f"({dt:.1f} s, oracle/ NumPy port + multithreaded OpenBLAS)"}
+        cpu = cpu_sample(args.config, A_host, args.cpu_seconds)
 
     if rank == 0:
         line = {
@@ -364,10 +407,7 @@ def run_ours(args, rank, world, local_rank):
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": args.config, "desc": desc, "kind": kind, "n": n, "w": w, "b": b,
-                       "lookahead": la, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
-                       "l2": f"input {n * n * 8 / 2**30:.2f} GiB vs 126 MB L2 (no flush needed)"
-                       if n * n * 8 > 126e6 else "input fits L2; restored from a separate copy each step"},
+            "config": same_config(args.config, la, world),
             "clocks": clocks.summary(),
             "e2e": {"value": e2e_val, "unit": "GFLOP/s", "h2d_bytes_per_step": n * n * 8,
                     "d2h_bytes_per_step": n * n * 8, "steps": e2e_steps,
@@ -461,9 +501,7 @@ def run_dist(args, rank, world, local_rank):
             "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.config, "desc": desc, "kind": kind, "n": n, "w": w, "b": b,
-                       "lookahead": la, "parallelism": f"1D block-cyclic columns x{world} (NCCL)",
-                       "l2": f"input {n * n * 8 / 2**30:.2f} GiB total vs 126 MB L2 per GPU"},
+            "config": same_config(args.config, la, world),
             "clocks": clocks.summary(),
             "e2e": {"value": flops / e2e_s / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": n * n * 8,
                     "d2h_bytes_per_step": n * n * 8, "steps": e2e_steps,

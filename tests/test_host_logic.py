@@ -141,3 +141,56 @@ def test_exec_groups_maps_to_lookahead_depth():
     assert S._depth(br.SevpConfig(8, 4, 4, br.SevpVariant.V2), br.ExecGroups(4, 1), None) == 1
     assert S._depth(br.SevpConfig(8, 4, 4), None, None) == 0
     assert S._depth(br.SevpConfig(8, 4, 4), None, 1) == 1
+
+
+def test_factor_panel_enumeration_matches_schedules():
+    """The packed factor layout's panel lists (factors.py) follow the
+    reference schedules (ref sevp.py:110-122, svd.py:179-202, 265-306)."""
+    import oracle as O
+    from paper_1709_00302_b200 import factors as F
+
+    for n, w, b in [(100, 8, 8), (131, 12, 5), (64, 16, 16), (40, 40, 8)]:
+        ks = O.sevp_schedule(n, w, b)
+        p = F.sevp_panels(n, w, b)
+        assert [q[0] for q in p] == ks
+        assert all(q[1] == q[0] + w and q[2] == n - q[0] - w and q[3] == min(b, n - q[0] - w) for q in p)
+    for m, n, w, b in [(100, 100, 8, 8), (120, 70, 10, 4), (33, 33, 16, 16)]:
+        left, right = F.tri_panels(m, n, w, b)
+        assert [(q[0], q[3]) for q in left] == O.tri_schedule(m, n, b)
+        for k, r0, rows, cols in right:
+            assert r0 == k + w and rows == n - k - w and cols == min(b, n - k, m - k, rows)
+    for m, n, w, b in [(100, 100, 8, 8), (120, 70, 10, 4)]:
+        left, right = F.band_panels(m, n, w, b)
+        sched = O.band_schedule(m, n, w, b)
+        assert [(q[0], q[3]) for q in left] == [(s[0], s[1]) for s in sched]
+        assert [(q[0], q[3]) for q in right] == [(s[0], s[3]) for s in sched if s[2] >= 1]
+
+
+def test_reference_driver_bounded_sample():
+    """bench.py's reference arm runs the installed reference package itself on
+    a bounded sample (baseline/ref_driver.py); its truncated run equals the
+    oracle's first iterations."""
+    import numpy as np
+    import pytest
+
+    from baseline import ref_driver as R
+
+    if not R.available():
+        pytest.skip("reference package not installed in baseline/_ref")
+    import oracle as O
+
+    mod = R.load("blas")
+    A = np.asfortranarray(np.random.default_rng(3).standard_normal((96, 96)))
+    fl, dt, done = R.sample(mod, "tri", A, 96, 8, 8, 3)
+    assert done == 3 and fl > 0 and dt > 0
+    S = (A + A.T) / 2
+    fl, dt, done = R.sample(mod, "sevp", S, 96, 8, 8, 4)
+    assert done == 4 and fl > 0
+    # the pure (unmodified) reference and the BLAS-rebound one agree on a full run
+    full_b = mod.reduce_tri_band(A, 8, 8).band
+    mod = R.load("pure")
+    full_p = mod.reduce_tri_band(A, 8, 8).band
+    R.load("blas")
+    assert np.linalg.norm(full_b - full_p) <= 1e-13 * np.linalg.norm(A)
+    band, _, _, _ = O.reduce_tri_band(A, 8, 8)
+    assert np.linalg.norm(full_b - band) <= 1e-13 * np.linalg.norm(A)
