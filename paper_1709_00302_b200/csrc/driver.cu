@@ -6,6 +6,8 @@
 #include <atomic>
 #include <new>
 
+#include <cuda.h>
+
 #include "../../include/bandred_b200.h"
 #include "driver.cuh"
 #include "gemm.cuh"
@@ -102,7 +104,7 @@ TimeScope::~TimeScope() {
   if (ws.timing) {
     cudaEvent_t b = ws_tevent(ws);
     cudaEventRecord(b, st);
-    ws.timed.push_back({cls, a, b, flops, tag, k, st == ws.panel ? 1 : 0});
+    ws.timed.push_back({cls, a, b, flops, tag, k, (st == ws.panel || st == ws.gpanel) ? 1 : 0});
   }
 }
 
@@ -358,6 +360,7 @@ int timed_reduction(Workspace& ws, br_stats* stats, double nominal, Workspace::G
   if (!rc) rc = cu(cudaEventRecord(e1, ws.main));
   if (!rc) rc = cu(cudaEventSynchronize(e1));
   if (!rc) rc = cu(cudaStreamSynchronize(ws.panel));
+  if (!rc && ws.gpanel) rc = cu(cudaStreamSynchronize(ws.gpanel));
   if (!rc) rc = cu(cudaGetLastError());
   if (!rc) rc = cu(cudaEventElapsedTime(&ms, e0, e1));
   if (!rc && ws.timing) rc = ws_collect_timing(ws);
@@ -453,6 +456,68 @@ static int ensure_scratch(Workspace& ws, int64_t main_doubles, int64_t panel_dou
   return 0;
 }
 
+// Optional SM partition for the panel stream (BR_GREEN_SMS = N): a green
+// context holding N SMs; the panel stream is created on it, so panel
+// kernels (leaf clusters, panel GEMMs) are confined to those SMs while the
+// main stream's kernels keep the whole device. Driver entry points are
+// resolved through the runtime (no libcuda link).
+typedef CUresult (*PFN_getDevRes)(CUdevice, CUdevResource*, CUdevResourceType);
+typedef CUresult (*PFN_split)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*, unsigned,
+                              unsigned);
+typedef CUresult (*PFN_genDesc)(CUdevResourceDesc*, CUdevResource*, unsigned);
+typedef CUresult (*PFN_gcCreate)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned);
+typedef CUresult (*PFN_gcStream)(CUstream*, CUgreenCtx, unsigned, int);
+template <class F>
+static int drv_sym(const char* name, F* f) {
+  cudaDriverEntryPointQueryResult q;
+  void* p = nullptr;
+  BR_CUDA(cudaGetDriverEntryPointByVersion(name, &p, 12090, cudaEnableDefault, &q));
+  if (!p || q != cudaDriverEntryPointSuccess) {
+    set_error("driver entry point %s unavailable", name);
+    return 1;
+  }
+  *f = (F)p;
+  return 0;
+}
+static int green_panel_streams(int device, int nsm, int prio, cudaStream_t* panel, cudaStream_t* aux,
+                               int* got_sms) {
+  PFN_getDevRes getres;
+  PFN_split split;
+  PFN_genDesc gen;
+  PFN_gcCreate create;
+  PFN_gcStream mkstream;
+  BR_CHECK(drv_sym("cuDeviceGetDevResource", &getres));
+  BR_CHECK(drv_sym("cuDevSmResourceSplitByCount", &split));
+  BR_CHECK(drv_sym("cuDevResourceGenerateDesc", &gen));
+  BR_CHECK(drv_sym("cuGreenCtxCreate", &create));
+  BR_CHECK(drv_sym("cuGreenCtxStreamCreate", &mkstream));
+  CUdevResource sm, part, rest;
+  unsigned n = 1;
+  if (getres((CUdevice)device, &sm, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS ||
+      split(&part, &n, &sm, &rest, CU_DEV_SM_RESOURCE_SPLIT_MAX_POTENTIAL_CLUSTER_SIZE, (unsigned)nsm) !=
+          CUDA_SUCCESS ||
+      n != 1) {
+    set_error("green context: SM split of %d failed", nsm);
+    return 1;
+  }
+  CUdevResourceDesc desc;
+  CUgreenCtx g;
+  if (gen(&desc, &part, 1) != CUDA_SUCCESS || create(&g, desc, (CUdevice)device, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) {
+    set_error("green context creation failed");
+    return 1;
+  }
+  CUstream s1, s2;
+  if (mkstream(&s1, g, CU_STREAM_NON_BLOCKING, prio) != CUDA_SUCCESS ||
+      mkstream(&s2, g, CU_STREAM_NON_BLOCKING, prio) != CUDA_SUCCESS) {
+    set_error("green context stream creation failed");
+    return 1;
+  }
+  *panel = (cudaStream_t)s1;
+  *aux = (cudaStream_t)s2;
+  *got_sms = (int)part.sm.smCount;
+  return 0;
+}
+
 extern "C" {
 
 int br_version(void) { return 100; }
@@ -482,6 +547,15 @@ int br_create(int device, br_handle_t* out) {
   h->ws.main = h->ws.own_main;
   h->ws.panel = h->ws.own_panel;
   BR_CUDA(cudaStreamCreateWithPriority(&h->ws.aux, cudaStreamNonBlocking, hi));
+  if (const char* g = std::getenv("BR_GREEN_SMS")) {  // experimental SM partition (see above)
+    cudaStream_t gp = nullptr, ga = nullptr;
+    int got = 0;
+    const int rc = green_panel_streams(device, std::atoi(g), hi, &gp, &ga, &got);
+    if (rc) return rc;
+    h->ws.gpanel = gp;
+    h->ws.green_sms = got;
+    if (const char* r = std::getenv("BR_GREEN_ROWS")) h->ws.green_rows = std::atoll(r);
+  }
   BR_CUDA(cudaStreamCreateWithFlags(&h->ws.copy, cudaStreamNonBlocking));
   BR_CUDA(cudaStreamCreateWithFlags(&h->ws.copy_in, cudaStreamNonBlocking));
   BR_CUDA(cudaMalloc(&h->ws.flags, 128 * sizeof(unsigned)));
@@ -548,6 +622,7 @@ int br_sync(br_handle_t h) {
   DEV(h);
   BR_CUDA(cudaStreamSynchronize(h->ws.main));
   BR_CUDA(cudaStreamSynchronize(h->ws.panel));
+  if (h->ws.gpanel) BR_CUDA(cudaStreamSynchronize(h->ws.gpanel));
   return 0;
 }
 

@@ -26,6 +26,22 @@ enum TimeClass { TC_PANEL = 0, TC_SYMM = 1, TC_SYR2K = 2, TC_GEMM = 3, TC_COUNT 
 struct Workspace {
   int device = 0;
   int num_sms = 148;
+  // SM-partitioned panel stream (green context, BR_GREEN_SMS): panels taller
+  // than green_rows run on gpanel, confined to green_sms SMs, so they take
+  // SMs only from that partition while the trailing update (whole device)
+  // runs; shorter panels (the critical path near the end) use `panel`.
+  cudaStream_t gpanel = nullptr;
+  int green_sms = 0;
+  int64_t green_rows = 8192;
+  bool confined(int64_t rows) const { return gpanel != nullptr && rows > green_rows; }
+  cudaStream_t pstream(int64_t rows) const { return confined(rows) ? gpanel : panel; }
+  // split-K plan of a panel's GEMMs: depends on the panel height only, so the
+  // schedules with and without look-ahead plan (and round) identically
+  Scratch pscratch_for(const Scratch& s, int64_t rows) const {
+    Scratch r = s;
+    if (confined(rows)) r.num_sms = green_sms;
+    return r;
+  }
   cudaStream_t main = nullptr, panel = nullptr;
   cudaStream_t own_main = nullptr, own_panel = nullptr;
   Scratch sk_main, sk_panel;  // split-K partials, one per stream

@@ -22,6 +22,7 @@
 // DMMA GEMMs, and the full T is assembled from the Gram matrix.
 #include <algorithm>
 #include <cstdlib>
+#include <functional>
 
 #include <cuda.h>
 
@@ -514,7 +515,34 @@ static bool leaf_w_mode() {
 }
 
 int64_t panel_scratch_doubles(int64_t b) {
-  return b * b + LEAF_NB * LEAF_NB + 2 * LEAF_NB * b + (b > TAB_MAXB ? b * TAB_MAXB : 0);
+  // + 3 b^2: Gram / product buffers of the recursive split (panel_qr)
+  return b * b + LEAF_NB * LEAF_NB + 2 * LEAF_NB * b + (b > TAB_MAXB ? b * TAB_MAXB : 0) + 3 * b * b;
+}
+
+// Recursive splitting of wide, tall panels (panel_qr). A panel of at least
+// rec_min_rows() rows whose column range is wider than rec_width() is split
+// in two halves: the left half is factored, its block reflector
+// (I + Y1 T1 Y1^T)^T is applied to the right half with three GEMMs
+// (Z = Y1^T P2, Z' = T1^T Z, P2 += Y1 Z'), then the right half is factored.
+// Narrower ranges run the right-looking leaf loop. Same reflectors, fewer
+// passes over the panel: the right-looking rank-nb updates re-read and
+// re-write the whole rest of the panel after every leaf (j x b^2 / (2 nb)
+// doubles each way), the recursion moves j x b per level.
+static int64_t rec_width() {
+  static int64_t v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("BR_REC_WIDTH");
+    v = e ? std::atoll(e) : 1 << 30;
+  }
+  return v;
+}
+static int64_t rec_min_rows() {
+  static int64_t v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("BR_REC_MIN_ROWS");
+    v = e ? std::atoll(e) : 0;
+  }
+  return v;
 }
 
 int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView Y, double* tau,
@@ -594,35 +622,61 @@ int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView 
     BR_CUDA(cudaStreamWaitEvent(st, w.ev_aux1, 0));
     BR_CHECK(mark(0, b));
   }
-  for (int64_t s = 0; s < b && !persist; s += nbl) {
-    const int64_t e = std::min<int64_t>(s + nbl, b);
-    const int64_t w = e - s;
-    MatView leafP = P.sub(s, s, j - s, w);
-    MatView leafY = Y.sub(s, s, j - s, w);
-    if (e < b && W && leaf_w_mode()) {
-      // P[s:, e:b] += (Y_blk T_blk^T)(Y_blk^T P[s:, e:b]); the leaf writes
-      // Y_blk T_blk^T into W's columns (W itself is formed at the end)
-      MatView What = W->sub(s, s, j - s, w);
-      BR_CHECK(launch_leaf(st, leafP, leafY, tau + s, T.p + s + s * T.ld, T.ld, &What, 1));
+  // right-looking leaves over columns [c0, c1): every update stops at c1
+  auto right_looking = [&](int64_t c0, int64_t c1) -> int {
+    for (int64_t s = c0; s < c1; s += nbl) {
+      const int64_t e = std::min<int64_t>(s + nbl, c1);
+      const int64_t w = e - s;
+      MatView leafP = P.sub(s, s, j - s, w);
+      MatView leafY = Y.sub(s, s, j - s, w);
+      if (e < c1 && W && leaf_w_mode()) {
+        // P[s:, e:c1] += (Y_blk T_blk^T)(Y_blk^T P[s:, e:c1]); the leaf writes
+        // Y_blk T_blk^T into W's columns (W itself is formed at the end)
+        MatView What = W->sub(s, s, j - s, w);
+        BR_CHECK(launch_leaf(st, leafP, leafY, tau + s, T.p + s + s * T.ld, T.ld, &What, 1));
+        BR_CHECK(mark(s, e));
+        MatView rest = P.sub(s, e, j - s, c1 - e);
+        MatView Zs = Z.sub(0, 0, w, c1 - e);
+        BR_CHECK(gemm(st, ws, Zs, leafY.T(), rest, 1.0, 0.0, nullptr, max_ctas));
+        BR_CHECK(gemm(st, ws, rest, What, Zs, 1.0, 1.0, nullptr, max_ctas));
+        continue;
+      }
+      BR_CHECK(launch_leaf(st, leafP, leafY, tau + s, T.p + s + s * T.ld, T.ld, nullptr));
       BR_CHECK(mark(s, e));
-      MatView rest = P.sub(s, e, j - s, b - e);
-      MatView Zs = Z.sub(0, 0, w, b - e);
-      BR_CHECK(gemm(st, ws, Zs, leafY.T(), rest, 1.0, 0.0, nullptr, max_ctas));
-      BR_CHECK(gemm(st, ws, rest, What, Zs, 1.0, 1.0, nullptr, max_ctas));
-      continue;
+      if (e < c1) {
+        // P[s:, e:c1] += Y_blk (T_blk^T (Y_blk^T P[s:, e:c1])): the T_blk^T product
+        // rides on the split-K reduction, so the leaf needs no W
+        MatView rest = P.sub(s, e, j - s, c1 - e);
+        MatView Z2s = Z2.sub(0, 0, w, c1 - e);
+        MatView Tb(T.p + s + s * T.ld, T.ld, w, w);  // the leaf's T block
+        BR_CHECK(gemm_tt(st, ws, Z2s, leafY.T(), rest, Tb));
+        BR_CHECK(gemm(st, ws, rest, leafY, Z2s, 1.0, 1.0, nullptr, max_ctas));
+      }
     }
-    BR_CHECK(launch_leaf(st, leafP, leafY, tau + s, T.p + s + s * T.ld, T.ld, nullptr));
-    BR_CHECK(mark(s, e));
-    if (e < b) {
-      // P[s:, e:b] += Y_blk (T_blk^T (Y_blk^T P[s:, e:b])): the T_blk^T product
-      // rides on the split-K reduction, so the leaf needs no W
-      MatView rest = P.sub(s, e, j - s, b - e);
-      MatView Z2s = Z2.sub(0, 0, w, b - e);
-      MatView Tb(T.p + s + s * T.ld, T.ld, w, w);  // the leaf's T block
-      BR_CHECK(gemm_tt(st, ws, Z2s, leafY.T(), rest, Tb));
-      BR_CHECK(gemm(st, ws, rest, leafY, Z2s, 1.0, 1.0, nullptr, max_ctas));
-    }
-  }
+    return 0;
+  };
+  double* rbuf = scratch + panel_scratch_doubles(b) - 3 * b * b;  // G1 | Z | Z'
+  std::function<int(int64_t, int64_t)> rec = [&](int64_t c0, int64_t c1) -> int {
+    const int64_t w = c1 - c0;
+    // halves on leaf (and 32-row T block) boundaries: the final T assembly
+    // reads the leaves' diagonal blocks at multiples of 32
+    const int64_t al = std::max<int64_t>(nbl, TAB);
+    const int64_t h = std::max<int64_t>(al, cdiv(w / 2, al) * al);
+    if (w <= rec_width() || h >= w || j < rec_min_rows()) return right_looking(c0, c1);
+    BR_CHECK(rec(c0, c0 + h));
+    // T1 of the left half from its Gram matrix (leaves wrote the diagonal blocks)
+    MatView Y1 = Y.sub(c0, c0, j - c0, h), T1 = T.sub(c0, c0, h, h);
+    MatView G1(rbuf, h, h, h), Zr(rbuf + b * b, h, h, w - h), Zr2(rbuf + 2 * b * b, h, h, w - h);
+    BR_CHECK(gemm(st, ws, G1, Y1.T(), Y1, 1.0, 0.0, nullptr, max_ctas));
+    BR_CHECK(t_from_gram(st, G1.p, G1.ld, tau + c0, h, T1.p, T1.ld, nbl % TAB == 0));
+    // P2 := (I + Y1 T1 Y1^T)^T P2
+    MatView P2 = P.sub(c0, c0 + h, j - c0, w - h);
+    BR_CHECK(gemm(st, ws, Zr, Y1.T(), P2, 1.0, 0.0, nullptr, max_ctas));
+    BR_CHECK(gemm(st, ws, Zr2, T1.T(), Zr, 1.0, 0.0, nullptr, max_ctas));
+    BR_CHECK(gemm(st, ws, P2, Y1, Zr2, 1.0, 1.0, nullptr, max_ctas));
+    return rec(c0 + h, c1);
+  };
+  if (!persist) BR_CHECK(rec(0, b));
   // full T: Gram, then the blocked recurrence in one kernel (T is written whole,
   // zeros below the diagonal). 32-wide leaves already wrote the 32 x 32
   // diagonal blocks of T.

@@ -124,7 +124,8 @@ int sevp_reduce(Workspace& ws, int64_t n, int64_t w, int64_t b, int lookahead, d
     MatView P(Aat(k + w, k), lda, j, bp);
     MatView Y(Yb[par], jmax, j, bp), T(Tb[par], b, bp, bp), W(Wb[par], jmax, j, bp);
     TimeScope ts(ws, st, TC_PANEL, panel_flops(j, bp), "qr", k);
-    BR_CHECK(panel_qr(st, sk, ws.pscratch, P, Y, taub[par], T, &W, panel_cap(j), &ws));
+    Scratch s = ws.pscratch_for(sk, j);
+    BR_CHECK(panel_qr(st, s, ws.pscratch, P, Y, taub[par], T, &W, panel_cap(j), &ws));
     return store_factors(ws, st, 0, k, k + w, j, bp, Yb[par], jmax, Tb[par], b, taub[par]);
   };
 
@@ -187,12 +188,13 @@ int sevp_reduce(Workspace& ws, int64_t n, int64_t w, int64_t b, int lookahead, d
       return gemm(ws.main, ws.sk_main, Qs, Z, Y.T(), 1.0, 1.0);
     };
     auto launch_next_panel = [&]() -> int {
+      cudaStream_t ps = ws.pstream(n - kn - w);
       cudaEvent_t ev = ws_event(ws);
       BR_CUDA(cudaEventRecord(ev, ws.main));
-      BR_CUDA(cudaStreamWaitEvent(ws.panel, ev, 0));
-      BR_CHECK(do_panel(ws.panel, ws.sk_panel, kn, par ^ 1));
+      BR_CUDA(cudaStreamWaitEvent(ps, ev, 0));
+      BR_CHECK(do_panel(ps, ws.sk_panel, kn, par ^ 1));
       ev_panel = ws_event(ws);
-      BR_CUDA(cudaEventRecord(ev_panel, ws.panel));
+      BR_CUDA(cudaEventRecord(ev_panel, ps));
       return 0;
     };
 
@@ -301,7 +303,8 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
     MatView P(Aat(k, k), lda, i, bp);
     MatView Y(Yu[par], m, i, bp), T(Tu[par], b, bp, bp), W(Wu[par], m, i, bp);
     TimeScope ts(ws, st, TC_PANEL, panel_flops(i, bp), "qr", k);
-    BR_CHECK(panel_qr(st, sk, ws.pscratch, P, Y, tauu[par], T, &W, panel_cap(i), &ws,
+    Scratch s = ws.pscratch_for(sk, i);
+    BR_CHECK(panel_qr(st, s, ws.pscratch, P, Y, tauu[par], T, &W, panel_cap(i), &ws,
                       pz_rows() > 0 ? &mk_qr[par] : nullptr));
     return store_factors(ws, st, 0, k, k, i, bp, Yu[par], m, Tu[par], b, tauu[par]);
   };
@@ -310,19 +313,20 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
     MatView P(Aat(k, k + w), lda, jr, bq, true);  // transposed view of the bq x jr rows
     MatView Y(Yv, n, jr, bq), T(Tv, b, bq, bq), W(Wv, n, jr, bq);
     TimeScope ts(ws, st, TC_PANEL, panel_flops(jr, bq), "lq", k);
-    BR_CHECK(panel_qr(st, sk, ws.pscratch, P, Y, tauv, T, &W, panel_cap(jr), &ws,
+    Scratch s = ws.pscratch_for(sk, jr);
+    BR_CHECK(panel_qr(st, s, ws.pscratch, P, Y, tauv, T, &W, panel_cap(jr), &ws,
                       pz_rows() > 0 ? &mk_lq : nullptr));
     return store_factors(ws, st, 1, k, k + w, jr, bq, Yv, n, Tv, b, tauv);
   };
-  auto handoff = [&]() -> int {  // main -> panel ordering point
+  auto handoff = [&](cudaStream_t ps) -> int {  // main -> panel ordering point
     cudaEvent_t ev = ws_event(ws);
     BR_CUDA(cudaEventRecord(ev, ws.main));
-    BR_CUDA(cudaStreamWaitEvent(ws.panel, ev, 0));
+    BR_CUDA(cudaStreamWaitEvent(ps, ev, 0));
     return 0;
   };
-  auto mark_panel = [&]() -> cudaEvent_t {  // completion point of the last panel launch
+  auto mark_panel = [&](cudaStream_t ps) -> cudaEvent_t {  // completion of the last panel launch
     cudaEvent_t ev = ws_event(ws);
-    cudaEventRecord(ev, ws.panel);
+    cudaEventRecord(ev, ps);
     return ev;
   };
   auto join = [&](cudaEvent_t ev) -> int {  // panel -> main
@@ -355,9 +359,10 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
     bool next_issued = false;
 
     auto next_qr_on_panel = [&]() -> int {
-      BR_CHECK(handoff());
-      BR_CHECK(qr(ws.panel, ws.sk_panel, kn, bpn, par ^ 1));
-      ev_qr = mark_panel();
+      cudaStream_t ps = ws.pstream(m - kn);
+      BR_CHECK(handoff(ps));
+      BR_CHECK(qr(ps, ws.sk_panel, kn, bpn, par ^ 1));
+      ev_qr = mark_panel(ps);
       next_issued = true;
       return 0;
     };
@@ -396,9 +401,10 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
         cudaEvent_t ev_lq = nullptr;
         auto issue_lq = [&]() -> int {  // LQ on the panel stream once its rows are updated
           if (!lookahead) return 0;
-          BR_CHECK(handoff());
-          BR_CHECK(lq(ws.panel, ws.sk_panel, k, bq));
-          ev_lq = mark_panel();
+          cudaStream_t ps = ws.pstream(jr);
+          BR_CHECK(handoff(ps));
+          BR_CHECK(lq(ps, ws.sk_panel, k, bq));
+          ev_lq = mark_panel(ps);
           return 0;
         };
         if (chunked) {
@@ -584,14 +590,16 @@ int band_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int f
     MatView P(Aat(t.k + w, t.k), lda, i, t.bp);
     MatView Y(Yu[par], m, i, t.bp), T(Tu[par], b, t.bp, t.bp), W(Wu[par], m, i, t.bp);
     TimeScope ts(ws, st, TC_PANEL, panel_flops(i, t.bp), "qr", t.k);
-    BR_CHECK(panel_qr(st, sk, ws.pscratch, P, Y, tauu[par], T, &W, panel_cap(i), &ws));
+    Scratch s = ws.pscratch_for(sk, i);
+    BR_CHECK(panel_qr(st, s, ws.pscratch, P, Y, tauu[par], T, &W, panel_cap(i), &ws));
     return store_factors(ws, st, 0, t.k, t.k + w, i, t.bp, Yu[par], m, Tu[par], b, tauu[par]);
   };
   auto lq = [&](cudaStream_t st, Scratch& sk, const It& t, int par) -> int {
     MatView P(Aat(t.k, t.k + w), lda, t.jr, t.bq, true);  // transposed view of the bq x jr rows
     MatView Y(Yv[par], n, t.jr, t.bq), T(Tv[par], b, t.bq, t.bq), W(Wv[par], n, t.jr, t.bq);
     TimeScope ts(ws, st, TC_PANEL, panel_flops(t.jr, t.bq), "lq", t.k);
-    BR_CHECK(panel_qr(st, sk, ws.pscratch, P, Y, tauv[par], T, &W, panel_cap(t.jr), &ws));
+    Scratch s = ws.pscratch_for(sk, t.jr);
+    BR_CHECK(panel_qr(st, s, ws.pscratch, P, Y, tauv[par], T, &W, panel_cap(t.jr), &ws));
     return store_factors(ws, st, 1, t.k, t.k + w, t.jr, t.bq, Yv[par], n, Tv[par], b, tauv[par]);
   };
   auto panels = [&](cudaStream_t st, Scratch& sk, const It& t, int par) -> int {
@@ -672,12 +680,13 @@ int band_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int f
       return ul(r0, r1, b1w + c0, b1w + c1);
     };
     auto issue_next = [&]() -> int {  // both next panels on the panel stream
+      cudaStream_t ps = ws.pstream(m - tn.k - w);
       cudaEvent_t ev = ws_event(ws);
       BR_CUDA(cudaEventRecord(ev, ws.main));
-      BR_CUDA(cudaStreamWaitEvent(ws.panel, ev, 0));
-      BR_CHECK(panels(ws.panel, ws.sk_panel, tn, par ^ 1));
+      BR_CUDA(cudaStreamWaitEvent(ps, ev, 0));
+      BR_CHECK(panels(ps, ws.sk_panel, tn, par ^ 1));
       ev_panels = ws_event(ws);
-      BR_CUDA(cudaEventRecord(ev_panels, ws.panel));
+      BR_CUDA(cudaEventRecord(ev_panels, ps));
       return 0;
     };
 
