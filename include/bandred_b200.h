@@ -155,6 +155,23 @@ int br_symm_lower(br_handle_t h, int64_t j, int64_t b, const double* A2, int64_t
 int br_syr2k_lower(br_handle_t h, int64_t j, int64_t b, double* A2, int64_t lda,
                    const double* X3, int64_t ldx, const double* Y, int64_t ldy, int64_t c0,
                    int64_t c1);
+/* Distributed SEVP (SURVEY 8(e), 1D block-cyclic columns; the multi-rank
+ * form of symm_lower / syr2k_lower, kernels.py:312-378). L is one rank's
+ * owned trailing block columns as a j x ncols slab: local column c is column
+ * r0 + (c / bs) * stride + c % bs of the j x j trailing matrix A2 (stride =
+ * world * bs), stored from that row down with ZEROS above (the rank keeps
+ * its strict upper triangle zero). */
+/* Rows [p0, p1) of this slab's share of X1 = sym(A2) W (overwritten; j x b):
+ * the sum over the ranks' slabs (an all-reduce) is sym(A2) W. The range must
+ * not split an owned block (chunked all-reduce: compute a row chunk, reduce
+ * it while the next chunk computes). */
+int br_symm_lower_cyclic(br_handle_t h, int64_t j, int64_t ncols, int64_t b, const double* L,
+                         int64_t ldl, const double* W, int64_t ldw, double* X1, int64_t ldx,
+                         int64_t r0, int64_t bs, int64_t stride, int64_t p0, int64_t p1);
+/* L += X3 Y^T + Y X3^T at the slab's columns, lower triangle of A2 only. */
+int br_syr2k_lower_cyclic(br_handle_t h, int64_t j, int64_t ncols, int64_t b, double* L,
+                          int64_t ldl, const double* X3, int64_t ldx, const double* Y, int64_t ldy,
+                          int64_t r0, int64_t bs, int64_t stride);
 /* sym_two_sided_update (kernels.py:381-401): A2 := Q^T A2 Q, lower only. */
 int br_sym_two_sided_update(br_handle_t h, int64_t j, int64_t b, double* A2, int64_t lda,
                             const double* Y, int64_t ldy, const double* W, int64_t ldw);

@@ -801,6 +801,58 @@ int br_syr2k_lower(br_handle_t h, int64_t j, int64_t b, double* A2, int64_t lda,
                      MatView((double*)Y, ldy, j, b), c0, c1);
 }
 
+// Block-cyclic slab kernels of the distributed SEVP (dist.py):
+// the rank's owned trailing block columns as ONE j x ncols slab, local column
+// c = trailing column r0 + (c / bs) * stride + c % bs, zeros above it.
+int br_symm_lower_cyclic(br_handle_t h, int64_t j, int64_t ncols, int64_t b, const double* L,
+                         int64_t ldl, const double* W, int64_t ldw, double* X1, int64_t ldx,
+                         int64_t r0, int64_t bs, int64_t stride, int64_t p0, int64_t p1) {
+  ARG(h != nullptr, 1);
+  ARG(j >= 0, 2);
+  ARG(ncols >= 0, 3);
+  ARG(b >= 0, 4);
+  ARG(L || ncols == 0, 5);
+  ARG(ldl >= std::max<int64_t>(j, 1), 6);
+  ARG(W && ldw >= std::max<int64_t>(j, 1), 8);
+  ARG(X1 && ldx >= std::max<int64_t>(j, 1), 10);
+  ARG(r0 >= 0, 11);
+  ARG(bs >= 1 && (ncols % bs) == 0, 12);
+  ARG(stride >= bs, 13);
+  ARG(0 <= p0 && p0 <= p1 && p1 <= j, 14);
+  DEV(h);
+  if (j == 0 || b == 0) return 0;
+  Workspace& ws = h->ws;
+  BR_CHECK(ensure_scratch(ws, 4 * std::max(j, ncols) * b + (1 << 20), 1 << 20, panel_scratch_doubles(1)));
+  DevBuf& tmp = cur_tmp(ws);
+  BR_CHECK(devbuf_reserve(tmp, 2 * std::max<int64_t>(ncols, 1) * b));
+  return symm_cyclic(cur_stream(ws), cur_sk(ws), MatView(X1, ldx, j, b),
+                     MatView((double*)L, ldl, j, ncols), MatView((double*)W, ldw, j, b),
+                     CycCols{r0, (int)bs, (int)stride}, tmp.p, p0, p1);
+}
+
+int br_syr2k_lower_cyclic(br_handle_t h, int64_t j, int64_t ncols, int64_t b, double* L,
+                          int64_t ldl, const double* X3, int64_t ldx, const double* Y, int64_t ldy,
+                          int64_t r0, int64_t bs, int64_t stride) {
+  ARG(h != nullptr, 1);
+  ARG(j >= 0, 2);
+  ARG(ncols >= 0, 3);
+  ARG(b >= 0, 4);
+  ARG(L || ncols == 0, 5);
+  ARG(ldl >= std::max<int64_t>(j, 1), 6);
+  ARG(X3 && ldx >= std::max<int64_t>(j, 1), 8);
+  ARG(Y && ldy >= std::max<int64_t>(j, 1), 10);
+  ARG(r0 >= 0, 11);
+  ARG(bs >= 1 && (ncols % bs) == 0, 12);
+  ARG(stride >= bs, 13);
+  DEV(h);
+  if (j == 0 || b == 0 || ncols == 0) return 0;
+  Workspace& ws = h->ws;
+  DevBuf& tmp = cur_tmp(ws);
+  BR_CHECK(devbuf_reserve(tmp, 2 * ncols * b));
+  return syr2k_cyclic(cur_stream(ws), MatView(L, ldl, j, ncols), MatView((double*)X3, ldx, j, b),
+                      MatView((double*)Y, ldy, j, b), CycCols{r0, (int)bs, (int)stride}, tmp.p);
+}
+
 int br_stream_select(br_handle_t h, int which) {
   ARG(h != nullptr, 1);
   ARG(which == 0 || which == 1, 2);

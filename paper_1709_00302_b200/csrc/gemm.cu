@@ -356,6 +356,163 @@ int syr2k_lower(cudaStream_t st, MatView A2, MatView X3, MatView Y, int64_t c0, 
   return launch_tile(cfg, A_N, B_T, EPI_LOWER, st, g, grid);
 }
 
+// ---------------------------------------------------------------------------
+// Block-cyclic column slabs (the distributed SEVP, dist.py)
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ int64_t cyc_col(const CycCols& m, int64_t c) {
+  const int64_t q = c / m.bs;
+  return m.r0 + q * m.stride + (c - q * m.bs);
+}
+
+// Rows of s0 / s1 (j x b) at the slab's columns -> d0 / d1 (ncols x b).
+__global__ void cyc_gather_kernel(int64_t ncols, int64_t b, CycCols m, const double* s0,
+                                  int64_t lds0, double* d0, int64_t ldd0, const double* s1,
+                                  int64_t lds1, double* d1, int64_t ldd1) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t total = ncols * b;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = idx % ncols, q = idx / ncols, r = cyc_col(m, c);
+    d0[c + q * ldd0] = s0[r + q * lds0];
+    if (s1) d1[c + q * ldd1] = s1[r + q * lds1];
+  }
+}
+
+// X1[map(c), q] += Xo[c, q] - L[map(c), c] Wown[c, q]: the slab's transposed
+// contributions land on its own rows (the map is one-to-one), without the
+// diagonal the first product already counted.
+__global__ void cyc_fold_kernel(int64_t ncols, int64_t b, CycCols m, const double* Xo, int64_t ldxo,
+                                const double* L, int64_t ldl, const double* Wown, int64_t ldwo,
+                                double* X1, int64_t ldx1) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t total = ncols * b;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = idx % ncols, q = idx / ncols, r = cyc_col(m, c);
+    X1[r + q * ldx1] += Xo[c + q * ldxo] - L[r + c * ldl] * Wown[c + q * ldwo];
+  }
+}
+
+static int cyc_check(const char* who, MatView L, int64_t b, CycCols m) {
+  const int64_t j = L.rows, nc = L.cols;
+  if (L.trans || m.bs < 1 || m.stride < m.bs || m.r0 < 0 || nc % m.bs != 0 ||
+      (nc > 0 && cyc_col(m, nc - 1) >= j) || b < 1) {
+    set_error("%s: bad block-cyclic slab (j %lld, ncols %lld, r0 %lld, bs %d, stride %d)", who,
+              (long long)j, (long long)nc, (long long)m.r0, m.bs, m.stride);
+    return -1;
+  }
+  return 0;
+}
+
+static int cyc_gather(cudaStream_t st, int64_t ncols, int64_t b, CycCols m, MatView s0, double* d0,
+                      const MatView* s1, double* d1) {
+  const int64_t total = ncols * b;
+  const int blocks = (int)std::min<int64_t>(cdiv(total, 256), 148 * 8);
+  count_launch();
+  BR_CUDA(launch_pdl(cyc_gather_kernel, dim3(blocks), dim3(256), 0, st, ncols, b, m,
+                     (const double*)s0.p, s0.ld, d0, ncols, s1 ? (const double*)s1->p : nullptr,
+                     s1 ? s1->ld : (int64_t)0, d1, ncols));
+  return 0;
+}
+
+int symm_cyclic(cudaStream_t st, Scratch& ws, MatView X1, MatView L, MatView W, CycCols m,
+                double* tmp, int64_t p0, int64_t p1) {
+  const int64_t j = L.rows, nc = L.cols, b = W.cols;
+  BR_CHECK(cyc_check("symm_cyclic", L, b, m));
+  if (X1.trans || W.trans || X1.rows != j || W.rows != j || X1.cols != b || p0 < 0 || p1 > j ||
+      p0 > p1) {
+    set_error("symm_cyclic: bad views / row range");
+    return -1;
+  }
+  if (p0 == p1) return 0;
+  MatView Xr = X1.sub(p0, 0, p1 - p0, b);
+  if (nc == 0) return gemm(st, ws, Xr, MatView(nullptr, 1, p1 - p0, 0), MatView(nullptr, 1, 0, b), 1.0, 0.0);
+  GemmArgs cg{};
+  cg.cyc_r0 = m.r0;
+  cg.cyc_bs = m.bs;
+  cg.cyc_stride = m.stride;
+  // columns whose first stored row lies in [p0, p1): their transposed
+  // contributions belong to these rows; whole owned blocks only
+  const int64_t ca = cyc_count(cg, p0 - 1), cb = cyc_count(cg, p1 - 1);
+  if (ca % m.bs || cb % m.bs) {
+    set_error("symm_cyclic: row range [%lld, %lld) splits an owned block", (long long)p0, (long long)p1);
+    return -1;
+  }
+  MatView Wown(tmp, nc, nc, b), Xo(tmp + nc * b, nc, nc, b);
+  BR_CHECK(cyc_gather(st, nc, b, m, W, Wown.p, nullptr, nullptr));
+  GemmArgs g;
+  int am = 0;
+  bool bt = false;
+  // X1[p0:p1] = L[p0:p1] Wown (K clipped to the columns that reach a tile's rows)
+  BR_CHECK(make_args(Xr, L.sub(p0, 0, p1 - p0, nc), Wown, 1.0, 0.0, nullptr, g, am, bt));
+  g.cyc_r0 = m.r0 - p0;
+  g.cyc_bs = m.bs;
+  g.cyc_stride = m.stride;
+  BR_CHECK(run_gemm(am, st, ws, g, bt, 0, 0));
+  if (cb == ca) return 0;
+  // Xo = L[:, ca:cb]^T W (K from each column's first stored row)
+  const CycCols ms{cyc_map(cg, ca), m.bs, m.stride};
+  MatView Ls = L.sub(0, ca, j, cb - ca), Xos = Xo.sub(ca, 0, cb - ca, b);
+  BR_CHECK(make_args(Xos, Ls.T(), W, 1.0, 0.0, nullptr, g, am, bt));
+  g.cyc_r0 = ms.r0;
+  g.cyc_bs = ms.bs;
+  g.cyc_stride = ms.stride;
+  BR_CHECK(run_gemm(am, st, ws, g, bt, 0, 0));
+  const int64_t total = (cb - ca) * b;
+  const int blocks = (int)std::min<int64_t>(cdiv(total, 256), 148 * 8);
+  count_launch();
+  BR_CUDA(launch_pdl(cyc_fold_kernel, dim3(blocks), dim3(256), 0, st, cb - ca, b, ms,
+                     (const double*)Xos.p, Xos.ld, (const double*)Ls.p, Ls.ld,
+                     (const double*)(Wown.p + ca), Wown.ld, X1.p, X1.ld));
+  return 0;
+}
+
+int syr2k_cyclic(cudaStream_t st, MatView L, MatView X3, MatView Y, CycCols m, double* tmp) {
+  const int64_t j = L.rows, nc = L.cols, b = X3.cols;
+  BR_CHECK(cyc_check("syr2k_cyclic", L, b, m));
+  if (X3.trans || Y.trans || X3.rows != j || Y.rows != j || Y.cols != b) {
+    set_error("syr2k_cyclic: bad views");
+    return -1;
+  }
+  if (nc == 0) return 0;
+  double* Yo = tmp;
+  double* Xo = tmp + nc * b;
+  BR_CHECK(cyc_gather(st, nc, b, m, Y, Yo, &X3, Xo));
+  GemmArgs g{};
+  g.M = j;
+  g.N = nc;
+  g.K = 2 * b;
+  // A_op = [X3 | Y] (trailing rows), B_op(k, c) = [Y | X3](map(c), k) gathered
+  g.A = X3.p;
+  g.lda = X3.ld;
+  g.A2 = Y.p;
+  g.lda2 = Y.ld;
+  g.ksplitA = b;
+  g.B = Yo;
+  g.ldb = nc;
+  g.B2 = Xo;
+  g.ldb2 = nc;
+  g.ksplitB = b;
+  g.C = L.p;
+  g.ldc = L.ld;
+  g.Cin = L.p;
+  g.ldcin = L.ld;
+  g.alpha = 1.0;
+  g.beta = 1.0;
+  g.c0 = 0;
+  g.c1 = nc;
+  g.cyc_r0 = m.r0;
+  g.cyc_bs = m.bs;
+  g.cyc_stride = m.stride;
+  g.vecA = al16(X3.p, X3.ld) && al16(Y.p, Y.ld) && (m.r0 % 2 == 0);
+  g.vecB = al16(Yo, nc) && al16(Xo, nc);
+  const int cfg = lower_cfg(j - m.r0);
+  dim3 grid((unsigned)cdiv(j - m.r0, kTiles[cfg].bm), (unsigned)cdiv(nc, kTiles[cfg].bn), 1);
+  return launch_tile(cfg, A_N, B_T, EPI_LOWER, st, g, grid);
+}
+
 // Load every GEMM instantiation and the split-K reduction (see g_preload_only).
 int preload_gemm_kernels() {
   GemmArgs g{};
@@ -372,6 +529,8 @@ int preload_gemm_kernels() {
   cudaFuncAttributes fa;
   BR_CUDA(cudaFuncGetAttributes(&fa, splitk_reduce_kernel));
   BR_CUDA(cudaFuncGetAttributes(&fa, splitk_reduce_tt_kernel));
+  BR_CUDA(cudaFuncGetAttributes(&fa, cyc_gather_kernel));
+  BR_CUDA(cudaFuncGetAttributes(&fa, cyc_fold_kernel));
   return 0;
 }
 

@@ -51,7 +51,29 @@ struct GemmArgs {
   int64_t c0, c1;       // EPI_LOWER: rows [c0, M) x cols [c0, c1)
   int vecA, vecB;       // 16-byte cp.async allowed for A / B
   int b_upper;          // B_N with B upper triangular: K range of a tile ends at its last column
+  // Block-cyclic staircase (the distributed SEVP, dist.py): local column c of
+  // a rank's owned block columns is column cyc_r0 + (c / cyc_bs) * cyc_stride
+  // + c % cyc_bs of the j x j trailing matrix, stored from that row down
+  // (zeros above). A_N: the K range of a tile ends at the last local column
+  // that starts at or above its last row; A_T: it starts at the first row of
+  // the tile's first column. EPI_LOWER: C columns are local columns (c0 = 0),
+  // rows run from cyc_r0, and element (r, c) is written iff r >= column c's
+  // global index. cyc_bs == 0: off.
+  int64_t cyc_r0;
+  int cyc_bs, cyc_stride;
 };
+
+// Global column (= first stored row) of local column c under the map.
+__host__ __device__ __forceinline__ int64_t cyc_map(const GemmArgs& g, int64_t c) {
+  const int64_t q = c / g.cyc_bs;
+  return g.cyc_r0 + q * g.cyc_stride + (c - q * g.cyc_bs);
+}
+// Number of local columns whose first stored row is <= r.
+__host__ __device__ __forceinline__ int64_t cyc_count(const GemmArgs& g, int64_t r) {
+  if (r < g.cyc_r0) return 0;
+  const int64_t d = r - g.cyc_r0, q = d / g.cyc_stride, rem = d - q * g.cyc_stride;
+  return q * g.cyc_bs + (rem + 1 < g.cyc_bs ? rem + 1 : g.cyc_bs);
+}
 
 // Host-side launch helpers (gemm.cu). All return 0 or a positive CUDA error.
 // C = alpha*op(A)*op(B) + beta*Cin (Cin defaults to C). Views carry the
@@ -73,5 +95,22 @@ int symm_lower(cudaStream_t st, Scratch& ws, MatView X1, MatView A2, MatView W,
 // A2[:, c0:c1] += X3*Y^T + Y*X3^T, lower triangle only.
 int syr2k_lower(cudaStream_t st, MatView A2, MatView X3, MatView Y, int64_t c0, int64_t c1,
                 int max_ctas = 0);
+
+// Block-cyclic column slab of a j x j lower-stored trailing matrix (the
+// distributed SEVP): L is j x ncols, local column c being trailing column
+// r0 + (c / bs) * stride + c % bs, stored from that row down with zeros above.
+struct CycCols {
+  int64_t r0;
+  int bs, stride;
+};
+// Rows [p0, p1) of this slab's share of X1 = sym(A2) W (all other entries of
+// A2 belong to other ranks): X1 = L Wown + fold(L^T W - diag(L) Wown), Wown
+// the rows of W at the slab's columns, fold placing column c's row at row
+// map(c); summed over a partition of A2's columns it is sym(A2) W. [p0, p1)
+// must not split an owned block. tmp: 2 * ncols * b doubles.
+int symm_cyclic(cudaStream_t st, Scratch& ws, MatView X1, MatView L, MatView W, CycCols m,
+                double* tmp, int64_t p0, int64_t p1);
+// L += lower part of X3 Y^T + Y X3^T at the slab's columns (tmp: 2 * ncols * b).
+int syr2k_cyclic(cudaStream_t st, MatView L, MatView X3, MatView Y, CycCols m, double* tmp);
 
 }  // namespace br

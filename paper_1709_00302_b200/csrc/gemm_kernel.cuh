@@ -143,10 +143,11 @@ __device__ __forceinline__ void dgemm_tile(const GemmArgs& g, const unsigned bx,
   const int wm = (warp % WM) * WTM, wn = (warp / WM) * WTN;
 
   int64_t m0, n0, kbeg, kend;
+  const bool cyc = g.cyc_bs != 0;
   if (EPI == EPI_LOWER) {
-    if (bx < by) return;
-    m0 = g.c0 + (int64_t)bx * BM;
+    m0 = (cyc ? g.cyc_r0 : g.c0) + (int64_t)bx * BM;
     n0 = g.c0 + (int64_t)by * BN;
+    if (cyc ? (m0 + BM <= cyc_map(g, n0)) : (bx < by)) return;  // tile above the diagonal
     kbeg = 0;
     kend = g.K;
   } else {
@@ -155,6 +156,10 @@ __device__ __forceinline__ void dgemm_tile(const GemmArgs& g, const unsigned bx,
     kbeg = (int64_t)bz * g.k_per_split;
     kend = min(g.K, kbeg + g.k_per_split);
     if (BMD == B_N && g.b_upper) kend = max(kbeg, min(kend, n0 + BN));  // rows > n of B are 0
+    if (cyc) {  // block-cyclic staircase operand: skip its all-zero K range
+      if (AM == A_N) kend = max(kbeg, min(kend, cyc_count(g, m0 + BM - 1)));
+      else if (AM == A_T) kbeg = min(kend, max(kbeg, cyc_map(g, m0) & ~(int64_t)1));
+    }
   }
   const int64_t nmax = (EPI == EPI_LOWER) ? g.c1 : g.N;
   pdl_wait();  // inputs written by the previous kernel in the stream
@@ -178,7 +183,7 @@ __device__ __forceinline__ void dgemm_tile(const GemmArgs& g, const unsigned bx,
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int64_t c = n0 + wn + j * 8 + 2 * tq + h;
-          const bool ok = r < g.M && c < nmax && (EPI != EPI_LOWER || r >= c);
+          const bool ok = r < g.M && c < nmax && (EPI != EPI_LOWER || r >= (cyc ? cyc_map(g, c) : c));
           if (ok) acc[i][j][h] = (EPI == EPI_LOWER || g.beta == 1.0)
                                      ? g.Cin[r + c * g.ldcin]
                                      : g.beta * g.Cin[r + c * g.ldcin];
@@ -366,7 +371,7 @@ __device__ __forceinline__ void dgemm_tile(const GemmArgs& g, const unsigned bx,
         } else if (EPI == EPI_SPLIT) {
           g.ws[((int64_t)bz * g.N + c) * g.M + r] = v;
         } else {
-          if (r >= c) g.C[r + c * g.ldc] = v;
+          if (r >= (cyc ? cyc_map(g, c) : c)) g.C[r + c * g.ldc] = v;
         }
       }
     }

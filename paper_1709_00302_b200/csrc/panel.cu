@@ -60,8 +60,12 @@ struct LeafArgs {
 namespace br {
 
 // Rows one cluster holds at leaf width nb: 16 CTAs x 256 threads x R rows
-// with R * NB = 64 register doubles per thread.
-static int leaf_rows_per_thread(int nb) { return nb > 32 ? 1 : (nb > 16 ? 2 : (nb > 8 ? 4 : 8)); }
+// with R * NB = 64 register doubles per thread. The 4- and 2-wide leaves
+// exist for panels taller than 32768 rows (SEVP n > 32768 + w, SVD m > 32768:
+// 65536 / 131072 rows per cluster; an n = 131072 fp64 matrix is 137 GB).
+static int leaf_rows_per_thread(int nb) {
+  return nb > 32 ? 1 : (nb > 16 ? 2 : (nb > 8 ? 4 : (nb > 4 ? 8 : (nb > 2 ? 16 : 32))));
+}
 // 64-wide leaves (8 column-group warps, <= 4096 rows): opt-in with
 // BR_LEAF64=1. Measured slower than two 32-wide leaves plus their block update
 // (4096 x 256 panel 760 vs 686 us): two warps per SM sub-partition lengthen
@@ -91,7 +95,7 @@ static int64_t leaf_capacity(int nb) {
 // Leaf width for a j x b panel: the widest of {32, 16, 8} (or b if narrower)
 // whose L rows fit one cluster.
 static int leaf_width(int64_t L, int64_t b) {
-  const int cand[4] = {64, 32, 16, 8};
+  const int cand[6] = {64, 32, 16, 8, 4, 2};
   for (int nb : cand) {
     if (nb == 64 && (b <= 32 || !leaf64_enabled())) continue;
     const int use = (int)std::min<int64_t>(nb, b);
@@ -275,8 +279,18 @@ static int launch_leaf(cudaStream_t st, MatView P, MatView Y, double* tau, doubl
     if (L <= (int64_t)LEAF_MAXC * 128 * 4) return launch_leaf_t<16, 4, 128>(st, a);
     return launch_leaf_t<16, 4, 256>(st, a);
   }
-  if (L <= (int64_t)LEAF_MAXC * 128 * 8) return launch_leaf_t<8, 8, 128>(st, a);
-  return launch_leaf_t<8, 8, 256>(st, a);
+  if (nb > 4 || L <= (int64_t)LEAF_MAXC * 256 * 8) {
+    if (L <= (int64_t)LEAF_MAXC * 128 * 8) return launch_leaf_t<8, 8, 128>(st, a);
+    return launch_leaf_t<8, 8, 256>(st, a);
+  }
+  // panels taller than 32768 rows: narrower leaves, more rows per thread (the
+  // W epilogue of these leaves is not formed in the kernel: panel_qr builds W)
+  if (a.W) {
+    set_error("narrow leaf (nb = %d) cannot form W", nb);
+    return -1;
+  }
+  if (nb > 2) return launch_leaf_t<4, 16, 256>(st, a);
+  return launch_leaf_t<2, 32, 256>(st, a);
 }
 
 }  // namespace br
@@ -570,11 +584,17 @@ int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView 
   const int nbl = leaf_width(j, b);
   if (nbl < 1) {
     set_error("panel_qr: %lld rows exceed one cluster's register capacity (%lld)", (long long)j,
-              (long long)leaf_capacity(8));
+              (long long)leaf_capacity(2));
     return -1;
   }
   if (b <= nbl) {
-    // single leaf: Y, tau, T and W in one kernel
+    // single leaf: Y, tau, T and W in one kernel (narrow leaves: W by a GEMM)
+    if (nbl < 8) {
+      BR_CHECK(zero_fill(st, T));
+      BR_CHECK(launch_leaf(st, P, Y, tau, T.p, T.ld, nullptr));
+      if (W) BR_CHECK(gemm(st, ws, *W, Y, T, 1.0, 0.0, nullptr, max_ctas, 0, true));
+      return mark(0, b);
+    }
     BR_CHECK(launch_leaf(st, P, Y, tau, T.p, T.ld, W));
     return mark(0, b);
   }
@@ -629,7 +649,7 @@ int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView 
       const int64_t w = e - s;
       MatView leafP = P.sub(s, s, j - s, w);
       MatView leafY = Y.sub(s, s, j - s, w);
-      if (e < c1 && W && leaf_w_mode()) {
+      if (e < c1 && W && leaf_w_mode() && nbl >= 8) {
         // P[s:, e:c1] += (Y_blk T_blk^T)(Y_blk^T P[s:, e:c1]); the leaf writes
         // Y_blk T_blk^T into W's columns (W itself is formed at the end)
         MatView What = W->sub(s, s, j - s, w);
@@ -743,6 +763,8 @@ int preload_panel_kernels() {
   BR_CHECK((launch_leaf_t<16, 4, 256>(0, a)));
   BR_CHECK((launch_leaf_t<8, 8, 128>(0, a)));
   BR_CHECK((launch_leaf_t<8, 8, 256>(0, a)));
+  BR_CHECK((launch_leaf_t<4, 16, 256>(0, a)));
+  BR_CHECK((launch_leaf_t<2, 32, 256>(0, a)));
   BR_CHECK((launch_leaf2_t<64, 8>(0, a)));
   BR_CHECK((launch_leaf2_t<8, 8>(0, a)));
   BR_CHECK((launch_leaf2_t<32, 4>(0, a)));

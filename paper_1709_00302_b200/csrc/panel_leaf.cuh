@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(LT, 1) leaf_reg_kernel(const LeafArgs a) {
     BR_PHASE(9);
     // ---- W = Y T on the tensor cores: each warp 4 independent 8-row slabs
     // at a time x NB columns ----
-    if (Wo) {
+    if constexpr (NB >= 8) if (Wo) {  // (the narrow tall-panel leaves never form W)
       const int gq = lane >> 2, tq = lane & 3;
       constexpr int U = 4;
       for (int rb = warp * 8; rb < ROWS; rb += LW * 8 * U) {

@@ -636,3 +636,54 @@ def test_set_option_validation(br):
     assert lib.br_set_option(h, 99, 1) == -2
     assert lib.br_set_option(h, _lib.BR_OPT_MAX_ITERS, -1) == -3
     assert lib.br_set_option(None, _lib.BR_OPT_MAX_ITERS, 0) == -1
+
+
+# --- panels taller than one cluster's 8-wide capacity (32768 rows) -------------
+# 4-wide (<= 65536 rows) and 2-wide (<= 131072 rows) leaves with right-looking
+# block updates; W by a GEMM (SEVP n > 32768 + w, SVD m > 32768).
+
+@pytest.mark.parametrize("j,b,seed", [(40000, 8, 11), (70000, 4, 12), (36000, 40, 13)])
+def test_qr_panel_tall_vs_oracle(br, j, b, seed):
+    P0 = rand(j, b, seed)
+    Pg, Po = P0.copy(order="F"), P0.copy(order="F")
+    f = br.qr_panel(Pg)
+    Y, T, W, R, tau = O.qr_panel(Po)
+    assert np.array_equal(np.sign(np.diag(f.r_or_l)), np.sign(np.diag(R)))
+    assert rel(f.r_or_l, R, np.linalg.norm(P0)) <= 1e-13
+    assert rel(f.y, Y, np.linalg.norm(Y)) <= 1e-12
+    assert rel(f.t, T, np.linalg.norm(T)) <= 1e-12
+    assert rel(f.w, W, np.linalg.norm(W)) <= 1e-12
+    assert rel(f.tau, tau, np.linalg.norm(tau)) <= 1e-13
+
+
+def test_qr_panel_tall_zero_column(br):
+    """tau = 0 / identity reflector for an exact zero column in a 4-wide leaf."""
+    P0 = rand(40000, 6, 14)
+    P0[:, 2] = 0.0
+    Pg, Po = P0.copy(order="F"), P0.copy(order="F")
+    f = br.qr_panel(Pg)
+    Y, T, W, R, tau = O.qr_panel(Po)
+    assert f.tau[2] == 0.0 and tau[2] == 0.0
+    assert rel(f.r_or_l, R, np.linalg.norm(P0)) <= 1e-13
+    assert rel(f.w, W, np.linalg.norm(W)) <= 1e-12
+
+
+@pytest.mark.parametrize("m,n", [(40000, 72), (72, 40000)])
+def test_tri_band_tall_vs_oracle(br, m, n):
+    """Triangular band with QR (m > n) or, through the transpose, LQ-side
+    panels taller than 32768 rows."""
+    A = rand(m, n, 15)
+    res = br.reduce_tri_band(A, 16, 16)
+    band, lo, up, it = O.reduce_tri_band(A, 16, 16)
+    assert res.iterations == it
+    assert (res.lower_bw, res.upper_bw) == (lo, up)
+    assert br.band_check(res.band, lo, up) == 0.0
+    assert rel(res.band, band, np.linalg.norm(A)) <= 1e-12 * np.sqrt(max(m, n))
+
+
+def test_band_svd_tall_vs_oracle(br):
+    A = rand(40000, 64, 16)
+    res = br.reduce_band_svd(A, br.SvdConfig(40000, 64, 16, 16, variant=br.SvdVariant.V2))
+    band, _, _, _ = O.reduce_band_svd(A, 16, 16, simultaneous=True)
+    assert br.band_check(res.band, 16, 16) == 0.0
+    assert rel(res.band, band, np.linalg.norm(A)) <= 1e-12 * np.sqrt(40000)
