@@ -451,9 +451,9 @@ def run_dist(args, rank, world, local_rank):
     peak = dgemm_peak(dev)
     lay = D.Layout(n, b, world, rank)
     ops = D.CudaOps(local_rank, torch)
-    comm = D.TorchComm(dist)
+    comm = D.TorchComm(dist, stream=torch.cuda.Stream(device=dev, priority=-1))
     A_host = make_input(args.config)
-    L0 = D.scatter_columns(A_host, lay, ops)
+    L0 = D.scatter_columns(A_host, lay, ops, kind)
     L = ops.alloc(n, lay.ncols_local)
     la = args.lookahead
     fn = D.reduce_sym_band_dist if kind == "sevp" else D.reduce_tri_band_dist
@@ -488,7 +488,7 @@ def run_dist(args, rank, world, local_rank):
     t0 = time.perf_counter()
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
     for _ in range(e2e_steps):
-        Lh = D.scatter_columns(A_host, lay, ops)
+        Lh = D.scatter_columns(A_host, lay, ops, kind)
         fn(Lh, lay, w, ops, comm, la)
         D.gather_band(Lh, lay, w, kind, comm, torch)
     torch.cuda.synchronize(dev)
@@ -504,8 +504,8 @@ def run_dist(args, rank, world, local_rank):
             "config": same_config(args.config, la, world),
             "clocks": clocks.summary(),
             "e2e": {"value": flops / e2e_s / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": n * n * 8,
-                    "d2h_bytes_per_step": n * n * 8, "steps": e2e_steps,
-                    "path": "scatter owned columns + distributed reduction + band gather to rank 0"},
+                    "d2h_bytes_per_step": lay.nblk * b * (b + w) * 8, "steps": e2e_steps,
+                    "path": "scatter owned columns + distributed reduction + band strips gathered to rank 0"},
             "gpu_launches": int(launches),
             "roofline": {"bound": "tensor", "kernel": "all", "achieved": value / 1e3 / world,
                          "peak": peak, "unit": "TFLOP/s", "frac": value / 1e3 / world / peak,
@@ -531,6 +531,8 @@ def main():
                     help="eager steps timed per kernel class for the roofline")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dist", action="store_true",
+                    help="run the multi-GPU (block-cyclic, NCCL) driver even at one rank")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -539,7 +541,12 @@ def main():
         sys.exit("the band-form workload is single-GPU, ours only")
     if args.impl == "reference":
         run_reference(args, rank, world)
-    elif world > 1:
+    elif world > 1 or args.dist:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29511")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         run_dist(args, rank, world, local_rank)
     else:
         run_ours(args, rank, world, local_rank)

@@ -161,10 +161,10 @@ int br_syr2k_lower(br_handle_t h, int64_t j, int64_t b, double* A2, int64_t lda,
  * r0 + (c / bs) * stride + c % bs of the j x j trailing matrix A2 (stride =
  * world * bs), stored from that row down with ZEROS above (the rank keeps
  * its strict upper triangle zero). */
-/* Rows [p0, p1) of this slab's share of X1 = sym(A2) W (overwritten; j x b):
- * the sum over the ranks' slabs (an all-reduce) is sym(A2) W. The range must
- * not split an owned block (chunked all-reduce: compute a row chunk, reduce
- * it while the next chunk computes). */
+/* Rows [p0, p1) of this slab's share of X1 = sym(A2) W into X1 ((p1 - p0) x
+ * b, overwritten): the sum over the ranks' slabs (an all-reduce) is
+ * sym(A2) W. The range must not split an owned block (chunked all-reduce:
+ * compute a row chunk, reduce it while the next chunk computes). */
 int br_symm_lower_cyclic(br_handle_t h, int64_t j, int64_t ncols, int64_t b, const double* L,
                          int64_t ldl, const double* W, int64_t ldw, double* X1, int64_t ldx,
                          int64_t r0, int64_t bs, int64_t stride, int64_t p0, int64_t p1);

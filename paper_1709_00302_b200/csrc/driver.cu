@@ -814,18 +814,18 @@ int br_symm_lower_cyclic(br_handle_t h, int64_t j, int64_t ncols, int64_t b, con
   ARG(L || ncols == 0, 5);
   ARG(ldl >= std::max<int64_t>(j, 1), 6);
   ARG(W && ldw >= std::max<int64_t>(j, 1), 8);
-  ARG(X1 && ldx >= std::max<int64_t>(j, 1), 10);
+  ARG(0 <= p0 && p0 <= p1 && p1 <= j, 14);
+  ARG(X1 && ldx >= std::max<int64_t>(p1 - p0, 1), 10);
   ARG(r0 >= 0, 11);
   ARG(bs >= 1 && (ncols % bs) == 0, 12);
   ARG(stride >= bs, 13);
-  ARG(0 <= p0 && p0 <= p1 && p1 <= j, 14);
   DEV(h);
   if (j == 0 || b == 0) return 0;
   Workspace& ws = h->ws;
   BR_CHECK(ensure_scratch(ws, 4 * std::max(j, ncols) * b + (1 << 20), 1 << 20, panel_scratch_doubles(1)));
   DevBuf& tmp = cur_tmp(ws);
   BR_CHECK(devbuf_reserve(tmp, 2 * std::max<int64_t>(ncols, 1) * b));
-  return symm_cyclic(cur_stream(ws), cur_sk(ws), MatView(X1, ldx, j, b),
+  return symm_cyclic(cur_stream(ws), cur_sk(ws), MatView(X1, ldx, p1 - p0, b),
                      MatView((double*)L, ldl, j, ncols), MatView((double*)W, ldw, j, b),
                      CycCols{r0, (int)bs, (int)stride}, tmp.p, p0, p1);
 }

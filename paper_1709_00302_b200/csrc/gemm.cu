@@ -384,14 +384,14 @@ __global__ void cyc_gather_kernel(int64_t ncols, int64_t b, CycCols m, const dou
 // diagonal the first product already counted.
 __global__ void cyc_fold_kernel(int64_t ncols, int64_t b, CycCols m, const double* Xo, int64_t ldxo,
                                 const double* L, int64_t ldl, const double* Wown, int64_t ldwo,
-                                double* X1, int64_t ldx1) {
+                                double* X1, int64_t ldx1, int64_t roff) {
   pdl_wait();
   pdl_trigger();
   const int64_t total = ncols * b;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = idx % ncols, q = idx / ncols, r = cyc_col(m, c);
-    X1[r + q * ldx1] += Xo[c + q * ldxo] - L[r + c * ldl] * Wown[c + q * ldwo];
+    X1[r - roff + q * ldx1] += Xo[c + q * ldxo] - L[r + c * ldl] * Wown[c + q * ldwo];
   }
 }
 
@@ -421,13 +421,13 @@ int symm_cyclic(cudaStream_t st, Scratch& ws, MatView X1, MatView L, MatView W, 
                 double* tmp, int64_t p0, int64_t p1) {
   const int64_t j = L.rows, nc = L.cols, b = W.cols;
   BR_CHECK(cyc_check("symm_cyclic", L, b, m));
-  if (X1.trans || W.trans || X1.rows != j || W.rows != j || X1.cols != b || p0 < 0 || p1 > j ||
-      p0 > p1) {
+  if (X1.trans || W.trans || p0 < 0 || p1 > j || p0 > p1 || X1.rows != p1 - p0 || W.rows != j ||
+      X1.cols != b) {
     set_error("symm_cyclic: bad views / row range");
     return -1;
   }
   if (p0 == p1) return 0;
-  MatView Xr = X1.sub(p0, 0, p1 - p0, b);
+  MatView Xr = X1;
   if (nc == 0) return gemm(st, ws, Xr, MatView(nullptr, 1, p1 - p0, 0), MatView(nullptr, 1, 0, b), 1.0, 0.0);
   GemmArgs cg{};
   cg.cyc_r0 = m.r0;
@@ -465,7 +465,7 @@ int symm_cyclic(cudaStream_t st, Scratch& ws, MatView X1, MatView L, MatView W, 
   count_launch();
   BR_CUDA(launch_pdl(cyc_fold_kernel, dim3(blocks), dim3(256), 0, st, cb - ca, b, ms,
                      (const double*)Xos.p, Xos.ld, (const double*)Ls.p, Ls.ld,
-                     (const double*)(Wown.p + ca), Wown.ld, X1.p, X1.ld));
+                     (const double*)(Wown.p + ca), Wown.ld, X1.p, X1.ld, p0));
   return 0;
 }
 

@@ -103,11 +103,12 @@ struct CycCols {
   int64_t r0;
   int bs, stride;
 };
-// Rows [p0, p1) of this slab's share of X1 = sym(A2) W (all other entries of
-// A2 belong to other ranks): X1 = L Wown + fold(L^T W - diag(L) Wown), Wown
-// the rows of W at the slab's columns, fold placing column c's row at row
-// map(c); summed over a partition of A2's columns it is sym(A2) W. [p0, p1)
-// must not split an owned block. tmp: 2 * ncols * b doubles.
+// Rows [p0, p1) of this slab's share of X1 = sym(A2) W into X1 ((p1 - p0) x
+// b; all other entries of A2 belong to other ranks): X1 = L Wown +
+// fold(L^T W - diag(L) Wown), Wown the rows of W at the slab's columns, fold
+// placing column c's row at row map(c); summed over a partition of A2's
+// columns it is sym(A2) W. [p0, p1) must not split an owned block.
+// tmp: 2 * ncols * b doubles.
 int symm_cyclic(cudaStream_t st, Scratch& ws, MatView X1, MatView L, MatView W, CycCols m,
                 double* tmp, int64_t p0, int64_t p1);
 // L += lower part of X3 Y^T + Y X3^T at the slab's columns (tmp: 2 * ncols * b).

@@ -2,35 +2,42 @@
 
 One process per GPU (torchrun). Block column t (width b) of the n x n matrix
 lives on rank t mod P, stored locally as a column-major n x (b * #owned)
-array. Per iteration k = t*b (w == b, the sharded BASELINE configs):
+array, so a rank's owned trailing block columns are ONE contiguous local
+slab at every iteration. Per iteration k = t*b (w == b, the sharded
+BASELINE configs):
 
 SEVP (ref sevp.py:194-273, look-ahead depth 1 as V2):
   1. the owner of block t factors the panel A[k+b:n, block t] (cluster leaf
-     kernels) and NCCL-broadcasts Y and T; every rank forms W = Y T;
-  2. every rank accumulates its owned block columns' share of
-     X1 = sym(A2) W from lower-stored data only - for block c:
-     X1[c] += sym(A2[c,c]) W[c];  X1[c+1:] += A2[c+1:,c] W[c];
-     X1[c] += A2[c+1:,c]^T W[c+1:] - then all-reduces X1 (the distributed
-     A V product, the path's real exchange step);
+     kernels) and NCCL-broadcasts [Y | T] from one packed buffer; every rank
+     forms W = Y T;
+  2. every rank computes its slab's share of X1 = sym(A2) W with ONE
+     block-cyclic SYMM per row chunk (br_symm_lower_cyclic: X1 = L Wown +
+     fold(L^T W - diag(L) Wown), the slab kept zero above the diagonal), and
+     each chunk is all-reduced on the communication stream while the next
+     chunk computes (the path's real exchange step);
   3. X2 = X1^T W / 2, X3 = X1 + Y X2 on every rank (replicated, small);
-  4. SYR2K on the owned block columns; look-ahead: the owner of block t+1
-     updates that block first and factors the next panel on its panel
-     stream while it finishes the rest.
+  4. ONE block-cyclic SYR2K over the slab (br_syr2k_lower_cyclic); with
+     look-ahead, the owner of block t+1 updates that block first and factors
+     the next panel on its panel stream while it finishes the rest.
 Triangular band (ref svd.py:179-202):
-  1. QR owner factors A[k:m, block t], broadcast Y_U, T_U;
-  2. the left update is local to each owned block column;
-  3. the LQ row panel A[k:k+b, k+b:n] spans all owners: NCCL all-gather of
-     the owned b x b pieces, then every rank factors the same LQ (identical
-     inputs and kernels -> bit-identical factors, no broadcast needed);
-  4. right update: partial Z = D[:, owned] W_V[owned] on every rank,
-     all-reduce(Z), then D[:, owned] += Z Y_V[owned]^T locally;
+  1. QR owner factors A[k:m, block t], broadcasts [Y_U | T_U];
+  2. the left update is local: one GEMM pair over the slab;
+  3. the LQ row panel A[k:k+b, k+b:n] spans all owners: all-gather of the
+     owned b x b pieces into one buffer, then every rank factors the same LQ
+     (identical inputs and kernels -> bit-identical factors, no broadcast);
+  4. right update, pipelined by row chunks: partial Z_c = D[c, slab] W_V[slab]
+     -> all-reduce(Z_c) on the communication stream -> D[c, slab] += Z_c
+     Y_V[slab]^T as soon as chunk c has arrived;
   5. look-ahead: block t+1's owner updates it first and factors QR(t+1) on
      its panel stream.
+The band is gathered to rank 0 only, and only the band strip of every block
+column travels.
 
 The algorithm is written once against two small interfaces so its host
 logic is testable on CPU: `ops` (rank-local dense kernels; `CudaOps` here
 drives the sm_100a library through the C ABI) and `comm` (torch.distributed:
-NCCL for GPUs; the gloo tests plug NumPy ops into the same driver).
+NCCL for GPUs on its own stream; the gloo tests plug NumPy ops into the same
+driver).
 """
 from __future__ import annotations
 
@@ -40,6 +47,8 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
+
+CHUNK_ROWS = 8192  # all-reduce pipeline granularity (rounded to whole blocks)
 
 
 @dataclass
@@ -67,6 +76,14 @@ class Layout:
     def ncols_local(self) -> int:
         return len(self.owned) * self.b
 
+    def owned_after(self, t: int):
+        """(first owned block > t or None, its local slot, how many owned blocks > t)."""
+        first = t + 1 + (self.rank - (t + 1)) % self.world
+        if first >= self.nblk:
+            return None, len(self.owned), 0
+        s0 = self.slot(first)
+        return first, s0, len(self.owned) - s0
+
 
 class CMat:
     """Column-major fp64 matrix on a torch tensor of shape (cols, ld)."""
@@ -86,6 +103,15 @@ class CMat:
         t = f((max(cols, 1), ld), dtype=torch.float64, device=device)
         m = cls(t, rows, cols)
         m.ld = ld
+        return m
+
+    @classmethod
+    def packed(cls, flat, off, rows, cols):
+        """rows x cols with ld = rows at element offset `off` of a 1-D tensor:
+        the matrix is one contiguous range (broadcast / all-reduce in place)."""
+        t = flat[off: off + rows * cols].view(cols, rows)
+        m = cls(t, rows, cols)
+        m.ld = max(rows, 1)
         return m
 
     def view(self, r0, r1, c0, c1):
@@ -121,6 +147,9 @@ class CudaOps:
     def alloc(self, rows, cols, zero=False):
         return CMat.alloc(self.torch, rows, cols, self.dev, zero)
 
+    def flat(self, count):
+        return self.torch.zeros(max(int(count), 1), dtype=self.torch.float64, device=self.dev)
+
     def _c(self, rc, what):
         _lib.check(rc, what)
 
@@ -145,19 +174,19 @@ class CudaOps:
         self._c(self.lib.br_gemm(self.h, int(ta), int(tb), m, n, k, alpha, A.ptr, A.ld, B.ptr, B.ld,
                                  beta, Cm.ptr, Cm.ld), "gemm")
 
-    def symm_acc(self, X, S, W, alpha=1.0, beta=1.0):
-        self._c(self.lib.br_symm_lower_ex(self.h, S.rows, W.cols, alpha, S.ptr, S.ld, W.ptr, W.ld,
-                                          beta, X.ptr, X.ld), "symm")
+    def symm_cyc(self, Xc, L, W, r0, stride, p0, p1):
+        """Rows [p0, p1) of the slab's share of sym(A2) W into Xc."""
+        self._c(self.lib.br_symm_lower_cyclic(self.h, W.rows, L.cols, W.cols,
+                                              L.ptr if L.cols else None, max(L.ld, W.rows), W.ptr,
+                                              W.ld, Xc.ptr, Xc.ld, r0, W.cols, stride, p0, p1),
+                "symm_cyclic")
 
-    def syr2k_cols(self, blk, j, cc0, X3, Y):
-        """A2[cc0:, cc0:cc0+b] += X3 Y^T + Y X3^T (lower part) where `blk` is the
-        locally stored block column holding A2 rows cc0..j-1 of those columns."""
-        b = blk.cols
-        # a j x j 'virtual' A2 whose columns cc0..cc0+b map onto blk; only
-        # lower tiles of that column range are ever touched by the kernel
-        fake = blk.ptr - 8 * (cc0 + cc0 * blk.ld)
-        self._c(self.lib.br_syr2k_lower(self.h, j, b, C.c_void_p(fake), blk.ld, X3.ptr, X3.ld,
-                                        Y.ptr, Y.ld, cc0, cc0 + b), "syr2k")
+    def syr2k_cyc(self, L, X3, Y, r0, stride):
+        if L.cols == 0:
+            return
+        self._c(self.lib.br_syr2k_lower_cyclic(self.h, L.rows, L.cols, Y.cols, L.ptr, L.ld, X3.ptr,
+                                               X3.ld, Y.ptr, Y.ld, r0, Y.cols, stride),
+                "syr2k_cyclic")
 
     def zero(self, M):
         M.t[: M.cols, : M.rows].zero_()
@@ -170,33 +199,60 @@ class CudaOps:
 
 
 class TorchComm:
-    """Collectives through torch.distributed (NCCL on GPUs, gloo on CPU)."""
+    """Collectives through torch.distributed (NCCL on GPUs, gloo on CPU).
 
-    def __init__(self, dist, group=None):
+    With `stream` (CUDA), every collective is issued on that stream after it
+    has waited for the compute stream, and returns an event; `wait(ev)` makes
+    the compute stream wait for it. Without a stream the calls are
+    synchronous and return None."""
+
+    def __init__(self, dist, group=None, stream=None):
         self.dist = dist
         self.group = group
+        self.stream = stream
 
-    def broadcast(self, M: CMat, src: int):
-        # contiguous staging when the view is strided
-        t = M.t[: M.cols, : M.rows]
-        if t.is_contiguous():
-            self.dist.broadcast(t, src=src, group=self.group)
-        else:
-            c = t.contiguous()
-            self.dist.broadcast(c, src=src, group=self.group)
-            t.copy_(c)
+    def _issue(self, t, fn):
+        if self.stream is None:
+            fn()
+            return None
+        import torch
 
-    def all_reduce(self, M: CMat):
-        t = M.t[: M.cols, : M.rows]
-        if t.is_contiguous():
-            self.dist.all_reduce(t, group=self.group)
-        else:
-            c = t.contiguous()
-            self.dist.all_reduce(c, group=self.group)
-            t.copy_(c)
+        self.stream.wait_stream(torch.cuda.current_stream(t.device))
+        with torch.cuda.stream(self.stream):
+            fn()
+            ev = torch.cuda.Event()
+            ev.record(self.stream)
+        return ev
 
-    def all_gather(self, out_list, inp):
-        self.dist.all_gather(out_list, inp, group=self.group)
+    def wait(self, ev):
+        if ev is not None:
+            import torch
+
+            torch.cuda.current_stream().wait_event(ev)
+
+    def broadcast(self, t, src: int):
+        """In place on a contiguous tensor (a packed CMat range)."""
+        return self._issue(t, lambda: self.dist.broadcast(t, src=src, group=self.group))
+
+    def all_reduce(self, t):
+        return self._issue(t, lambda: self.dist.all_reduce(t, group=self.group))
+
+    def all_gather_into(self, out, inp):
+        """out (world * inp.numel()) <- every rank's inp, rank order."""
+        def fn():
+            if hasattr(self.dist, "all_gather_into_tensor"):
+                try:
+                    self.dist.all_gather_into_tensor(out, inp, group=self.group)
+                    return
+                except (RuntimeError, NotImplementedError):
+                    pass
+            parts = list(out.view(-1, inp.numel()).unbind(0))
+            self.dist.all_gather(parts, inp, group=self.group)
+        return self._issue(inp, fn)
+
+    def gather_to0(self, inp, out_list):
+        """Rank 0 receives every rank's `inp` into out_list (None elsewhere)."""
+        self.dist.gather(inp, out_list, dst=0, group=self.group)
 
 
 def _sevp_iters(n, w, b):
@@ -207,10 +263,18 @@ def _sevp_iters(n, w, b):
     return ks
 
 
-def reduce_sym_band_dist(Aloc: CMat, lay: Layout, w: int, ops, comm, lookahead: int = 1):
+def _chunks(rows, b, chunk_rows):
+    """Row ranges of about chunk_rows rows, on multiples of b (never split a block)."""
+    step = max(b, chunk_rows // b * b)
+    return [(p, min(rows, p + step)) for p in range(0, rows, step)] or [(0, 0)]
+
+
+def reduce_sym_band_dist(Aloc: CMat, lay: Layout, w: int, ops, comm, lookahead: int = 1,
+                         chunk_rows: int = CHUNK_ROWS):
     """Distributed SEVP on the local block columns `Aloc` (n x ncols_local,
-    lower triangle authoritative), in place. Returns the iteration count.
-    Band entries of owned columns are final afterwards (use gather_band)."""
+    lower triangle authoritative and ZERO above the diagonal - scatter_columns
+    stores it so), in place. Returns the iteration count. Band entries of
+    owned columns are final afterwards (gather_band)."""
     n, b, P, me = lay.n, lay.b, lay.world, lay.rank
     if w != b:
         raise ValueError("the distributed path is built for w == b (the sharded configs)")
@@ -218,13 +282,14 @@ def reduce_sym_band_dist(Aloc: CMat, lay: Layout, w: int, ops, comm, lookahead: 
     if not ks:
         return 0
     jmax = n - w
-    Yb = [ops.alloc(jmax, b), ops.alloc(jmax, b)]
-    Wb = [ops.alloc(jmax, b), ops.alloc(jmax, b)]
-    Tb = [ops.alloc(b, b, zero=True), ops.alloc(b, b, zero=True)]
+    stride = P * b
+    pk = [ops.flat(jmax * b + b * b), ops.flat(jmax * b + b * b)]  # [Y | T] per parity
     taub = [ops.alloc(b, 1), ops.alloc(b, 1)]
-    X1 = ops.alloc(jmax, b)
-    X3 = ops.alloc(jmax, b)
-    X2 = ops.alloc(b, b)
+    wbuf, x1buf, x3buf = ops.flat(jmax * b), ops.flat(jmax * b), ops.flat(jmax * b)
+    X2 = CMat.packed(ops.flat(b * b), 0, b, b)
+
+    def yt(par, j):
+        return CMat.packed(pk[par], 0, j, b), CMat.packed(pk[par], j * b, b, b)
 
     def block(t, r0):  # local block column t, rows r0..n
         s = lay.slot(t)
@@ -235,57 +300,57 @@ def reduce_sym_band_dist(Aloc: CMat, lay: Layout, w: int, ops, comm, lookahead: 
         t = k // b
         j = n - k - w
         par = idx & 1
-        Y, W, T, tau = Yb[par].view(0, j, 0, b), Wb[par].view(0, j, 0, b), Tb[par], taub[par]
+        Y, T = yt(par, j)
         owner = lay.owner(t)
         if me == owner:
             if prefetched:
                 ops.join(waiter_panel=False)
             else:
-                ops.qr_panel(block(t, k + w), Y, T, None, tau)
+                ops.qr_panel(block(t, k + w), Y, T, None, taub[par])
         prefetched = False
-        comm.broadcast(Y, owner)
-        comm.broadcast(T, owner)
+        comm.wait(comm.broadcast(pk[par][: j * b + b * b], owner))
+        W = CMat.packed(wbuf, 0, j, b)
         ops.gemm(W, Y, T)  # same kernel on every rank -> identical W everywhere
-        # ---- X1 = sym(A2) W, owned block columns only, then all-reduce ----
-        Xv = X1.view(0, j, 0, b)
-        ops.zero(Xv)
-        mine = [c for c in lay.owned if c > t]
-        for c in mine:
-            cc0 = c * b - (k + w)
-            cc1 = cc0 + b
-            blk = block(c, c * b)
-            ops.symm_acc(Xv.view(cc0, cc1, 0, b), blk.view(0, b, 0, b), W.view(cc0, cc1, 0, b))
-            if cc1 < j:
-                below = blk.view(b, n - c * b, 0, b)
-                ops.gemm(Xv.view(cc1, j, 0, b), below, W.view(cc0, cc1, 0, b), 1.0, 1.0)
-                ops.gemm(Xv.view(cc0, cc1, 0, b), below, W.view(cc1, j, 0, b), 1.0, 1.0, ta=True)
-        comm.all_reduce(Xv)
-        X2v, X3v = X2, X3.view(0, j, 0, b)
-        ops.gemm(X2v, Xv, W, 0.5, 0.0, ta=True)
-        ops.copy(X3v, Xv)
-        ops.gemm(X3v, Y, X2v, 1.0, 1.0)
-        # ---- SYR2K on owned columns; look-ahead on the next panel's owner ----
-        nxt = ks[idx + 1] // b if idx + 1 < len(ks) else None
-        order = list(mine)
-        if lookahead and nxt is not None and lay.owner(nxt) == me and nxt in order:
-            cc0 = nxt * b - (k + w)
-            ops.syr2k_cols(block(nxt, nxt * b), j, cc0, X3v, Y)
-            order.remove(nxt)
+        first, s0, nown = lay.owned_after(t)
+        L = Aloc.view(k + w, n, s0 * b, lay.ncols_local)  # the owned trailing slab
+        r0 = first * b - (k + w) if first is not None else 0
+        # ---- X1 = sym(A2) W: slab share by row chunk, each chunk all-reduced
+        # on the comm stream while the next one computes ----
+        chunks = _chunks(j, b, chunk_rows)
+        X1c, evs = [], []
+        for p0, p1 in chunks:
+            Xc = CMat.packed(x1buf, p0 * b, p1 - p0, b)
+            ops.symm_cyc(Xc, L, W, r0, stride, p0, p1)
+            evs.append(comm.all_reduce(x1buf[p0 * b: p1 * b]))
+            X1c.append(Xc)
+        # ---- X2 = X1^T W / 2, X3 = X1 + Y X2 (chunk by chunk as they arrive) ----
+        for c, (p0, p1) in enumerate(chunks):
+            comm.wait(evs[c])
+            ops.gemm(X2, X1c[c], W.view(p0, p1, 0, b), 0.5, 0.0 if c == 0 else 1.0, ta=True)
+        X3 = CMat.packed(x3buf, 0, j, b)
+        for c, (p0, p1) in enumerate(chunks):
+            X3c = X3.view(p0, p1, 0, b)
+            ops.copy(X3c, X1c[c])
+            ops.gemm(X3c, Y.view(p0, p1, 0, b), X2, 1.0, 1.0)
+        # ---- SYR2K on the slab; look-ahead on the next panel's owner ----
+        if nown and lookahead and idx + 1 < len(ks) and first == t + 1:
+            ops.syr2k_cyc(L.view(0, j, 0, b), X3, Y, r0, stride)
             kn = ks[idx + 1]
             jn = n - kn - w
+            Yn, Tn = yt(par ^ 1, jn)
             ops.join(waiter_panel=True)
             ops.panel_stream(True)
-            ops.qr_panel(block(nxt, kn + w), Yb[par ^ 1].view(0, jn, 0, b), Tb[par ^ 1], None,
-                         taub[par ^ 1])
+            ops.qr_panel(block(first, kn + w), Yn, Tn, None, taub[par ^ 1])
             ops.panel_stream(False)
             prefetched = True
-        for c in order:
-            cc0 = c * b - (k + w)
-            ops.syr2k_cols(block(c, c * b), j, cc0, X3v, Y)
+            ops.syr2k_cyc(L.view(0, j, b, L.cols), X3, Y, r0 + stride, stride)
+        elif nown:
+            ops.syr2k_cyc(L, X3, Y, r0, stride)
     return len(ks)
 
 
-def reduce_tri_band_dist(Aloc: CMat, lay: Layout, w: int, ops, comm, lookahead: int = 1):
+def reduce_tri_band_dist(Aloc: CMat, lay: Layout, w: int, ops, comm, lookahead: int = 1,
+                         chunk_rows: int = CHUNK_ROWS):
     """Distributed upper triangular-band reduction of a square n x n matrix
     held as local block columns, in place. Returns the iteration count."""
     n, b, P, me = lay.n, lay.b, lay.world, lay.rank
@@ -293,16 +358,21 @@ def reduce_tri_band_dist(Aloc: CMat, lay: Layout, w: int, ops, comm, lookahead: 
     if w != b:
         raise ValueError("the distributed path is built for w == b (the sharded configs)")
     torch = ops.torch
-    Yu = [ops.alloc(m, b), ops.alloc(m, b)]
-    Wu = [ops.alloc(m, b), ops.alloc(m, b)]
-    Tu = [ops.alloc(b, b, zero=True), ops.alloc(b, b, zero=True)]
+    pk = [ops.flat(m * b + b * b), ops.flat(m * b + b * b)]  # [Y_U | T_U] per parity
     tauu = [ops.alloc(b, 1), ops.alloc(b, 1)]
+    Wu = ops.alloc(m, b)
     Yv, Wv, Tv, tauv = ops.alloc(n, b), ops.alloc(n, b), ops.alloc(b, b, zero=True), ops.alloc(b, 1)
     Zl = ops.alloc(b, max(b, lay.ncols_local))
-    Zr = ops.alloc(m, b)
+    zbuf = ops.flat(m * b)
     rowp = ops.alloc(b, n)  # gathered LQ row panel (b x jr)
     Yg = ops.alloc(lay.ncols_local + b, b)  # Y_V / W_V rows of the owned blocks, gathered
     Wg = ops.alloc(lay.ncols_local + b, b)
+    per_max = -(-lay.nblk // P)
+    stage = ops.flat(per_max * b * b)
+    gathered = ops.flat(P * per_max * b * b)
+
+    def yt(par, i):
+        return CMat.packed(pk[par], 0, i, b), CMat.packed(pk[par], i * b, b, b)
 
     def block(t, r0, r1=None):
         s = lay.slot(t)
@@ -322,20 +392,18 @@ def reduce_tri_band_dist(Aloc: CMat, lay: Layout, w: int, ops, comm, lookahead: 
         t = k // b
         i = m - k
         par = idx & 1
-        Y, W, T, tau = Yu[par].view(0, i, 0, b), Wu[par].view(0, i, 0, b), Tu[par], tauu[par]
+        Y, T = yt(par, i)
+        W = Wu.view(0, i, 0, b)
         owner = lay.owner(t)
         if me == owner:
             if prefetched:
                 ops.join(waiter_panel=False)
             else:
-                ops.qr_panel(block(t, k), Y, T, None, tau)
+                ops.qr_panel(block(t, k), Y, T, None, tauu[par])
         prefetched = False
-        comm.broadcast(Y, owner)
-        comm.broadcast(T, owner)
+        comm.wait(comm.broadcast(pk[par][: i * b + b * b], owner))
         ops.gemm(W, Y, T)  # same kernel on every rank -> identical W everywhere
-        mine = [c for c in lay.owned if c > t]
-        nown = len(mine)
-        s0 = lay.slot(mine[0]) if nown else lay.ncols_local // b
+        first, s0, nown = lay.owned_after(t)
         # ---- left update of all owned trailing block columns (one local range) ----
         if nown:
             E = blocks(s0, k)
@@ -348,84 +416,116 @@ def reduce_tri_band_dist(Aloc: CMat, lay: Layout, w: int, ops, comm, lookahead: 
         # ---- LQ row panel: all-gather the owned b x b pieces, factor everywhere ----
         nb_right = (n - (k + b)) // b  # blocks t+1 .. nblk-1
         per = -(-nb_right // P)  # max blocks any rank owns among t+1..
-        stage = torch.zeros((P, per * b, b), dtype=torch.float64, device=Aloc.t.device)
+        sv = stage[: per * b * b].view(per * b, b)
         if nown:
-            stage[me, : nown * b].copy_(Aloc.t[s0 * b: lay.ncols_local, k: k + b])
-        parts = [torch.empty_like(stage[0]) for _ in range(P)]
-        comm.all_gather(parts, stage[me].contiguous())
+            sv[: nown * b].copy_(Aloc.t[s0 * b: lay.ncols_local, k: k + b])
+        gv = gathered[: P * per * b * b]
+        comm.wait(comm.all_gather_into(gv, stage[: per * b * b]))
+        parts = gv.view(P, per * b, b)
         R = rowp.view(0, b, 0, jr)
         R3 = rowp.t[: nb_right * b].view(nb_right, b, rowp.t.shape[1])
         for r in range(P):
-            first = (r - (t + 1)) % P  # first block t+1+first owned by rank r
-            cnt = len(range(first, nb_right, P))
+            f = (r - (t + 1)) % P  # first block t+1+f owned by rank r
+            cnt = len(range(f, nb_right, P))
             if cnt:
-                R3[first::P, :, :b].copy_(parts[r][: cnt * b].view(cnt, b, b))
+                R3[f::P, :, :b].copy_(parts[r][: cnt * b].view(cnt, b, b))
         Yvv, Wvv = Yv.view(0, jr, 0, b), Wv.view(0, jr, 0, b)
         ops.qr_panel(R, Yvv, Tv, Wvv, tauv, lq=True)
         if lay.owner(t + 1) == me:  # L into block t+1's rows k..k+b
             ops.copy(block(t + 1, k, k + b), R.view(0, b, 0, b))
-        # ---- right update: partial Z over owned columns, all-reduce, local apply ----
-        Zv = Zr.view(0, i - b, 0, b)
+        # ---- right update, pipelined by row chunks: Z_c = D_c W_V (partial),
+        # all-reduce(Z_c) on the comm stream, D_c += Z_c Y_V^T once it lands ----
+        rows = i - b
+        chunks = _chunks(rows, b, chunk_rows)
         if nown:
-            # rows of Y_V / W_V belonging to the owned blocks, in local order
-            first = (me - (t + 1)) % P
+            fo = (me - (t + 1)) % P  # rows of Y_V / W_V of the owned blocks, local order
             Yg3 = Yg.t[:b, : nown * b].view(b, nown, b)
             Wg3 = Wg.t[:b, : nown * b].view(b, nown, b)
             Yv3 = Yv.t[:b, : nb_right * b].view(b, nb_right, b)
             Wv3 = Wv.t[:b, : nb_right * b].view(b, nb_right, b)
-            Yg3.copy_(Yv3[:, first::P, :])
-            Wg3.copy_(Wv3[:, first::P, :])
-            ops.gemm(Zv, blocks(s0, k + b), Wg.view(0, nown * b, 0, b), 1.0, 0.0)
-        else:
-            ops.zero(Zv)
-        comm.all_reduce(Zv)
+            Yg3.copy_(Yv3[:, fo::P, :])
+            Wg3.copy_(Wv3[:, fo::P, :])
+        Zc, evs = [], []
+        for p0, p1 in chunks:
+            Zp = CMat.packed(zbuf, p0 * b, p1 - p0, b)
+            if nown:
+                ops.gemm(Zp, blocks(s0, k + b + p0, k + b + p1), Wg.view(0, nown * b, 0, b), 1.0, 0.0)
+            else:
+                ops.zero(Zp)
+            evs.append(comm.all_reduce(zbuf[p0 * b: p1 * b]))
+            Zc.append(Zp)
         nxt = t + 1 if idx + 1 < len(its) else None
-        lead = 0
-        if lookahead and nxt is not None and lay.owner(nxt) == me and nown and mine[0] == nxt:
-            ops.gemm(block(nxt, k + b), Zv, Yg.view(0, b, 0, b), 1.0, 1.0, tb=True)
-            lead = 1
+        lead = 1 if (lookahead and nxt is not None and nown and first == nxt) else 0
+        for c, (p0, p1) in enumerate(chunks):
+            comm.wait(evs[c])
+            if lead:
+                ops.gemm(block(nxt, k + b + p0, k + b + p1), Zc[c], Yg.view(0, b, 0, b), 1.0, 1.0,
+                         tb=True)
+            elif nown:
+                ops.gemm(blocks(s0, k + b + p0, k + b + p1), Zc[c], Yg.view(0, nown * b, 0, b), 1.0,
+                         1.0, tb=True)
+        if lead:
             kn = its[idx + 1]
+            Yn, Tn = yt(par ^ 1, m - kn)
             ops.join(waiter_panel=True)
             ops.panel_stream(True)
-            ops.qr_panel(block(nxt, kn), Yu[par ^ 1].view(0, m - kn, 0, b), Tu[par ^ 1], None,
-                         tauu[par ^ 1])
+            ops.qr_panel(block(nxt, kn), Yn, Tn, None, tauu[par ^ 1])
             ops.panel_stream(False)
             prefetched = True
-        if nown > lead:
-            ops.gemm(blocks(s0 + lead, k + b), Zv, Yg.view(lead * b, nown * b, 0, b), 1.0, 1.0,
-                     tb=True)
+            if nown > 1:
+                for c, (p0, p1) in enumerate(chunks):
+                    ops.gemm(blocks(s0 + 1, k + b + p0, k + b + p1), Zc[c],
+                             Yg.view(b, nown * b, 0, b), 1.0, 1.0, tb=True)
     return len(its)
 
 
-def scatter_columns(A: np.ndarray, lay: Layout, ops) -> CMat:
-    """Upload this rank's block columns of a host matrix (F-order)."""
+def scatter_columns(A: np.ndarray, lay: Layout, ops, kind: str = "tri") -> CMat:
+    """Upload this rank's block columns of a host matrix (F-order). For SEVP
+    only the lower triangle is stored (zeros above the diagonal: the
+    block-cyclic SYMM relies on it; the upper triangle is never read, ref
+    sevp.py:290)."""
     torch = ops.torch
-    L = ops.alloc(A.shape[0], lay.ncols_local)
+    n = A.shape[0]
+    L = ops.alloc(n, lay.ncols_local)
     for q, t in enumerate(lay.owned):
-        blk = np.ascontiguousarray(A[:, t * lay.b : (t + 1) * lay.b].T)  # (b, n) row-major
-        L.t[q * lay.b : (q + 1) * lay.b, : A.shape[0]].copy_(torch.from_numpy(blk))
+        blk = np.ascontiguousarray(A[:, t * lay.b: (t + 1) * lay.b].T)  # (b, n) row-major
+        if kind == "sevp":
+            c = np.arange(t * lay.b, (t + 1) * lay.b)[:, None]
+            blk = np.where(np.arange(n)[None, :] >= c, blk, 0.0)
+        L.t[q * lay.b: (q + 1) * lay.b, :n].copy_(torch.from_numpy(blk))
     return L
 
 
+def _strip(t, b, w, n, kind):
+    """Rows of block column t's band strip: SEVP the diagonal block and w
+    rows below it; triband w rows above and the diagonal block."""
+    if kind == "sevp":
+        return t * b, min(n, t * b + b + w)
+    return max(0, t * b - w), t * b + b
+
+
 def gather_band(Aloc: CMat, lay: Layout, w: int, kind: str, comm, torch) -> np.ndarray | None:
-    """Assemble the band on rank 0: SEVP -> full symmetric band (mirrored,
-    off-band exactly 0, ref sevp.py:276-284); triband -> upper band with
-    lower bw 0 (ref svd.py:237-239). Other ranks return None."""
+    """Assemble the band on rank 0 only: SEVP -> full symmetric band
+    (mirrored, off-band exactly 0, ref sevp.py:276-284); triband -> upper
+    band with lower bw 0 (ref svd.py:237-239). Each rank sends only the band
+    strips of its block columns ((b + w) x b per block). Other ranks return None."""
     n, b, P = lay.n, lay.b, lay.world
-    local = Aloc.t[: lay.ncols_local, :n].contiguous()
-    per = -(-lay.nblk // P) * b
-    stage = torch.zeros((per, n), dtype=torch.float64, device=Aloc.t.device)
-    stage[: lay.ncols_local].copy_(local)
-    parts = [torch.empty_like(stage) for _ in range(P)]
-    comm.all_gather(parts, stage)
+    h = b + w
+    per = -(-lay.nblk // P)
+    stage = torch.zeros((per, b, h), dtype=torch.float64, device=Aloc.t.device)
+    for q, t in enumerate(lay.owned):
+        r0, r1 = _strip(t, b, w, n, kind)
+        stage[q, :, : r1 - r0].copy_(Aloc.t[q * b: (q + 1) * b, r0:r1])
+    parts = [torch.empty_like(stage) for _ in range(P)] if lay.rank == 0 else None
+    comm.gather_to0(stage, parts)
     if lay.rank != 0:
         return None
     full = np.zeros((n, n), order="F")
     for r in range(P):
         host = parts[r].cpu().numpy()
-        blks = [t for t in range(lay.nblk) if t % P == r]
-        for q, t in enumerate(blks):
-            full[:, t * b : (t + 1) * b] = host[q * b : (q + 1) * b, :].T
+        for q, t in enumerate([t for t in range(lay.nblk) if t % P == r]):
+            r0, r1 = _strip(t, b, w, n, kind)
+            full[r0:r1, t * b: (t + 1) * b] = host[q, :, : r1 - r0].T
     ii = np.arange(n)[:, None]
     jj = np.arange(n)[None, :]
     if kind == "sevp":
