@@ -558,8 +558,9 @@ int br_create(int device, br_handle_t* out) {
   }
   BR_CUDA(cudaStreamCreateWithFlags(&h->ws.copy, cudaStreamNonBlocking));
   BR_CUDA(cudaStreamCreateWithFlags(&h->ws.copy_in, cudaStreamNonBlocking));
-  BR_CUDA(cudaMalloc(&h->ws.flags, 128 * sizeof(unsigned)));
-  BR_CUDA(cudaMemset(h->ws.flags, 0, 128 * sizeof(unsigned)));
+  // [0, 128): persistent-panel handshakes; [128, 130): xchain grid barrier
+  BR_CUDA(cudaMalloc(&h->ws.flags, 256 * sizeof(unsigned)));
+  BR_CUDA(cudaMemset(h->ws.flags, 0, 256 * sizeof(unsigned)));
   BR_CUDA(cudaEventCreateWithFlags(&h->ws.ev_aux0, cudaEventDisableTiming));
   BR_CUDA(cudaEventCreateWithFlags(&h->ws.ev_aux1, cudaEventDisableTiming));
   // load every kernel now: under lazy loading a first launch inside the
@@ -567,6 +568,7 @@ int br_create(int device, br_handle_t* out) {
   g_preload_only = true;
   int prc = preload_gemm_kernels();
   if (!prc) prc = preload_panel_kernels();
+  if (!prc) prc = preload_xchain_kernels();
   g_preload_only = false;
   if (prc) return prc;
   {

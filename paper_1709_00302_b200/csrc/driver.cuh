@@ -178,6 +178,7 @@ int house_gen_dev(cudaStream_t st, int64_t L, const double* x, double* v, double
 
 // Force-load every kernel of the library (gemm.cu, panel.cu, driver.cu).
 int preload_gemm_kernels();
+int preload_xchain_kernels();
 int preload_panel_kernels();
 
 // Elementwise helpers (driver.cu)

@@ -61,6 +61,7 @@ struct GemmArgs {
   // global index. cyc_bs == 0: off.
   int64_t cyc_r0;
   int cyc_bs, cyc_stride;
+  int no_trigger;  // persistent callers (xchain): no early PDL trigger from a tile
 };
 
 // Global column (= first stored row) of local column c under the map.
@@ -113,5 +114,13 @@ int symm_cyclic(cudaStream_t st, Scratch& ws, MatView X1, MatView L, MatView W, 
                 double* tmp, int64_t p0, int64_t p1);
 // L += lower part of X3 Y^T + Y X3^T at the slab's columns (tmp: 2 * ncols * b).
 int syr2k_cyclic(cudaStream_t st, MatView L, MatView X3, MatView Y, CycCols m, double* tmp);
+
+// The SEVP X products in ONE persistent launch (b <= 64, ref sevp.py:156-176):
+// X1 = sym(A2) W, X2 = X1^T W / 2, X3 = X1 + Y X2, phases separated by a
+// grid barrier (bar: 2 zeroed words, self-resetting). Returns 1 (nothing
+// launched) when the shape is not covered; the caller then runs the
+// separate kernels.
+int xchain(cudaStream_t st, Scratch& ws, MatView X1, MatView X2, MatView X3, MatView A2,
+           MatView W, MatView Y, unsigned* bar);
 
 }  // namespace br

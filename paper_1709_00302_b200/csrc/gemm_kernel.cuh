@@ -346,7 +346,7 @@ __device__ __forceinline__ void dgemm_tile(const GemmArgs& g, const unsigned bx,
     }
   }
   cp_async_wait<0>();
-  pdl_trigger();  // the next kernel may start launching during the epilogue
+  if (!g.no_trigger) pdl_trigger();  // the next kernel may start launching during the epilogue
 
   // ---- epilogue ----
 #pragma unroll

@@ -59,6 +59,19 @@ static int64_t pz_rows() {
   return r;
 }
 
+// The fused X-product launch (xchain, BR_XCHAIN=1) for narrow panels.
+// Measured on c1 (one box, 2 x 3 steps): 5.68 ms fused vs 5.62 ms with the
+// separate SYMM / X2 / X3 kernels - the three grid barriers and the lost
+// PDL overlap of the next launch cost what the saved launches win - so off.
+static bool xchain_enabled() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = std::getenv("BR_XCHAIN");
+    m = (e && std::atoi(e) == 1) ? 1 : 0;
+  }
+  return m == 1;
+}
+
 static double panel_flops(int64_t j, int64_t b) {
   return 2.0 * j * b * b - 2.0 * b * b * b / 3.0 + (double)j * b * b;  // QR + T/W
 }
@@ -164,6 +177,12 @@ int sevp_reduce(Workspace& ws, int64_t n, int64_t w, int64_t b, int lookahead, d
     // X1 = sym(A2) W; X2 = 1/2 X1^T W; X3 = X1 + Y X2 (ref sevp.py:156-176)
     auto xprods = [&]() -> int {
       MatView X1(X1b, jmax, j, bp), X3(X3b, jmax, j, bp), X2(X2b, b, bp, bp);
+      if (xchain_enabled()) {  // narrow panels: the three products in one launch
+        TimeScope ts(ws, ws.main, TC_SYMM,
+                     gemm_flops(j, bp, j) + gemm_flops(bp, bp, j) + gemm_flops(j, bp, bp), "xchain", k);
+        const int r = xchain(ws.main, ws.sk_main, X1, X2, X3, A2, W, Y, ws.flags + 128);
+        if (r <= 0) return r;
+      }
       {
         TimeScope ts(ws, ws.main, TC_SYMM, gemm_flops(j, bp, j), "xprod1", k);
         BR_CHECK(symm_lower(ws.main, ws.sk_main, X1, A2, W));

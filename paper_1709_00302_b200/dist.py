@@ -485,14 +485,16 @@ def scatter_columns(A: np.ndarray, lay: Layout, ops, kind: str = "tri") -> CMat:
     block-cyclic SYMM relies on it; the upper triangle is never read, ref
     sevp.py:290)."""
     torch = ops.torch
-    n = A.shape[0]
+    n, b = A.shape[0], lay.b
+    A = np.asfortranarray(A)
     L = ops.alloc(n, lay.ncols_local)
     for q, t in enumerate(lay.owned):
-        blk = np.ascontiguousarray(A[:, t * lay.b: (t + 1) * lay.b].T)  # (b, n) row-major
-        if kind == "sevp":
-            c = np.arange(t * lay.b, (t + 1) * lay.b)[:, None]
-            blk = np.where(np.arange(n)[None, :] >= c, blk, 0.0)
-        L.t[q * lay.b: (q + 1) * lay.b, :n].copy_(torch.from_numpy(blk))
+        dst = L.t[q * b: (q + 1) * b]
+        # an F-order column block is one contiguous (b, n) row-major range: no host copy
+        dst[:, :n].copy_(torch.from_numpy(A[:, t * b: (t + 1) * b].T))
+        if kind == "sevp":  # zero above the diagonal, on the device
+            dst[:, : t * b].zero_()
+            dst[:, t * b: (t + 1) * b].copy_(torch.triu(dst[:, t * b: (t + 1) * b]))
     return L
 
 

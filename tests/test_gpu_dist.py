@@ -99,6 +99,7 @@ def test_cyclic_slab_kernels_vs_numpy(world, rank, j, b):
             _lib.check(lib.br_symm_lower_cyclic(h, j, nc, b, Ld.data_ptr() if nc else None, ld,
                                                 Wd.data_ptr(), j, Xc.data_ptr(), p1 - p0, r0, b,
                                                 world * b, p0, p1), "symm_cyclic")
+            _lib.check(lib.br_sync(h), "sync")  # the library's own stream, then torch's copy
             X1d[:, p0:p1] = Xc
         torch.cuda.synchronize()
         share = X1d.cpu().numpy().T
