@@ -176,6 +176,20 @@ int br_syr2k_lower_cyclic(br_handle_t h, int64_t j, int64_t ncols, int64_t b, do
 int br_sym_two_sided_update(br_handle_t h, int64_t j, int64_t b, double* A2, int64_t lda,
                             const double* Y, int64_t ldy, const double* W, int64_t ldw);
 
+/* ---- second stage (beyond the reference, which stops at
+ * the band) ------------------------------------------------------ */
+/* Symmetric band (bandwidth w <= 128, lower triangle of the n x n device
+ * matrix A) -> symmetric tridiagonal by Householder bulge chasing, in place;
+ * d (n) = diagonal, e (n - 1) = subdiagonal (device). The eigenvalues are
+ * those of the band. */
+int br_band_to_tridiag(br_handle_t h, int64_t n, int64_t w, double* A, int64_t lda, double* d,
+                       double* e);
+/* Upper triangular band (bandwidth w <= 128; m x n device matrix, m >= n,
+ * rows >= n zero) -> upper bidiagonal, in place; d (n), e (n - 1) =
+ * superdiagonal. The singular values are those of the band. */
+int br_band_to_bidiag(br_handle_t h, int64_t m, int64_t n, int64_t w, double* A, int64_t lda,
+                      double* d, double* e);
+
 /* ---- reductions --------------------------------------------------------- */
 /* Every reduction takes `factors` (nullable, see br_factors): when given,
  * each panel's Y, T and tau are stored there as the panel is factored. */

@@ -28,6 +28,7 @@ from .kernels import (
 from .runtime import EventTrace, ExecGroups, WriteOverlapError
 from .sevp import SevpConfig, SevpResult, SevpVariant, V2Mapping, reduce_sym_band
 from .svd import SvdConfig, SvdForm, SvdResult, SvdVariant, reduce_band_svd, reduce_tri_band
+from .stage2 import band_to_bidiagonal, band_to_tridiagonal
 from ._dev import set_device, get_device
 
 __all__ = [
@@ -61,6 +62,8 @@ __all__ = [
     "reduce_tri_band",
     "reduce_band_svd",
     "svd_nominal_flops",
+    "band_to_tridiagonal",
+    "band_to_bidiagonal",
     "band_check",
     "orth_residual",
     "spectra_match",

@@ -68,6 +68,8 @@ SIGNATURES = {
                                        i64, i64, i64, i64, i64]),
     "br_syr2k_lower_cyclic": (C.c_int, [C.c_void_p, i64, i64, i64, dptr, i64, dptr, i64, dptr, i64,
                                         i64, i64, i64]),
+    "br_band_to_tridiag": (C.c_int, [C.c_void_p, i64, i64, dptr, i64, dptr, dptr]),
+    "br_band_to_bidiag": (C.c_int, [C.c_void_p, i64, i64, i64, dptr, i64, dptr, dptr]),
     "br_sym_two_sided_update": (C.c_int, [C.c_void_p, i64, i64, dptr, i64, dptr, i64, dptr, i64]),
     "br_set_option": (C.c_int, [C.c_void_p, C.c_int, i64]),
     "br_reduce_sym_band": (C.c_int, [C.c_void_p, i64, i64, i64, C.c_int, dptr, i64, dptr, i64,

@@ -569,6 +569,7 @@ int br_create(int device, br_handle_t* out) {
   int prc = preload_gemm_kernels();
   if (!prc) prc = preload_panel_kernels();
   if (!prc) prc = preload_xchain_kernels();
+  if (!prc) prc = preload_stage2_kernels();
   g_preload_only = false;
   if (prc) return prc;
   {
@@ -592,6 +593,7 @@ int br_destroy(br_handle_t h) {
   devbuf_free(ws.factors);
   devbuf_free(ws.tmp);
   devbuf_free(ws.tmp_panel);
+  devbuf_free(ws.s2prog);
   devbuf_free(ws.pscratch_panel);
   devbuf_free(ws.stageA);
   devbuf_free(ws.stageQ);
@@ -853,6 +855,40 @@ int br_syr2k_lower_cyclic(br_handle_t h, int64_t j, int64_t ncols, int64_t b, do
   BR_CHECK(devbuf_reserve(tmp, 2 * ncols * b));
   return syr2k_cyclic(cur_stream(ws), MatView(L, ldl, j, ncols), MatView((double*)X3, ldx, j, b),
                       MatView((double*)Y, ldy, j, b), CycCols{r0, (int)bs, (int)stride}, tmp.p);
+}
+
+// ---- second stage (no reference counterpart) ----------------
+int br_band_to_tridiag(br_handle_t h, int64_t n, int64_t w, double* A, int64_t lda, double* d,
+                       double* e) {
+  ARG(h != nullptr, 1);
+  ARG(n >= 0, 2);
+  ARG(w >= 1 && w <= 128, 3);
+  ARG(A || n == 0, 4);
+  ARG(lda >= std::max<int64_t>(n, 1), 5);
+  ARG(d || n == 0, 6);
+  ARG(e || n <= 1, 7);
+  DEV(h);
+  if (n == 0) return 0;
+  Workspace& ws = h->ws;
+  BR_CHECK(devbuf_reserve(ws.s2prog, n / 2 + 1));
+  return band_to_condensed(cur_stream(ws), false, n, w, A, lda, d, e, (int*)ws.s2prog.p, ws.num_sms);
+}
+
+int br_band_to_bidiag(br_handle_t h, int64_t m, int64_t n, int64_t w, double* A, int64_t lda,
+                      double* d, double* e) {
+  ARG(h != nullptr, 1);
+  ARG(m >= 0, 2);
+  ARG(n >= 0 && n <= m, 3);
+  ARG(w >= 1 && w <= 128, 4);
+  ARG(A || n == 0, 5);
+  ARG(lda >= std::max<int64_t>(m, 1), 6);
+  ARG(d || n == 0, 7);
+  ARG(e || n <= 1, 8);
+  DEV(h);
+  if (n == 0) return 0;
+  Workspace& ws = h->ws;
+  BR_CHECK(devbuf_reserve(ws.s2prog, n / 2 + 1));
+  return band_to_condensed(cur_stream(ws), true, n, w, A, lda, d, e, (int*)ws.s2prog.p, ws.num_sms);
 }
 
 int br_stream_select(br_handle_t h, int which) {

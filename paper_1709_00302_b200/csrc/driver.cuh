@@ -49,6 +49,7 @@ struct Workspace {
   DevBuf pscratch;  // panel_qr internal scratch (reductions; kernel-level calls on main)
   DevBuf pscratch_panel;  // panel_qr scratch of kernel-level calls on the panel stream
   DevBuf factors;   // reduction buffers
+  DevBuf s2prog;    // second stage: per-sweep progress counters
   DevBuf tmp, tmp_panel;  // kernel-level API temporaries, one per stream
   DevBuf stageA, stageQ;  // host-buffer entry points
   DevBuf stageF;          // host-buffer entry points: device copy of the factor output
@@ -179,6 +180,13 @@ int house_gen_dev(cudaStream_t st, int64_t L, const double* x, double* v, double
 // Force-load every kernel of the library (gemm.cu, panel.cu, driver.cu).
 int preload_gemm_kernels();
 int preload_xchain_kernels();
+int preload_stage2_kernels();
+// Second stage (stage2.cu): band (bandwidth w) -> tridiagonal (bd = false,
+// symmetric band in the lower triangle) or upper bidiagonal (bd = true,
+// upper triangular band, n x n) by bulge chasing, in place on A; d (n) and
+// e (n - 1) receive the diagonals. prog: n ints of scratch.
+int band_to_condensed(cudaStream_t st, bool bd, int64_t n, int64_t w, double* A, int64_t lda,
+                      double* d, double* e, int* prog, int num_sms);
 int preload_panel_kernels();
 
 // Elementwise helpers (driver.cu)
