@@ -12,10 +12,10 @@
 // occupancy query), CTA q running sweeps q, q + G, q + 2G, ... in order.
 // Sweep s publishes the number of tasks it has completed in prog[s]
 // (release); task j of sweep s waits (acquire) until sweep s - 1 has
-// completed the tasks whose index ranges overlap it (LAG_SB = 3 tasks ahead
-// for the symmetric chase, LAG_BD = 4 for the bidiagonal one, derived from
-// the index ranges in the comments below; overlap with older sweeps follows
-// by transitivity). Tasks that do not overlap commute, so the result equals
+// completed every task that shares a matrix element with it (LAG_SB = 2:
+// tasks <= j+1 for the symmetric chase, LAG_BD = 3: tasks <= j+2 for the
+// bidiagonal one; the element sets are in the comments below; conflicts
+// with older sweeps follow by transitivity). Tasks that do not overlap commute, so the result equals
 // the sequential task order to the last bit, whatever the grid size (tested).
 // Each task stages its block (at most w x w, w <= 128) in shared memory; all
 // matrix loads bypass L1 (ld.global.cg), since other CTAs wrote the data.
@@ -26,7 +26,7 @@
 namespace br {
 
 constexpr int S2_WMAX = 128;
-constexpr int LAG_SB = 3, LAG_BD = 4;
+constexpr int LAG_SB = 2, LAG_BD = 3;
 
 struct Stage2Args {
   int64_t n;
@@ -138,26 +138,28 @@ __device__ void store_blk(const double* O, const Stage2Args& a, int64_t r0, int6
   }
 }
 
-__device__ __forceinline__ void wait_prev(const Stage2Args& a, int64_t s, int need) {
+// `seen` (thread 0's register): the last progress value read for sweep
+// s - 1; the acquire load is skipped while it already covers the need.
+__device__ __forceinline__ void wait_prev(const Stage2Args& a, int64_t s, int need, int& seen) {
   if (threadIdx.x == 0 && s > 0) {
-    while (ld_acquire_i32(&a.prog[s - 1]) < need) {
-    }
+    while (seen < need) seen = ld_acquire_i32(&a.prog[s - 1]);
   }
   __syncthreads();
 }
+// The CTA barrier orders every thread's stores of the task before thread
+// 0's release store (st.release carries the gpu-scope fence).
 __device__ __forceinline__ void publish(const Stage2Args& a, int64_t s, int done) {
-  __syncthreads();  // every store of the task issued
-  if (threadIdx.x == 0) {
-    __threadfence();
-    st_release_i32(&a.prog[s], done);
-  }
+  __syncthreads();
+  if (threadIdx.x == 0) st_release_i32(&a.prog[s], done);
 }
 
 // ---------------------------------------------------------------------------
-// SEVP: band -> tridiagonal. Sweep s, task 0 touches indices [s, s+w]
-// (column s and D0 = [s+1, s+1+w)^2); task j >= 1 touches [r_{j-1}, r_j + w)
-// with r_j = s + 1 + j w (O = rows [r_j, r_j+w) x cols [r_{j-1}, r_j), then
-// D_j). Sweep s task j overlaps sweep s-1 tasks <= j+2 only: wait for j+3.
+// SEVP: band -> tridiagonal. With r_j = s + 1 + j w, sweep s task 0 writes
+// column s (rows [r_0, r_0+w)) and D_0 = [r_0, r_0+w)^2 (lower); task j >= 1
+// writes O_j = rows [r_j, r_j+w) x cols [r_{j-1}, r_j) and D_j. Sweep s+1
+// (all indices + 1) task j shares elements with sweep s tasks j (D_j, O_j)
+// and j+1 (row r_{j+1} = r_j + w of O_{j+1} and D_{j+1}), none with j+2
+// (its rows start at r_j + 2w): wait until sweep s - 1 has done j + 2 tasks.
 // ---------------------------------------------------------------------------
 template <int NT, int WM>
 __global__ void __launch_bounds__(NT) sb2st_kernel(const Stage2Args a) {
@@ -174,8 +176,8 @@ __global__ void __launch_bounds__(NT) sb2st_kernel(const Stage2Args a) {
   for (int64_t s = blockIdx.x; s + 2 < n; s += gridDim.x) {
     int64_t r = s + 1;
     int L = (int)min((int64_t)w, n - r);
-    int task = 0;
-    wait_prev(a, s, LAG_SB);
+    int task = 0, seen = 0;
+    wait_prev(a, s, LAG_SB, seen);
     if (L >= 2) {
       // ---- task 0: annihilate column s below the subdiagonal ----
       for (int i = threadIdx.x; i < L; i += NT) v[i] = __ldcg(&a.A[(r + i) + s * a.lda]);
@@ -192,7 +194,7 @@ __global__ void __launch_bounds__(NT) sb2st_kernel(const Stage2Args a) {
         const int64_t rb = r + L;
         const int L2 = (int)min((int64_t)w, n - rb);
         if (L2 <= 0) break;
-        wait_prev(a, s, task + LAG_SB);
+        wait_prev(a, s, task + LAG_SB, seen);
         load_blk<NT, LDB>(B, a, rb, r, L2, L);
         // O := O H
         for (int i = threadIdx.x; i < L2; i += NT) {
@@ -248,12 +250,13 @@ __global__ void __launch_bounds__(NT) sb2st_kernel(const Stage2Args a) {
 }
 
 // ---------------------------------------------------------------------------
-// SVD: upper triangular band -> upper bidiagonal. Sweep s, task 0 touches
-// indices [s, s+2w] (row s's right reflector on columns s+1..s+w, rows
-// s..s+w; column s+1's left reflector on rows s+1..s+w, columns up to
-// s+2w); task j >= 1 (r = s+1+(j-1)w, c0 = r+w) touches rows [r, c0+w) and
-// columns [c0, c0+2w): indices [r, r+3w). Sweep s task j overlaps sweep s-1
-// tasks <= j+3: wait for j+4.
+// SVD: upper triangular band -> upper bidiagonal. Sweep s task j >= 1
+// (r = s+1+(j-1)w, c0 = r+w) writes rows [r, c0+w) x cols [c0, c0+w) (the
+// right reflector of row r) and rows [c0, c0+w) x cols [c0, c0+2w) (the left
+// reflector of column c0); task 0 the same shape from row s / column s+1.
+// Sweep s+1 task j shares elements with sweep s tasks up to j+2 (the single
+// element (c0+w, c0+2w) of task j+2), none with j+3 (its rows start at
+// c0 + 2w): wait until sweep s - 1 has done j + 3 tasks.
 // ---------------------------------------------------------------------------
 template <int NT, int WM>
 __global__ void __launch_bounds__(NT) tb2bd_kernel(const Stage2Args a) {
@@ -309,8 +312,8 @@ __global__ void __launch_bounds__(NT) tb2bd_kernel(const Stage2Args a) {
     }
   };
   for (int64_t s = blockIdx.x; s + 1 < n; s += gridDim.x) {
-    int task = 0;
-    wait_prev(a, s, LAG_BD);
+    int task = 0, seen = 0;
+    wait_prev(a, s, LAG_BD, seen);
     // ---- task 0 ----
     const int L = (int)min((int64_t)w, n - s - 1);
     if (L >= 2) {  // right reflector on row s
@@ -337,7 +340,7 @@ __global__ void __launch_bounds__(NT) tb2bd_kernel(const Stage2Args a) {
         const int64_t c0 = r + Lr;
         const int L2 = (int)min((int64_t)w, n - c0);
         if (L2 <= 0) break;
-        wait_prev(a, s, task + LAG_BD);
+        wait_prev(a, s, task + LAG_BD, seen);
         if (L2 >= 2) {  // right reflector on row r, columns [c0, c0+L2)
           for (int c = threadIdx.x; c < L2; c += NT) v[c] = __ldcg(&a.A[r + (c0 + c) * a.lda]);
           __syncthreads();
