@@ -174,6 +174,23 @@ __device__ __forceinline__ void dgemm_tile(const GemmArgs& g, const unsigned bx,
   for (int i = 0; i < MI; ++i)
 #pragma unroll
     for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  // EPI_LOWER: first row written in each of this thread's columns (its
+  // global column: itself, or the block-cyclic map), formed once per thread
+  // under a uniform branch so the plain SYR2K pays no division
+  int64_t cthr[NI][2];
+  if constexpr (EPI == EPI_LOWER) {
+    if (cyc) {
+#pragma unroll
+      for (int j = 0; j < NI; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) cthr[j][h] = cyc_map(g, n0 + wn + j * 8 + 2 * tq + h);
+    } else {
+#pragma unroll
+      for (int j = 0; j < NI; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) cthr[j][h] = n0 + wn + j * 8 + 2 * tq + h;
+    }
+  }
   if (cpre) {
 #pragma unroll
     for (int i = 0; i < MI; ++i) {
@@ -183,7 +200,7 @@ __device__ __forceinline__ void dgemm_tile(const GemmArgs& g, const unsigned bx,
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int64_t c = n0 + wn + j * 8 + 2 * tq + h;
-          const bool ok = r < g.M && c < nmax && (EPI != EPI_LOWER || r >= (cyc ? cyc_map(g, c) : c));
+          const bool ok = r < g.M && c < nmax && (EPI != EPI_LOWER || r >= cthr[j][h]);
           if (ok) acc[i][j][h] = (EPI == EPI_LOWER || g.beta == 1.0)
                                      ? g.Cin[r + c * g.ldcin]
                                      : g.beta * g.Cin[r + c * g.ldcin];
@@ -371,7 +388,7 @@ __device__ __forceinline__ void dgemm_tile(const GemmArgs& g, const unsigned bx,
         } else if (EPI == EPI_SPLIT) {
           g.ws[((int64_t)bz * g.N + c) * g.M + r] = v;
         } else {
-          if (r >= (cyc ? cyc_map(g, c) : c)) g.C[r + c * g.ldc] = v;
+          if (r >= cthr[j][h]) g.C[r + c * g.ldc] = v;
         }
       }
     }
