@@ -1144,23 +1144,28 @@ static int factors_stage(Workspace& ws, const br_factors* hf, int64_t m, int64_t
   fs.m = m;
   fs.n = n;
   fs.b = b;
-  const int64_t need = m * n + b * n + n + (right ? n * n + b * n + n : 0);
+  // only the requested members are staged (a tau-only request is n doubles)
+  const int64_t ny = hf->yl ? m * n : 0, nt = hf->tl ? b * n : 0, na = hf->taul ? n : 0;
+  const int64_t nyr = right && hf->yr ? n * n : 0, ntr = right && hf->tr ? b * n : 0,
+                nar = right && hf->taur ? n : 0;
+  const int64_t need = ny + nt + na + nyr + ntr + nar;
   BR_CHECK(devbuf_reserve(ws.stageF, need));
   BR_CUDA(cudaMemsetAsync(ws.stageF.p, 0, need * sizeof(double), ws.main));
   double* p = ws.stageF.p;
   br_factors& d = fs.dev;
-  d.yl = hf->yl ? p : nullptr, d.ldyl = m;
-  p += m * n;
-  d.tl = hf->tl ? p : nullptr, d.ldtl = b;
-  p += b * n;
-  d.taul = hf->taul ? p : nullptr;
-  p += n;
+  d = br_factors{};
+  d.yl = ny ? p : nullptr, d.ldyl = m;
+  p += ny;
+  d.tl = nt ? p : nullptr, d.ldtl = b;
+  p += nt;
+  d.taul = na ? p : nullptr;
+  p += na;
   if (right) {
-    d.yr = hf->yr ? p : nullptr, d.ldyr = n;
-    p += n * n;
-    d.tr = hf->tr ? p : nullptr, d.ldtr = b;
-    p += b * n;
-    d.taur = hf->taur ? p : nullptr;
+    d.yr = nyr ? p : nullptr, d.ldyr = n;
+    p += nyr;
+    d.tr = ntr ? p : nullptr, d.ldtr = b;
+    p += ntr;
+    d.taur = nar ? p : nullptr;
   }
   return 0;
 }

@@ -116,6 +116,20 @@ def alloc_host(m, n, b, right):
     return f, arrs
 
 
+def alloc_tau(n, right):
+    """Only the reflector scalars (n doubles per chain): what the wrappers
+    need for the reference-exact flop count when factors are not requested."""
+    taul = np.zeros(n)
+    arrs = {"taul": taul}
+    f = _lib.BrFactors()
+    f.taul = taul.ctypes.data
+    if right:
+        taur = np.zeros(n)
+        arrs["taur"] = taur
+        f.taur = taur.ctypes.data
+    return f, arrs
+
+
 def sevp_panels(n, w, b, max_iters=None):
     """(k, r0, rows, cols) of every SEVP panel (ref sevp.py:110-122, 128-134)."""
     out, k = [], 0

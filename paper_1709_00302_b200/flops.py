@@ -5,13 +5,16 @@ skipped when a dimension is 0 or alpha == 0; ref kernels.py:53-60) and
 every `house_gen` (3*L; ref kernels.py:98), keyed "matmul" / "house"
 (ref flops.py:12-49). The GPU path has no such per-call hook, so this module
 walks the same task decomposition on the host and sums the same formulas.
-The count is exact for inputs whose panels have no exactly-zero columns
-(tau != 0); a tau == 0 column makes the reference skip a few small rank-1
-products that this count still includes.
+A tau == 0 column (an exactly-zero panel column) makes the reference skip
+a few small products; `tau_zero_correction` subtracts them given the
+reductions' tau values (the wrappers fetch tau through the C ABI's factor
+output), so the totals equal the reference's on every input.
 """
 from __future__ import annotations
 
 import threading
+
+import numpy as np
 
 SYM_STRIP = 64  # ref kernels.py:30 (syr2k strip width)
 
@@ -215,6 +218,34 @@ def band_counted_flops(m, n, w, b, simultaneous=False, inner_b=16):
         k += bp
         it += 1
     return acc.as_dict(), it
+
+
+def tau_zero_correction(panels, tau, inner_b=16):
+    """matmul flops the reference does NOT count for tau == 0 reflectors:
+    the rank-1 update of the inner block (`if ... ti != 0.0`, ref
+    kernels.py:196-201 / 244-249) and _t_extend's second product, whose
+    alpha = -tau = 0 returns before counting (ref kernels.py:161, 57-60).
+    panels: (k, r0, rows, cols) per panel of one chain, tau[k:k+cols] its
+    reflector scalars."""
+    corr = 0
+    tau = np.asarray(tau)
+    for k, _r0, j, bp in panels:
+        for i in np.nonzero(tau[k:k + bp] == 0.0)[0]:
+            i = int(i)
+            e = min((i // inner_b) * inner_b + inner_b, bp)
+            if i + 1 < e:
+                corr += 4 * (j - i) * (e - i - 1)
+            if i > 0:
+                corr += 2 * i * i
+    return corr
+
+
+def apply_correction(flops, corr):
+    """Subtract tau == 0 skips from a counted-flop dict (in place)."""
+    if corr:
+        flops["matmul"] = flops.get("matmul", 0) - corr
+        flops["total"] = flops.get("total", 0) - corr
+    return flops
 
 
 def sevp_nominal_flops(n):

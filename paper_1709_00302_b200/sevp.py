@@ -23,7 +23,7 @@ import numpy as np
 
 from . import _dev, _lib
 from . import factors as _factors
-from .flops import FLOPS, sevp_counted_flops, sevp_nominal_flops  # noqa: F401
+from .flops import FLOPS, apply_correction, sevp_counted_flops, sevp_nominal_flops, tau_zero_correction  # noqa: F401
 
 
 class SevpVariant(Enum):
@@ -105,15 +105,16 @@ def reduce_sym_band(A, cfg, groups=None, *, lookahead=None, device=None, stats=N
     if A.shape[0] != cfg.n:
         raise ValueError(f"cfg.n={cfg.n} does not match matrix order {A.shape[0]}")
     depth = _depth(cfg, groups, lookahead)
+    ks = _schedule(cfg.n, cfg.w, cfg.b)
+    if not ks:  # n <= w + 1: the copy, unchanged (ref sevp.py:302-305); no arithmetic
+        return SevpResult(band=A, q=None, flops={"total": 0}, iterations=0)
     lib = _lib.load()
     h, _ = _dev.ctx(device)
-    ks = _schedule(cfg.n, cfg.w, cfg.b)
-    if not ks:
-        return SevpResult(band=A, q=None, flops={"total": 0}, iterations=0)
     n = cfg.n
     band = np.empty((n, n), order="F")
     Q = np.empty((n, n), order="F") if cfg.accumulate_q else None
-    fo, arrs = _factors.alloc_host(n, n, cfg.b, False) if return_factors else (None, None)
+    fo, arrs = (_factors.alloc_host(n, n, cfg.b, False) if return_factors
+                else _factors.alloc_tau(n, False))
     st = _lib.BrStats()
     rc = _dev.run_traced(h, groups, lambda: lib.br_reduce_sym_band_host(
         h, n, cfg.w, cfg.b, depth, A.ctypes.data, n, band.ctypes.data, n,
@@ -121,6 +122,8 @@ def reduce_sym_band(A, cfg, groups=None, *, lookahead=None, device=None, stats=N
     _lib.check(rc, "reduce_sym_band")
     variant = {SevpVariant.REFERENCE: "reference", SevpVariant.V1: "v1", SevpVariant.V2: "v2"}[cfg.variant]
     flops, iters = sevp_counted_flops(n, cfg.w, cfg.b, variant, cfg.accumulate_q, cfg.inner_b)
+    apply_correction(flops, tau_zero_correction(_factors.sevp_panels(n, cfg.w, cfg.b), arrs["taul"],
+                                                cfg.inner_b))
     for key, val in flops.items():
         if key != "total":
             FLOPS.add(key, val)

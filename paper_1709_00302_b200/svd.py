@@ -26,7 +26,8 @@ import numpy as np
 
 from . import _dev, _lib
 from . import factors as _factors
-from .flops import FLOPS, band_counted_flops, svd_nominal_flops, tri_counted_flops  # noqa: F401
+from .flops import (FLOPS, apply_correction, band_counted_flops, svd_nominal_flops,  # noqa: F401
+                    tau_zero_correction, tri_counted_flops)
 from .sevp import V2Mapping
 
 
@@ -129,12 +130,15 @@ def reduce_tri_band(A, w, b, groups=None, range_log=None, inner_b=16, *, lookahe
                          form=SvdForm.TRIANGULAR_BAND, lower_bw=w, upper_bw=0,
                          iterations=inner.iterations, factors=_swap(inner.factors))
     band = np.empty((m, n), order="F")
-    fo, arrs = _factors.alloc_host(m, n, b, True) if return_factors else (None, None)
+    fo, arrs = _factors.alloc_host(m, n, b, True) if return_factors else _factors.alloc_tau(n, True)
     st = _lib.BrStats()
     rc = _dev.run_traced(h, groups, lambda: lib.br_reduce_tri_band_host(
         h, m, n, w, b, depth, A.ctypes.data, m, band.ctypes.data, m, fo, st))
     _lib.check(rc, "reduce_tri_band")
     flops, _ = tri_counted_flops(m, n, w, b, inner_b)
+    pl, pr = _factors.tri_panels(m, n, w, b)
+    apply_correction(flops, tau_zero_correction(pl, arrs["taul"], inner_b) +
+                     tau_zero_correction(pr, arrs["taur"], inner_b))
     for key, val in flops.items():
         if key != "total":
             FLOPS.add(key, val)
@@ -142,7 +146,7 @@ def reduce_tri_band(A, w, b, groups=None, range_log=None, inner_b=16, *, lookahe
         stats.update(device_ms=st.device_ms, launches=st.launches, iterations=st.iterations)
     return SvdResult(band=band, flops=flops, form=SvdForm.TRIANGULAR_BAND, lower_bw=0, upper_bw=w,
                      iterations=int(st.iterations),
-                     factors=_chains(arrs, _factors.tri_panels(m, n, w, b), m, n))
+                     factors=_chains(arrs if return_factors else None, (pl, pr), m, n))
 
 
 def _chains(arrs, panels, m, n):
@@ -196,7 +200,7 @@ def reduce_band_svd(A, cfg, groups=None, range_log=None, *, lookahead=None, devi
     lib = _lib.load()
     h, _ = _dev.ctx(device)
     band = np.empty((m, n), order="F")
-    fo, arrs = _factors.alloc_host(m, n, b, True) if return_factors else (None, None)
+    fo, arrs = _factors.alloc_host(m, n, b, True) if return_factors else _factors.alloc_tau(n, True)
     st = _lib.BrStats()
     rc = _dev.run_traced(h, groups, lambda: lib.br_reduce_band_host(
         h, m, n, w, b, int(simultaneous), depth, A.ctypes.data, m, band.ctypes.data, m, fo, st))
@@ -205,6 +209,9 @@ def reduce_band_svd(A, cfg, groups=None, range_log=None, *, lookahead=None, devi
         flops = {"total": 0}
     else:
         flops, _ = band_counted_flops(m, n, w, b, simultaneous, cfg.inner_b)
+        pl, pr = _factors.band_panels(m, n, w, b)
+        apply_correction(flops, tau_zero_correction(pl, arrs["taul"], cfg.inner_b) +
+                         tau_zero_correction(pr, arrs["taur"], cfg.inner_b))
         for key, val in flops.items():
             if key != "total":
                 FLOPS.add(key, val)
@@ -212,4 +219,5 @@ def reduce_band_svd(A, cfg, groups=None, range_log=None, *, lookahead=None, devi
         stats.update(device_ms=st.device_ms, launches=st.launches, iterations=st.iterations)
     return SvdResult(band=band, flops=flops, form=SvdForm.BAND, lower_bw=w, upper_bw=w,
                      iterations=int(st.iterations),
-                     factors=_chains(arrs, _factors.band_panels(m, n, w, b), m, n))
+                     factors=_chains(arrs if return_factors else None, _factors.band_panels(m, n, w, b),
+                                     m, n))

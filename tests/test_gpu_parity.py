@@ -687,3 +687,36 @@ def test_band_svd_tall_vs_oracle(br):
     band, _, _, _ = O.reduce_band_svd(A, 16, 16, simultaneous=True)
     assert br.band_check(res.band, 16, 16) == 0.0
     assert rel(res.band, band, np.linalg.norm(A)) <= 1e-12 * np.sqrt(40000)
+
+
+# --- counted flops with tau == 0 panel columns (exactly-zero columns) --------
+# The reference skips a few small products for tau == 0 reflectors; the
+# wrappers fetch tau through the C ABI and subtract them (flops.py), so
+# result.flops equals the reference's on these inputs too (golden counts made
+# by the reference: tests/golden/make_golden_tau0.py).
+
+TAU0 = np.load(os.path.join(G, "tau0_flops.npz"))
+
+
+@pytest.mark.parametrize("name", ["diag40", "zcols48"])
+def test_flops_with_zero_columns_equal_reference(br, name):
+    A = TAU0[f"{name}_A"]
+    n = A.shape[0]
+    checked = 0
+    for key in TAU0.files:
+        if not key.startswith(name + "_") or key.endswith("_A"):
+            continue
+        parts = key[len(name) + 1:].split("_")
+        kind, w, b = parts[0], int(parts[1]), int(parts[2])
+        want = int(TAU0[key][0])
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            if kind == "sevp":
+                res = br.reduce_sym_band(A, br.SevpConfig(n, w, b, getattr(br.SevpVariant, parts[3])))
+            elif kind == "tri":
+                res = br.reduce_tri_band(A, w, b)
+            else:
+                res = br.reduce_band_svd(A, br.SvdConfig(n, n, w, b, variant=getattr(br.SvdVariant, parts[3])))
+        assert res.flops["total"] == want, (key, res.flops["total"], want)
+        checked += 1
+    assert checked >= 10
