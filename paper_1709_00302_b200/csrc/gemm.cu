@@ -148,7 +148,8 @@ static int64_t pick_kps(int cfg, const Scratch& ws, const GemmArgs& g, int max_c
 // for the whole product (gemm_plan_kps), so every element is summed in the
 // same order whatever the pieces are (bitwise split invariance).
 static int run_gemm(int am, cudaStream_t st, Scratch& ws, GemmArgs g, bool btrans, int max_ctas,
-                    int64_t fixed_kps, const double* tt = nullptr, int64_t ldtt = 0) {
+                    int64_t fixed_kps, const double* tt = nullptr, int64_t ldtt = 0,
+                    bool cyc = false) {
   if (g.M <= 0 || g.N <= 0) return 0;
   if (g.K <= 0) {  // C = beta*Cin
     const int64_t total = g.M * g.N;
@@ -158,7 +159,11 @@ static int run_gemm(int am, cudaStream_t st, Scratch& ws, GemmArgs g, bool btran
                        (const double*)nullptr, g.alpha, g.beta, g.Cin, g.ldcin, g.C, g.ldc));
     return 0;
   }
-  const int cfg = pick_cfg(am, g);
+  // block-cyclic staircase products run the GF_CYC instantiations (config G)
+  const int cfg = cyc ? CFG_G : pick_cfg(am, g);
+  auto lt = [&](int c, int a, int bm_, int e, cudaStream_t s_, const GemmArgs& g_, dim3 gr) {
+    return cyc ? launch_tile_cyc(c, a, bm_, e, s_, g_, gr) : launch_tile(c, a, bm_, e, s_, g_, gr);
+  };
   const int bm = kTiles[cfg].bm, bn = kTiles[cfg].bn;
   const int sms = ws.num_sms;
   int64_t kps = fixed_kps > 0 ? std::min(fixed_kps, g.K) : pick_kps(cfg, ws, g, max_ctas);
@@ -177,17 +182,17 @@ static int run_gemm(int am, cudaStream_t st, Scratch& ws, GemmArgs g, bool btran
       return -1;
     }
     g.ws = ws.p;
-    BR_CHECK(launch_tile(cfg, am, bmd, EPI_SPLIT, st, g, grid));
+    BR_CHECK(lt(cfg, am, bmd, EPI_SPLIT, st, g, grid));
     count_launch();
     BR_CUDA(launch_pdl(splitk_reduce_tt_kernel, dim3((unsigned)cdiv(g.N, TT_COLS)), dim3(256), 0, st, g.M,
                        g.N, (int)S, (const double*)ws.p, tt, ldtt, g.C, g.ldc));
     return 0;
   }
   if (S == 1) {
-    BR_CHECK(launch_tile(cfg, am, bmd, EPI_GEN, st, g, grid));
+    BR_CHECK(lt(cfg, am, bmd, EPI_GEN, st, g, grid));
   } else {
     g.ws = ws.p;
-    BR_CHECK(launch_tile(cfg, am, bmd, EPI_SPLIT, st, g, grid));
+    BR_CHECK(lt(cfg, am, bmd, EPI_SPLIT, st, g, grid));
     const int64_t total = g.M * g.N;
     int blocks = (int)std::min<int64_t>(cdiv(total, 256), (int64_t)sms * 8);
     count_launch();
@@ -450,7 +455,7 @@ int symm_cyclic(cudaStream_t st, Scratch& ws, MatView X1, MatView L, MatView W, 
   g.cyc_r0 = m.r0 - p0;
   g.cyc_bs = m.bs;
   g.cyc_stride = m.stride;
-  BR_CHECK(run_gemm(am, st, ws, g, bt, 0, 0));
+  BR_CHECK(run_gemm(am, st, ws, g, bt, 0, 0, nullptr, 0, true));
   if (cb == ca) return 0;
   // Xo = L[:, ca:cb]^T W (K from each column's first stored row)
   const CycCols ms{cyc_map(cg, ca), m.bs, m.stride};
@@ -459,7 +464,7 @@ int symm_cyclic(cudaStream_t st, Scratch& ws, MatView X1, MatView L, MatView W, 
   g.cyc_r0 = ms.r0;
   g.cyc_bs = ms.bs;
   g.cyc_stride = ms.stride;
-  BR_CHECK(run_gemm(am, st, ws, g, bt, 0, 0));
+  BR_CHECK(run_gemm(am, st, ws, g, bt, 0, 0, nullptr, 0, true));
   const int64_t total = (cb - ca) * b;
   const int blocks = (int)std::min<int64_t>(cdiv(total, 256), 148 * 8);
   count_launch();
@@ -508,9 +513,9 @@ int syr2k_cyclic(cudaStream_t st, MatView L, MatView X3, MatView Y, CycCols m, d
   g.cyc_stride = m.stride;
   g.vecA = al16(X3.p, X3.ld) && al16(Y.p, Y.ld) && (m.r0 % 2 == 0);
   g.vecB = al16(Yo, nc) && al16(Xo, nc);
-  const int cfg = lower_cfg(j - m.r0);
+  const int cfg = (j - m.r0) >= 4096 ? CFG_J : CFG_L;  // as lower_cfg; GF_CYC instantiations
   dim3 grid((unsigned)cdiv(j - m.r0, kTiles[cfg].bm), (unsigned)cdiv(nc, kTiles[cfg].bn), 1);
-  return launch_tile(cfg, A_N, B_T, EPI_LOWER, st, g, grid);
+  return launch_tile_cyc(cfg, A_N, B_T, EPI_LOWER, st, g, grid);
 }
 
 // Load every GEMM instantiation and the split-K reduction (see g_preload_only).
@@ -529,6 +534,10 @@ int preload_gemm_kernels() {
   cudaFuncAttributes fa;
   BR_CUDA(cudaFuncGetAttributes(&fa, splitk_reduce_kernel));
   BR_CUDA(cudaFuncGetAttributes(&fa, splitk_reduce_tt_kernel));
+  for (int am : {A_N, A_T})
+    for (int epi : {EPI_GEN, EPI_SPLIT}) BR_CHECK(launch_tile_cyc(CFG_G, am, B_N, epi, 0, g, grid));
+  BR_CHECK(launch_tile_cyc(CFG_J, A_N, B_T, EPI_LOWER, 0, g, grid));
+  BR_CHECK(launch_tile_cyc(CFG_L, A_N, B_T, EPI_LOWER, 0, g, grid));
   BR_CUDA(cudaFuncGetAttributes(&fa, cyc_gather_kernel));
   BR_CUDA(cudaFuncGetAttributes(&fa, cyc_fold_kernel));
   return 0;

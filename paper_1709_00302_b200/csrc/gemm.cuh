@@ -61,7 +61,6 @@ struct GemmArgs {
   // global index. cyc_bs == 0: off.
   int64_t cyc_r0;
   int cyc_bs, cyc_stride;
-  int no_trigger;  // persistent callers (xchain): no early PDL trigger from a tile
 };
 
 // Global column (= first stored row) of local column c under the map.

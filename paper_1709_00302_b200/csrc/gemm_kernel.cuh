@@ -120,8 +120,15 @@ __device__ __forceinline__ int sym_case(int64_t k0, int64_t m0, int BK, int BM) 
   return 2;
 }
 
+// Compile-time variants of a tile (FL bit mask; 0 for every hot-path
+// instantiation, so those compile exactly as without the variants):
+//   GF_CYC: the block-cyclic staircase map of GemmArgs.cyc_* (dist.py),
+//   GF_NOTRIG: no early PDL trigger (persistent callers, xchain.cu).
+enum GemmFlags { GF_CYC = 1, GF_NOTRIG = 2 };
+
 // One output tile (bx, by) of K-split bz.
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, int AM, int BMD, int EPI>
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, int AM, int BMD, int EPI,
+          int FL = 0>
 __device__ __forceinline__ void dgemm_tile(const GemmArgs& g, const unsigned bx, const unsigned by,
                                            const unsigned bz) {
   constexpr int NT = WM * WN * 32;
@@ -143,11 +150,17 @@ __device__ __forceinline__ void dgemm_tile(const GemmArgs& g, const unsigned bx,
   const int wm = (warp % WM) * WTM, wn = (warp / WM) * WTN;
 
   int64_t m0, n0, kbeg, kend;
-  const bool cyc = g.cyc_bs != 0;
+  constexpr bool cyc = (FL & GF_CYC) != 0;
   if (EPI == EPI_LOWER) {
-    m0 = (cyc ? g.cyc_r0 : g.c0) + (int64_t)bx * BM;
-    n0 = g.c0 + (int64_t)by * BN;
-    if (cyc ? (m0 + BM <= cyc_map(g, n0)) : (bx < by)) return;  // tile above the diagonal
+    if constexpr (cyc) {
+      m0 = g.cyc_r0 + (int64_t)bx * BM;
+      n0 = g.c0 + (int64_t)by * BN;
+      if (m0 + BM <= cyc_map(g, n0)) return;  // tile above the staircase
+    } else {
+      if (bx < by) return;
+      m0 = g.c0 + (int64_t)bx * BM;
+      n0 = g.c0 + (int64_t)by * BN;
+    }
     kbeg = 0;
     kend = g.K;
   } else {
@@ -156,7 +169,7 @@ __device__ __forceinline__ void dgemm_tile(const GemmArgs& g, const unsigned bx,
     kbeg = (int64_t)bz * g.k_per_split;
     kend = min(g.K, kbeg + g.k_per_split);
     if (BMD == B_N && g.b_upper) kend = max(kbeg, min(kend, n0 + BN));  // rows > n of B are 0
-    if (cyc) {  // block-cyclic staircase operand: skip its all-zero K range
+    if constexpr (cyc) {  // block-cyclic staircase operand: skip its all-zero K range
       if (AM == A_N) kend = max(kbeg, min(kend, cyc_count(g, m0 + BM - 1)));
       else if (AM == A_T) kbeg = min(kend, max(kbeg, cyc_map(g, m0) & ~(int64_t)1));
     }
@@ -174,23 +187,17 @@ __device__ __forceinline__ void dgemm_tile(const GemmArgs& g, const unsigned bx,
   for (int i = 0; i < MI; ++i)
 #pragma unroll
     for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  // EPI_LOWER: first row written in each of this thread's columns (its
-  // global column: itself, or the block-cyclic map), formed once per thread
-  // under a uniform branch so the plain SYR2K pays no division
-  int64_t cthr[NI][2];
-  if constexpr (EPI == EPI_LOWER) {
-    if (cyc) {
+  // EPI_LOWER with the block-cyclic map: first row written in each of this
+  // thread's columns (the column's global index), formed once per thread;
+  // without the map the test is r >= c, as before the map existed
+  int64_t cthr[cyc ? NI : 1][2];
+  if constexpr (EPI == EPI_LOWER && cyc) {
 #pragma unroll
-      for (int j = 0; j < NI; ++j)
+    for (int j = 0; j < NI; ++j)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) cthr[j][h] = cyc_map(g, n0 + wn + j * 8 + 2 * tq + h);
-    } else {
-#pragma unroll
-      for (int j = 0; j < NI; ++j)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) cthr[j][h] = n0 + wn + j * 8 + 2 * tq + h;
-    }
+      for (int h = 0; h < 2; ++h) cthr[j][h] = cyc_map(g, n0 + wn + j * 8 + 2 * tq + h);
   }
+#define BR_LOWER_OK(r, c, j, h) (cyc ? ((r) >= cthr[cyc ? (j) : 0][h]) : ((r) >= (c)))
   if (cpre) {
 #pragma unroll
     for (int i = 0; i < MI; ++i) {
@@ -200,7 +207,7 @@ __device__ __forceinline__ void dgemm_tile(const GemmArgs& g, const unsigned bx,
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int64_t c = n0 + wn + j * 8 + 2 * tq + h;
-          const bool ok = r < g.M && c < nmax && (EPI != EPI_LOWER || r >= cthr[j][h]);
+          const bool ok = r < g.M && c < nmax && (EPI != EPI_LOWER || BR_LOWER_OK(r, c, j, h));
           if (ok) acc[i][j][h] = (EPI == EPI_LOWER || g.beta == 1.0)
                                      ? g.Cin[r + c * g.ldcin]
                                      : g.beta * g.Cin[r + c * g.ldcin];
@@ -363,7 +370,7 @@ __device__ __forceinline__ void dgemm_tile(const GemmArgs& g, const unsigned bx,
     }
   }
   cp_async_wait<0>();
-  if (!g.no_trigger) pdl_trigger();  // the next kernel may start launching during the epilogue
+  if constexpr (!(FL & GF_NOTRIG)) pdl_trigger();  // the next kernel may start launching during the epilogue
 
   // ---- epilogue ----
 #pragma unroll
@@ -388,19 +395,21 @@ __device__ __forceinline__ void dgemm_tile(const GemmArgs& g, const unsigned bx,
         } else if (EPI == EPI_SPLIT) {
           g.ws[((int64_t)bz * g.N + c) * g.M + r] = v;
         } else {
-          if (r >= cthr[j][h]) g.C[r + c * g.ldc] = v;
+          if (BR_LOWER_OK(r, c, j, h)) g.C[r + c * g.ldc] = v;
         }
       }
     }
   }
+#undef BR_LOWER_OK
 }
 
 
 
 // One CTA per tile.
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, int AM, int BMD, int EPI>
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, int AM, int BMD, int EPI,
+          int FL = 0>
 __global__ void __launch_bounds__(WM* WN * 32, MINB) dgemm_kernel(const GemmArgs g) {
-  dgemm_tile<BM, BN, BK, WM, WN, STAGES, MINB, AM, BMD, EPI>(g, blockIdx.x, blockIdx.y, blockIdx.z);
+  dgemm_tile<BM, BN, BK, WM, WN, STAGES, MINB, AM, BMD, EPI, FL>(g, blockIdx.x, blockIdx.y, blockIdx.z);
 }
 
 template <int BM, int BN, int BK, int STAGES, int AM, int BMD>
@@ -413,10 +422,11 @@ constexpr int smem_bytes() {
   return STAGES * (A_STAGE + B_STAGE) * 8;
 }
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, int AM, int BMD, int EPI>
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, int AM, int BMD, int EPI,
+          int FL = 0>
 static int launch(cudaStream_t st, const GemmArgs& g, dim3 grid) {
   constexpr int smem = smem_bytes<BM, BN, BK, STAGES, AM, BMD>();
-  auto kern = dgemm_kernel<BM, BN, BK, WM, WN, STAGES, MINB, AM, BMD, EPI>;
+  auto kern = dgemm_kernel<BM, BN, BK, WM, WN, STAGES, MINB, AM, BMD, EPI, FL>;
   static int attr_dev_mask = 0;  // per-instantiation, per-device
   int dev = 0;
   BR_CUDA(cudaGetDevice(&dev));

@@ -48,6 +48,9 @@ int launch_tile_G(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, 
 int launch_tile_H(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
 int launch_tile_J(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
 int launch_tile_K(int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
+// block-cyclic (GF_CYC) instantiations: config G (A_N / A_T, B_N, GEN /
+// SPLIT) and the LOWER epilogue on configs J / L (gemm_tile_CYC.cu)
+int launch_tile_cyc(int cfg, int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g, dim3 grid);
 
 inline int launch_tile(int cfg, int am, int bmd, int epi, cudaStream_t st, const GemmArgs& g,
                        dim3 grid) {

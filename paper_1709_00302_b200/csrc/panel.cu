@@ -145,11 +145,11 @@ static int launch_leaf_t(cudaStream_t st, const LeafArgs& a) {
   return 0;
 }
 
-// 2D-layout leaf (leaf2_kernel): NW warps of 8 columns x 256 rows each.
-template <int NB, int NW>
+// 2D-layout leaf (leaf2_kernel): NW warps of 8 columns x 32 RPT rows each.
+template <int NB, int NW, int RPT = 8>
 static int launch_leaf2_t(cudaStream_t st, const LeafArgs& a) {
-  auto kern = leaf2_kernel<NB, NW>;
-  constexpr int ROWS = (NW / (NB / 8)) * 256;
+  auto kern = leaf2_kernel<NB, NW, RPT>;
+  constexpr int ROWS = (NW / (NB / 8)) * 32 * RPT;
   int C = 1;
   while (C < cdiv(a.L, ROWS)) C *= 2;
   const size_t smem = ((size_t)NB * (ROWS + 8) + 2 * (size_t)NB * (NB + 1)) * sizeof(double);
@@ -199,6 +199,17 @@ static int leaf2_mode() {
   return m;
 }
 
+// Rows per thread of the 2D leaf (BR_LEAF_RPT=4: 4 rows x 8 columns per
+// thread with twice the warps over the same rows; default 8).
+static int leaf_rpt() {
+  static int r = -1;
+  if (r < 0) {
+    const char* e = std::getenv("BR_LEAF_RPT");
+    r = (e && std::atoi(e) == 4) ? 4 : 8;
+  }
+  return r;
+}
+
 // Launch the 2D-layout leaf when it covers (nb, L) (sets *done).
 static int launch_leaf2(cudaStream_t st, const LeafArgs& a, bool* done) {
   const int mode = leaf2_mode();
@@ -206,6 +217,15 @@ static int launch_leaf2(cudaStream_t st, const LeafArgs& a, bool* done) {
   if (mode == 0 || a.nleaves != 1) return *done = false, 0;
   const int64_t L = a.L;
   const bool wide = mode == 2;
+  if (leaf_rpt() == 4 && !wide) {
+    if (a.nb > 16 && a.nb <= 32) {
+      if (L <= (int64_t)LEAF_MAXC * 256) return launch_leaf2_t<32, 8, 4>(st, a);
+      if (L <= (int64_t)LEAF_MAXC * 512) return launch_leaf2_t<32, 16, 4>(st, a);
+    } else if (a.nb > 8 && a.nb <= 16) {
+      if (L <= 256) return launch_leaf2_t<16, 4, 4>(st, a);
+      if (L <= (int64_t)LEAF_MAXC * 512) return launch_leaf2_t<16, 8, 4>(st, a);
+    }
+  }
   if (a.nb > 32) {
     if (a.nb <= 64 && L <= (int64_t)LEAF_MAXC * 256) return launch_leaf2_t<64, 8>(st, a);
     return *done = false, 0;
@@ -772,6 +792,10 @@ int preload_panel_kernels() {
   BR_CHECK((launch_leaf2_t<16, 2>(0, a)));
   BR_CHECK((launch_leaf2_t<16, 4>(0, a)));
   BR_CHECK((launch_leaf2_t<16, 8>(0, a)));
+  BR_CHECK((launch_leaf2_t<32, 8, 4>(0, a)));
+  BR_CHECK((launch_leaf2_t<32, 16, 4>(0, a)));
+  BR_CHECK((launch_leaf2_t<16, 4, 4>(0, a)));
+  BR_CHECK((launch_leaf2_t<16, 8, 4>(0, a)));
   cudaFuncAttributes fa;
   BR_CUDA(cudaFuncGetAttributes(&fa, t_assemble_kernel));
   BR_CUDA(cudaFuncGetAttributes(&fa, house_gen_kernel));

@@ -14,9 +14,9 @@ __device__ __forceinline__ void st_async_f64(uint32_t raddr, double a, uint32_t 
 // One leaf (L x nb, nb <= NB, NB in {8, 16, 32, 64}) of a Householder panel, same
 // outputs and arithmetic contract as leaf_reg_kernel (Y, tau, T, W, R rows of
 // P), with a 2D layout: warp w owns the 8 columns 8*(w % CG) .. +8 (CG = NB/8
-// column groups) of the 256 rows of its row group rg = w / CG, and lane l of
-// it rows rg*256 + 32 r + l (r < 8) of the CTA's block: 8 x 8 doubles per
-// thread. The warps owning the current column rotate their 8 register
+// column groups) of the 32 RPT rows of its row group rg = w / CG, and lane l
+// of it rows rg*32*RPT + 32 r + l (r < RPT) of the CTA's block: RPT x 8
+// doubles per thread (RPT = 8, or 4 with twice the warps per row span). The warps owning the current column rotate their 8 register
 // columns by one per step, so every register index is compile-time in a
 // non-unrolled step loop (see below).
 //
@@ -36,11 +36,13 @@ __device__ __forceinline__ void st_async_f64(uint32_t raddr, double a, uint32_t 
 //      order: beta = -sign(x0)||x||, alpha_c = P_ic - (x^T P_c)/beta,
 //      v = x / (x0 - beta), and updates its columns.
 // Deterministic: all CTAs sum the same received vectors in the same order.
-template <int NB, int NW>
+template <int NB, int NW, int RPT = 8>
 __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
-  constexpr int CG = NB / 8;      // column groups
-  constexpr int RG = NW / CG;     // row groups (256 rows each)
-  constexpr int ROWS = RG * 256;  // rows per CTA
+  constexpr int CG = NB / 8;           // column groups
+  constexpr int RG = NW / CG;          // row groups (32 RPT rows each)
+  constexpr int RGR = 32 * RPT;        // rows per row group
+  constexpr int ROWS = RG * RGR;       // rows per CTA
+  static_assert(RPT % 2 == 0 && RPT >= (NB + 31) / 32, "rows per thread");
   constexpr int NT = NW * 32;
   // PRE: the RG row-group warps of a column group first combine their slot
   // partials through shared memory (named barrier), so each CTA pushes one
@@ -70,7 +72,7 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wcg = warp % CG, rg = warp / CG;
   const int64_t base = (int64_t)rank * ROWS;
-  const int lrow0 = rg * 256 + lane;  // local row of register row r: lrow0 + 32 r
+  const int lrow0 = rg * RGR + lane;  // local row of register row r: lrow0 + 32 r
   const int64_t gr0 = base + lrow0;
   const bool xch = (ncta > 1) || (RG > 1);
   const int nsrc = PRE ? (int)ncta : (int)ncta * RG;
@@ -98,13 +100,13 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
     mbar_init(&mbar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  double p[8][8];
+  double p[RPT][8];
   {
     // branch-free addressing of the (possibly transposed) view
     const int64_t rs = P.trans ? P.ld : 1, cs = P.trans ? 1 : P.ld;
     const double* pb = P.p + gr0 * rs + (int64_t)(wcg * 8) * cs;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
+    for (int r = 0; r < RPT; ++r) {
       const bool rok = gr0 + 32 * r < Lr;
 #pragma unroll
       for (int c = 0; c < 8; ++c)
@@ -172,7 +174,7 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
     // ---- 1. publish x (owner warps) and row i (CTA 0, row group 0, lane i) ----
     if (own) {
 #pragma unroll
-      for (int r = 0; r < 8; ++r) xs[buf][lrow0 + 32 * r] = (r < RB && above[r]) ? 0.0 : p[r][0];
+      for (int r = 0; r < RPT; ++r) xs[buf][lrow0 + 32 * r] = (r < RB && above[r]) ? 0.0 : p[r][0];
     }
 #pragma unroll
     for (int r = 0; r < RB; ++r)
@@ -192,12 +194,12 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
         }
     }
     // ---- 2. partial sums over this warp's rows ----
-    double xv[8], s[8];
+    double xv[RPT], s[8];
 #pragma unroll
-    for (int r = 0; r < 8; ++r) xv[r] = xs[buf][lrow0 + 32 * r];
+    for (int r = 0; r < RPT; ++r) xv[r] = xs[buf][lrow0 + 32 * r];
     double nr0 = 0.0, nr1 = 0.0;
 #pragma unroll
-    for (int r = 0; r < 8; r += 2) {
+    for (int r = 0; r < RPT; r += 2) {
       nr0 = fma(xv[r], xv[r], nr0);
       nr1 = fma(xv[r + 1], xv[r + 1], nr1);
     }
@@ -206,7 +208,7 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
     for (int c = 0; c < 8; ++c) {
       double t0 = 0.0, t1 = 0.0;
 #pragma unroll
-      for (int r = 0; r < 8; r += 2) {
+      for (int r = 0; r < RPT; r += 2) {
         t0 = fma(xv[r], p[r][c], t0);
         t1 = fma(xv[r + 1], p[r + 1][c], t1);
       }
@@ -297,12 +299,12 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
       double al[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) al[c] = __shfl_sync(FULL, alpha, 4 * c);
-      double vk[8];
+      double vk[RPT];
 #pragma unroll
-      for (int r = 0; r < 8; ++r) vk[r] = (r < RB && piv[r]) ? 1.0 : xv[r] * rinv;  // 0 above row i
+      for (int r = 0; r < RPT; ++r) vk[r] = (r < RB && piv[r]) ? 1.0 : xv[r] * rinv;  // 0 above row i
       if (own) {  // rotate: slot s <- slot s+1 updated; Y column i (R kept above) to slot 7
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
+        for (int r = 0; r < RPT; ++r) {
           const double x = p[r][0];
 #pragma unroll
           for (int c = 0; c < 7; ++c) p[r][c] = fma(-vk[r], al[c + 1], p[r][c + 1]);
@@ -310,7 +312,7 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
         }
       } else {
 #pragma unroll
-        for (int r = 0; r < 8; ++r)
+        for (int r = 0; r < RPT; ++r)
 #pragma unroll
           for (int c = 0; c < 8; ++c) p[r][c] = fma(-vk[r], al[c], p[r][c]);
       }
@@ -323,7 +325,7 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
 #pragma unroll 1
       for (int t = nb & 7; t < 8; ++t) {
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
+        for (int r = 0; r < RPT; ++r) {
           const double x = p[r][0];
 #pragma unroll
           for (int c = 0; c < 7; ++c) p[r][c] = p[r][c + 1];
@@ -339,7 +341,7 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
   // the other warps store Y; then warp 0 stores its own Y ----
   auto store_y = [&]() {
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
+    for (int r = 0; r < RPT; ++r) {
       const int lrow = lrow0 + 32 * r;
       const int64_t row = base + lrow;
 #pragma unroll

@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB) xchain_kernel(const XArgs x
   for (int wi = blockIdx.x; wi < nwork; wi += G) {
     const int bx = wi % x.tiles_m, rest = wi / x.tiles_m;
     const int by = rest % x.tiles_n, bz = rest / x.tiles_n;
-    dgemm_tile<BM, BN, BK, WM, WN, STAGES, MINB, A_SYM, B_N, EPI_SPLIT>(x.g, bx, by, bz);
+    dgemm_tile<BM, BN, BK, WM, WN, STAGES, MINB, A_SYM, B_N, EPI_SPLIT, GF_NOTRIG>(x.g, bx, by, bz);
     __syncthreads();  // shared memory reused by the next tile
   }
   grid_barrier(x.bar, G);
@@ -203,7 +203,6 @@ int xchain(cudaStream_t st, Scratch& ws, MatView X1, MatView X2, MatView X3, Mat
   g.vecA = (reinterpret_cast<uintptr_t>(A2.p) % 16 == 0) && (A2.ld % 2 == 0);
   g.vecB = (reinterpret_cast<uintptr_t>(W.p) % 16 == 0) && (W.ld % 2 == 0);
   g.ws = ws.p;
-  g.no_trigger = 1;
   x.j = j;
   x.b = b;
   x.tiles_m = (int)cdiv(j, bm);

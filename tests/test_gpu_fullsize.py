@@ -270,3 +270,30 @@ def test_c5_full(env):
     err = float((ea - eb).abs().max()) / float(ea.abs().max())
     print(f"c5 eigenvalues: max |diff| / ||A||_2 = {err:.2e}")
     assert err <= 1e-10
+
+
+def test_sevp_beyond_one_cluster(env):
+    """SEVP n = 34000 > 32768 + w: the first panels (up to 33744 rows) run
+    the 4-wide tall-panel leaves. Properties, look-ahead bitwise equality and
+    the accumulate_q backward error at full size."""
+    torch, lib, h = env
+    n, w, b = 34000, 256, 256
+    g = torch.Generator(device="cuda").manual_seed(34000)
+    ld = (n + 31) // 32 * 32
+    A0d = torch.randn((n, ld), dtype=torch.float64, device="cuda", generator=g)
+    A0d[:, :n] = (A0d[:, :n] + A0d[:, :n].T) * 0.5
+    Ad = A0d[:, :n].T
+    nA = _fro(Ad, torch)
+    Q = torch.empty_like(A0d)
+    d1, st = _run("sevp", A0d, ld, n, w, b, 1, h, lib, torch, Q=Q)
+    band = d1[:, :n]
+    assert _pattern(band, n, w, "sevp", torch) == 0.0
+    assert torch.equal(band, band.T)
+    assert abs(_fro(band, torch) - nA) <= 1e-12 * np.sqrt(n) * nA
+    d0, _ = _run("sevp", A0d, ld, n, w, b, 0, h, lib, torch)
+    assert torch.equal(d0[:, :n], band)
+    del d0
+    B, Qm = band.T, Q[:, :n].T
+    be = _fro(Ad - Qm @ B @ Qm.T, torch) / (n * EPS * nA)
+    print(f"sevp n=34000 backward error {be:.3f}")
+    assert be <= 10.0
