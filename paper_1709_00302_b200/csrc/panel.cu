@@ -324,9 +324,9 @@ extern "C" int br_leaf_prof_dump() {
   const double st = h[11] ? (double)h[11] : 1.0, nl = h[12] ? (double)h[12] : 1.0;
   printf("leaf phases (cycles/step over %lld steps): reduce %.0f sync1 %.0f push %.0f cbar %.0f "
          "scalars %.0f sync2 %.0f update %.0f | per leaf (%lld): prologue %.0f tail %.0f "
-         "cbar-exit+Y/R %.0f W %.0f\n",
+         "cbar-exit+Y/R (2D: tau+sync) %.0f W %.0f | 2D: store_y %.0f T %.0f\n",
          h[11], h[0] / st, h[1] / st, h[2] / st, h[3] / st, h[4] / st, h[5] / st, h[6] / st,
-         h[12], h[7] / nl, h[8] / nl, h[9] / nl, h[10] / nl);
+         h[12], h[7] / nl, h[8] / nl, h[9] / nl, h[10] / nl, h[13] / nl, h[14] / nl);
   cudaMemset(br::g_leaf_prof, 0, sizeof(h));
   return 0;
 }

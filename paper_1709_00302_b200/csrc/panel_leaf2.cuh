@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
 
 #ifdef BR_LEAF_PROF  // phase counters: build with BR_BUILD_PROF=1, run with BR_LEAF_PROF=1
   const bool pr = a.prof != nullptr && rank == 0 && tid == 0;
-  long long tp[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long tp[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long tc = pr ? clock64() : 0;
 #define BR_PHASE2(k)                \
   if (pr) {                         \
@@ -369,7 +369,35 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
     scal[tid][0] = (be != 0.0) ? (be - scal[tid][0]) / be : 0.0;
   }
   __syncthreads();
-  if (warp < NB / 32 || (NB < 32 && warp == 0)) {
+  BR_PHASE2(9);
+  if constexpr (NB <= 32) {
+    // Warp 0 stores its Y first (its register columns are then dead), then
+    // forms T row r = lane by the reference recurrence
+    //   T[r][i] = -tau_i sum_{c<i} T[r][c] G[c][i]   (ref kernels.py:152-162)
+    // in right-looking order: once T[r][c] is known it is folded into every
+    // later column's sum, so the dependent chain is one FMA + one multiply
+    // per column instead of a dot product per column.
+    store_y();
+    BR_PHASE2(13);
+    if (warp == 0) {
+      const int r = lane;
+      double acc[NB], tr[NB];
+#pragma unroll
+      for (int i = 0; i < NB; ++i) acc[i] = 0.0;
+#pragma unroll
+      for (int c = 0; c < NB; ++c) {
+        const double tc = (c < r || c >= nb) ? 0.0 : ((c == r) ? -scal[c][0] : -scal[c][0] * acc[c]);
+        tr[c] = tc;
+#pragma unroll
+        for (int i = c + 1; i < NB; ++i) acc[i] = fma(tc, G[c][i], acc[i]);
+      }
+      if (r < NB) {
+#pragma unroll
+        for (int c = 0; c < NB; ++c) Ts[r][c] = tr[c];
+      }
+    }
+    BR_PHASE2(14);
+  } else if (warp < NB / 32) {
     // T rows 32 warp + lane by the reference recurrence
     // T[r][i] = -tau_i sum_{c<i} T[r][c] G[c][i] (ref kernels.py:152-162)
     const int r = warp * 32 + lane;
@@ -447,6 +475,7 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
 #ifdef BR_LEAF_PROF
   if (pr) {
     for (int k = 0; k < 11; ++k) atomicAdd((unsigned long long*)&a.prof[k], (unsigned long long)tp[k]);
+    for (int k = 13; k < 15; ++k) atomicAdd((unsigned long long*)&a.prof[k], (unsigned long long)tp[k]);
     atomicAdd((unsigned long long*)&a.prof[11], (unsigned long long)nb);
     atomicAdd((unsigned long long*)&a.prof[12], 1ull);
   }
