@@ -199,13 +199,21 @@ static int leaf2_mode() {
   return m;
 }
 
-// Rows per thread of the 2D leaf (BR_LEAF_RPT=4: 4 rows x 8 columns per
-// thread with twice the warps over the same rows; default 8).
+// Rows per thread of the 2D leaf. Default (44): leaves of 257..2048 rows
+// run 4 rows x 8 columns per thread with the same 1 warp per SM
+// sub-partition and twice the CTAs of the 8-row layout (half the partial
+// sums and update per column step; the cluster exchange exists either way):
+// 2016 x 32 60.8 -> 57.6 us, 1024 x 32 59.3 -> 54.4, 2048 x 16 38.6 -> 35.0;
+// c1 5.36 -> 5.26 ms, c2 8.96 -> 8.44 ms. At <= 256 rows the 8-row layout
+// keeps the leaf in one CTA (no exchange) and stays. BR_LEAF_RPT=8: the
+// 8-row layout everywhere; BR_LEAF_RPT=4: 4 rows per thread with twice the
+// warps over the same rows (measured slower everywhere).
 static int leaf_rpt() {
   static int r = -1;
   if (r < 0) {
     const char* e = std::getenv("BR_LEAF_RPT");
-    r = (e && std::atoi(e) == 4) ? 4 : 8;
+    r = e ? std::atoi(e) : 44;
+    if (r != 4 && r != 8) r = 44;
   }
   return r;
 }
@@ -217,6 +225,10 @@ static int launch_leaf2(cudaStream_t st, const LeafArgs& a, bool* done) {
   if (mode == 0 || a.nleaves != 1) return *done = false, 0;
   const int64_t L = a.L;
   const bool wide = mode == 2;
+  if (leaf_rpt() == 44 && !wide && L > 256 && L <= (int64_t)LEAF_MAXC * 128) {
+    if (a.nb > 16 && a.nb <= 32) return launch_leaf2_t<32, 4, 4>(st, a);
+    if (a.nb > 8 && a.nb <= 16) return launch_leaf2_t<16, 2, 4>(st, a);
+  }
   if (leaf_rpt() == 4 && !wide) {
     if (a.nb > 16 && a.nb <= 32) {
       if (L <= (int64_t)LEAF_MAXC * 256) return launch_leaf2_t<32, 8, 4>(st, a);
@@ -793,6 +805,8 @@ int preload_panel_kernels() {
   BR_CHECK((launch_leaf2_t<16, 4>(0, a)));
   BR_CHECK((launch_leaf2_t<16, 8>(0, a)));
   BR_CHECK((launch_leaf2_t<32, 8, 4>(0, a)));
+  BR_CHECK((launch_leaf2_t<32, 4, 4>(0, a)));
+  BR_CHECK((launch_leaf2_t<16, 2, 4>(0, a)));
   BR_CHECK((launch_leaf2_t<32, 16, 4>(0, a)));
   BR_CHECK((launch_leaf2_t<16, 4, 4>(0, a)));
   BR_CHECK((launch_leaf2_t<16, 8, 4>(0, a)));

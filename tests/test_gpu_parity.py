@@ -486,7 +486,8 @@ def test_streamed_band_output_matches(br, kind):
 @pytest.mark.gpu
 def test_leaf_layouts_agree(tmp_path):
     """The 2D-layout leaf (default; 1 CTA without exchange, clusters of 4- or
-    8-warp CTAs, opt-in 64-wide leaves up to 4096 rows) and the 1D-layout leaf
+    8-warp CTAs with 8 or 4 rows per thread, opt-in 64-wide leaves up to 4096
+    rows, 4-row threads with twice the warps) and the 1D-layout leaf
     (BR_LEAF2=0, at most 32 wide) factor the same panels to rounding,
     including zero columns and zero tails."""
     import os
@@ -508,7 +509,7 @@ def test_leaf_layouts_agree(tmp_path):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
     for mode in ({"BR_LEAF2": "0"}, {"BR_LEAF2": "1"}, {"BR_LEAF2": "1", "BR_LEAF2_WIDE": "1"},
-                 {"BR_LEAF2": "1", "BR_LEAF64": "1"}):
+                 {"BR_LEAF2": "1", "BR_LEAF64": "1"}, {"BR_LEAF_RPT": "8"}, {"BR_LEAF_RPT": "4"}):
         path = tmp_path / f"leaf{len(outs)}.npz"
         env = dict(os.environ, **mode)
         r = subprocess.run([sys.executable, "-c", code % path], cwd=root, env=env,
