@@ -410,6 +410,13 @@ static int s2_max_ctas() {
   return e ? std::atoi(e) : 0;
 }
 
+// Threads per CTA for w <= 32 (BR_S2_THREADS = 32 / 64 / 128; tuning aid).
+static int s2_threads() {
+  const char* e = std::getenv("BR_S2_THREADS");
+  const int t = e ? std::atoi(e) : 128;
+  return (t == 32 || t == 64) ? t : 128;
+}
+
 int band_to_condensed(cudaStream_t st, bool bd, int64_t n, int64_t w, double* A, int64_t lda,
                       double* d, double* e, int* prog, int num_sms) {
   if (n < 1) return 0;
@@ -421,8 +428,12 @@ int band_to_condensed(cudaStream_t st, bool bd, int64_t n, int64_t w, double* A,
   Stage2Args a{n, (int)w, A, lda, prog, d, e};
   const int cap = s2_max_ctas();
   if (n > 2 || (bd && n > 1)) {
-    if (w <= 32) BR_CHECK((launch_stage2<128, 32>(bd, st, a, num_sms, cap)));
-    else if (w <= 64) BR_CHECK((launch_stage2<128, 64>(bd, st, a, num_sms, cap)));
+    if (w <= 32) {
+      const int nt = s2_threads();
+      if (nt == 32) BR_CHECK((launch_stage2<32, 32>(bd, st, a, num_sms, cap)));
+      else if (nt == 64) BR_CHECK((launch_stage2<64, 32>(bd, st, a, num_sms, cap)));
+      else BR_CHECK((launch_stage2<128, 32>(bd, st, a, num_sms, cap)));
+    } else if (w <= 64) BR_CHECK((launch_stage2<128, 64>(bd, st, a, num_sms, cap)));
     else BR_CHECK((launch_stage2<256, 128>(bd, st, a, num_sms, cap)));
   }
   const int blocks = (int)std::min<int64_t>(cdiv(n, 256), 1024);
@@ -435,6 +446,8 @@ int band_to_condensed(cudaStream_t st, bool bd, int64_t n, int64_t w, double* A,
 int preload_stage2_kernels() {
   Stage2Args a{};
   for (bool bd : {false, true}) {
+    BR_CHECK((launch_stage2<32, 32>(bd, 0, a, 148, 0)));
+    BR_CHECK((launch_stage2<64, 32>(bd, 0, a, 148, 0)));
     BR_CHECK((launch_stage2<128, 32>(bd, 0, a, 148, 0)));
     BR_CHECK((launch_stage2<128, 64>(bd, 0, a, 148, 0)));
     BR_CHECK((launch_stage2<256, 128>(bd, 0, a, 148, 0)));
