@@ -276,6 +276,145 @@ int gemm_tt(cudaStream_t st, Scratch& ws, MatView C, MatView A, MatView B, MatVi
   return run_gemm(am, st, ws, g, bt, 0, 0, T.p, T.ld);
 }
 
+// ---------------------------------------------------------------------------
+// Split-K products with a small update fused into their reduction pass (the
+// narrow-panel chains of the triangular band: Z_L then the LQ panel's rows,
+// Z_R then the next QR panel's columns). One launch instead of the split-K
+// reduction plus a small GEMM on the critical path of every iteration.
+// ---------------------------------------------------------------------------
+constexpr int FU_MAX = 64;   // max bp / bq / update width
+constexpr int FU_COLS = 16;  // columns of C per CTA (left form)
+constexpr int FU_ROWS = 16;  // rows of C per CTA (right form)
+
+// C (M x N, M <= 64) = sum_z ws[z] (fixed order), and D (pr x N) += P (pr x M) C.
+__global__ void __launch_bounds__(256) reduce_left_update_kernel(
+    int64_t M, int64_t N, int S, const double* __restrict__ ws, double* C, int64_t ldc,
+    const double* __restrict__ P, int64_t ldp, int pr, double* D, int64_t ldd) {
+  __shared__ double Ps[FU_MAX][FU_MAX + 1];
+  __shared__ double Cs[FU_MAX][FU_COLS + 1];
+  pdl_wait();
+  pdl_trigger();
+  const int tid = threadIdx.x;
+  const int64_t c0 = (int64_t)blockIdx.x * FU_COLS;
+  const int m = (int)M, nc = (int)min((int64_t)FU_COLS, N - c0);
+  for (int e = tid; e < pr * m; e += 256) {
+    const int r = e % pr, k = e / pr;
+    Ps[r][k] = P[r + (int64_t)k * ldp];
+  }
+  const int64_t tot = M * N;
+  for (int e = tid; e < m * nc; e += 256) {
+    const int k = e % m, c = e / m;
+    const double* src = ws + (c0 + c) * M + k;
+    double sacc = 0.0;
+    for (int z = 0; z < S; ++z) sacc += src[(int64_t)z * tot];
+    Cs[k][c] = sacc;
+    C[k + (c0 + c) * ldc] = sacc;
+  }
+  __syncthreads();
+  for (int e = tid; e < pr * nc; e += 256) {
+    const int r = e % pr, c = e / pr;
+    double* d = D + r + (c0 + c) * ldd;
+    double acc = *d;
+    for (int k = 0; k < m; ++k) acc = fma(Ps[r][k], Cs[k][c], acc);
+    *d = acc;
+  }
+}
+
+// C (M x N, N <= 64) = sum_z ws[z] (fixed order), and D (M x qc) += C Q^T
+// (Q qc x N).
+__global__ void __launch_bounds__(256) reduce_right_update_kernel(
+    int64_t M, int64_t N, int S, const double* __restrict__ ws, double* C, int64_t ldc,
+    const double* __restrict__ Q, int64_t ldq, int qc, double* D, int64_t ldd) {
+  __shared__ double Qs[FU_MAX][FU_MAX + 1];
+  __shared__ double Cs[FU_ROWS][FU_MAX + 1];
+  pdl_wait();
+  pdl_trigger();
+  const int tid = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.x * FU_ROWS;
+  const int n = (int)N, nr = (int)min((int64_t)FU_ROWS, M - r0);
+  for (int e = tid; e < qc * n; e += 256) {
+    const int q = e % qc, k = e / qc;
+    Qs[q][k] = Q[q + (int64_t)k * ldq];
+  }
+  const int64_t tot = M * N;
+  for (int e = tid; e < nr * n; e += 256) {
+    const int r = e % nr, k = e / nr;
+    const double* src = ws + (int64_t)k * M + r0 + r;
+    double sacc = 0.0;
+    for (int z = 0; z < S; ++z) sacc += src[(int64_t)z * tot];
+    Cs[r][k] = sacc;
+    C[(r0 + r) + (int64_t)k * ldc] = sacc;
+  }
+  __syncthreads();
+  for (int e = tid; e < nr * qc; e += 256) {
+    const int r = e % nr, q = e / nr;
+    double* d = D + (r0 + r) + (int64_t)q * ldd;
+    double acc = *d;
+    for (int k = 0; k < n; ++k) acc = fma(Cs[r][k], Qs[q][k], acc);
+    *d = acc;
+  }
+}
+
+// The split-K partials of C = op(A) op(B) (always through the workspace),
+// for the fused reductions below. Returns the number of splits in *S.
+static int splitk_partials(cudaStream_t st, Scratch& ws, MatView C, MatView A, MatView B, int* S) {
+  GemmArgs g;
+  int am = 0;
+  bool bt = false;
+  BR_CHECK(make_args(C, A, B, 1.0, 0.0, nullptr, g, am, bt));
+  if (g.K <= 0) {
+    set_error("fused split-K reduction needs K > 0");
+    return -1;
+  }
+  const int cfg = pick_cfg(am, g);
+  const int64_t kps = pick_kps(cfg, ws, g, 0);
+  const int64_t s = cdiv(g.K, kps);
+  if (s * g.M * g.N > ws.cap) {
+    set_error("fused split-K reduction: scratch too small");
+    return -1;
+  }
+  g.k_per_split = kps;
+  g.ws = ws.p;
+  dim3 grid((unsigned)cdiv(g.M, kTiles[cfg].bm), (unsigned)cdiv(g.N, kTiles[cfg].bn), (unsigned)s);
+  BR_CHECK(launch_tile(cfg, am, bt ? B_T : B_N, EPI_SPLIT, st, g, grid));
+  *S = (int)s;
+  return 0;
+}
+
+int gemm_left_update(cudaStream_t st, Scratch& ws, MatView C, MatView A, MatView B, MatView D,
+                     MatView P) {
+  if (C.trans || D.trans || P.trans || C.rows > FU_MAX || P.rows > FU_MAX || P.cols != C.rows ||
+      D.rows != P.rows || D.cols != C.cols) {
+    set_error("gemm_left_update: bad views");
+    return -1;
+  }
+  if (C.rows == 0 || C.cols == 0) return 0;
+  int S = 0;
+  BR_CHECK(splitk_partials(st, ws, C, A, B, &S));
+  count_launch();
+  BR_CUDA(launch_pdl(reduce_left_update_kernel, dim3((unsigned)cdiv(C.cols, FU_COLS)), dim3(256), 0,
+                     st, C.rows, C.cols, S, (const double*)ws.p, C.p, C.ld, (const double*)P.p, P.ld,
+                     (int)P.rows, D.p, D.ld));
+  return 0;
+}
+
+int gemm_right_update(cudaStream_t st, Scratch& ws, MatView C, MatView A, MatView B, MatView D,
+                      MatView Q) {
+  if (C.trans || D.trans || Q.trans || C.cols > FU_MAX || Q.rows > FU_MAX || Q.cols != C.cols ||
+      D.rows != C.rows || D.cols != Q.rows) {
+    set_error("gemm_right_update: bad views");
+    return -1;
+  }
+  if (C.rows == 0 || C.cols == 0) return 0;
+  int S = 0;
+  BR_CHECK(splitk_partials(st, ws, C, A, B, &S));
+  count_launch();
+  BR_CUDA(launch_pdl(reduce_right_update_kernel, dim3((unsigned)cdiv(C.rows, FU_ROWS)), dim3(256), 0,
+                     st, C.rows, C.cols, S, (const double*)ws.p, C.p, C.ld, (const double*)Q.p, Q.ld,
+                     (int)Q.rows, D.p, D.ld));
+  return 0;
+}
+
 int64_t gemm_plan_kps(const Scratch& ws, MatView C, MatView A, MatView B, double beta) {
   GemmArgs g;
   int am = 0;
@@ -539,6 +678,8 @@ int preload_gemm_kernels() {
   BR_CHECK(launch_tile_cyc(CFG_J, A_N, B_T, EPI_LOWER, 0, g, grid));
   BR_CHECK(launch_tile_cyc(CFG_L, A_N, B_T, EPI_LOWER, 0, g, grid));
   BR_CUDA(cudaFuncGetAttributes(&fa, cyc_gather_kernel));
+  BR_CUDA(cudaFuncGetAttributes(&fa, reduce_left_update_kernel));
+  BR_CUDA(cudaFuncGetAttributes(&fa, reduce_right_update_kernel));
   BR_CUDA(cudaFuncGetAttributes(&fa, cyc_fold_kernel));
   return 0;
 }

@@ -96,6 +96,14 @@ int symm_lower(cudaStream_t st, Scratch& ws, MatView X1, MatView A2, MatView W,
 int syr2k_lower(cudaStream_t st, MatView A2, MatView X3, MatView Y, int64_t c0, int64_t c1,
                 int max_ctas = 0);
 
+// C = op(A) op(B) through split-K partials, and in the same reduction pass
+// D += P C (left; C at most 64 rows, P at most 64 x C.rows) or D += C Q^T
+// (right; C at most 64 columns, Q at most 64 x C.cols). Deterministic.
+int gemm_left_update(cudaStream_t st, Scratch& ws, MatView C, MatView A, MatView B, MatView D,
+                     MatView P);
+int gemm_right_update(cudaStream_t st, Scratch& ws, MatView C, MatView A, MatView B, MatView D,
+                      MatView Q);
+
 // Block-cyclic column slab of a j x j lower-stored trailing matrix (the
 // distributed SEVP): L is j x ncols, local column c being trailing column
 // r0 + (c / bs) * stride + c % bs, stored from that row down with zeros above.

@@ -72,6 +72,20 @@ static bool xchain_enabled() {
   return m == 1;
 }
 
+// Narrow panels (b <= 64): Z_L's split-K reduction also updates the LQ
+// panel's rows, Z_R's the next QR panel's columns (gemm_left_update /
+// gemm_right_update: one launch instead of reduction + small GEMM on the
+// panel chain). BR_FUSE_SMALL=0: separate kernels (A/B aid). Used by both
+// look-ahead depths, so they stay bitwise equal.
+static bool fuse_small() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = std::getenv("BR_FUSE_SMALL");
+    m = (e && std::atoi(e) == 0) ? 0 : 1;
+  }
+  return m == 1;
+}
+
 static double panel_flops(int64_t j, int64_t b) {
   return 2.0 * j * b * b - 2.0 * b * b * b / 3.0 + (double)j * b * b;  // QR + T/W
 }
@@ -447,8 +461,15 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
           BR_CHECK(band_in_wait(ws, bi, n));
           BR_CHECK(issue_lq());
         } else {
-          BR_CHECK(zleft());
-          {  // rows of the LQ panel first
+          if (fuse_small() && !pz && bp <= 64 && bq <= 64) {
+            // Z_L = W_U^T E and the LQ panel's rows E[0:bq] += Y_U[0:bq] Z_L in one reduction
+            TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(bp, ncE, i) + gemm_flops(bq, ncE, bp),
+                         "zleft+lq-rows", k);
+            BR_CHECK(gemm_left_update(ws.main, ws.sk_main, Z, Wuv.T(), E, E.sub(0, 0, bq, ncE),
+                                      Yuv.sub(0, 0, bq, bp)));
+          } else {
+            BR_CHECK(zleft());
+            // rows of the LQ panel first
             TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(bq, ncE, bp), "left-lq-rows", k);
             BR_CHECK(gemm(ws.main, ws.sk_main, E.sub(0, 0, bq, ncE), Yuv.sub(0, 0, bq, bp), Z, 1.0,
                           1.0));
@@ -467,7 +488,25 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
         MatView Yvv(Yv, n, jr, bq), Wvv(Wv, n, jr, bq);
         MatView Zr(ZR, m, i - bq, bq);
         if (pz && lookahead && i - bq <= 0) BR_CHECK(join(ev_lq));
-        if (i - bq > 0) {
+        const int64_t sc_f = std::min(splitc, jr);
+        const bool fuse_r = fuse_small() && !pz && bq <= 64 && has_next && !next_issued &&
+                            splitc > 0 && sc_f <= 64 && i - bq > 0;
+        if (fuse_r) {
+          // Z_R = D W_V and the next QR panel's columns D[:, 0:sc] += Z_R Y_V[0:sc]^T
+          // in one reduction, then (look-ahead) QR(k+1) and the rest of D
+          {
+            TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, bq, jr) + gemm_flops(i - bq, sc_f, bq),
+                         "zright+right-head", k);
+            BR_CHECK(gemm_right_update(ws.main, ws.sk_main, Zr, D, Wvv, D.sub(0, 0, i - bq, sc_f),
+                                       Yvv.sub(0, 0, sc_f, bq)));
+          }
+          if (la) BR_CHECK(next_qr_on_panel());
+          if (sc_f < jr) {
+            TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, jr - sc_f, bq), "right", k);
+            BR_CHECK(gemm(ws.main, ws.sk_main, D.sub(0, sc_f, i - bq, jr - sc_f), Zr,
+                          Yvv.sub(sc_f, 0, jr - sc_f, bq).T(), 1.0, 1.0));
+          }
+        } else if (i - bq > 0) {
           if (pz) {
             MatView Zrr(ZRr, m, i - bq, bq);
             for (int s = 0; s < mk_lq.n; ++s) {

@@ -47,6 +47,19 @@ __device__ __forceinline__ void st_release_i32(int* p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v / 2); }
+// Element loops over an R x C block (R <= LDB - 1, a power of two): the
+// row / column split is a mask and a shift, not a division by a runtime R.
+#define S2_FOR(R, C, body)                                                      \
+  {                                                                             \
+    constexpr int WMc = LDB - 1, SHc = ilog2c(LDB - 1);                         \
+    static_assert((WMc & (WMc - 1)) == 0, "block height a power of two");      \
+    for (int e = threadIdx.x; e < WMc * (C); e += NT) {                         \
+      const int i = e & (WMc - 1), c = e >> SHc;                                \
+      if (i < (R)) { body; }                                                    \
+    }                                                                           \
+  }
+
 template <int NT>
 __device__ __forceinline__ double block_sum(double v, double* red) {
   v = warp_sum(v);
@@ -98,44 +111,28 @@ __device__ void two_sided_smem(double* D, int L, const double* v, double tau, do
   const double a = 0.5 * tau * block_sum<NT>(p, red);
   for (int i = threadIdx.x; i < L; i += NT) y[i] = fma(-a, v[i], y[i]);  // y := w
   __syncthreads();
-  for (int e = threadIdx.x; e < L * L; e += NT) {
-    const int i = e % L, c = e / L;
-    D[c * LDB + i] -= __dadd_rn(__dmul_rn(v[i], y[c]), __dmul_rn(y[i], v[c]));
-  }
+  S2_FOR(L, L, D[c * LDB + i] -= __dadd_rn(__dmul_rn(v[i], y[c]), __dmul_rn(y[i], v[c])));
   __syncthreads();
 }
 
 // Symmetric block A[r0 : r0+L]^2 from its lower triangle into smem (full).
 template <int NT, int LDB>
 __device__ void load_sym(double* D, const Stage2Args& a, int64_t r0, int L) {
-  for (int e = threadIdx.x; e < L * L; e += NT) {
-    const int i = e % L, c = e / L;
-    const int lo = max(i, c), hi = min(i, c);
-    D[c * LDB + i] = __ldcg(&a.A[(r0 + lo) + (r0 + hi) * a.lda]);
-  }
+  S2_FOR(L, L, D[c * LDB + i] = __ldcg(&a.A[(r0 + max(i, c)) + (r0 + min(i, c)) * a.lda]));
   __syncthreads();
 }
 template <int NT, int LDB>
 __device__ void store_lower(const double* D, const Stage2Args& a, int64_t r0, int L) {
-  for (int e = threadIdx.x; e < L * L; e += NT) {
-    const int i = e % L, c = e / L;
-    if (i >= c) a.A[(r0 + i) + (r0 + c) * a.lda] = D[c * LDB + i];
-  }
+  S2_FOR(L, L, if (i >= c) a.A[(r0 + i) + (r0 + c) * a.lda] = D[c * LDB + i]);
 }
 template <int NT, int LDB>
 __device__ void load_blk(double* O, const Stage2Args& a, int64_t r0, int64_t c0, int R, int Cn) {
-  for (int e = threadIdx.x; e < R * Cn; e += NT) {
-    const int i = e % R, c = e / R;
-    O[c * LDB + i] = __ldcg(&a.A[(r0 + i) + (c0 + c) * a.lda]);
-  }
+  S2_FOR(R, Cn, O[c * LDB + i] = __ldcg(&a.A[(r0 + i) + (c0 + c) * a.lda]));
   __syncthreads();
 }
 template <int NT, int LDB>
 __device__ void store_blk(const double* O, const Stage2Args& a, int64_t r0, int64_t c0, int R, int Cn) {
-  for (int e = threadIdx.x; e < R * Cn; e += NT) {
-    const int i = e % R, c = e / R;
-    a.A[(r0 + i) + (c0 + c) * a.lda] = O[c * LDB + i];
-  }
+  S2_FOR(R, Cn, a.A[(r0 + i) + (c0 + c) * a.lda] = O[c * LDB + i]);
 }
 
 // `seen` (thread 0's register): the last progress value read for sweep
@@ -203,10 +200,7 @@ __global__ void __launch_bounds__(NT) sb2st_kernel(const Stage2Args a) {
           y[i] = tau * t;
         }
         __syncthreads();
-        for (int e = threadIdx.x; e < L2 * L; e += NT) {
-          const int i = e % L2, c = e / L2;
-          B[c * LDB + i] = fma(-y[i], v[c], B[c * LDB + i]);
-        }
+        S2_FOR(L2, L, B[c * LDB + i] = fma(-y[i], v[c], B[c * LDB + i]));
         __syncthreads();
         double tau2 = 0.0, beta2 = 0.0;
         if (L2 >= 2) {
@@ -220,11 +214,8 @@ __global__ void __launch_bounds__(NT) sb2st_kernel(const Stage2Args a) {
             y[c] = tau2 * t;
           }
           __syncthreads();
-          for (int e = threadIdx.x; e < L2 * L; e += NT) {
-            const int i = e % L2, c = e / L2;
-            if (c == 0) B[i] = (i == 0) ? beta2 : 0.0;
-            else B[c * LDB + i] = fma(-v2[i], y[c], B[c * LDB + i]);
-          }
+          S2_FOR(L2, L, if (c == 0) B[i] = (i == 0) ? beta2 : 0.0;
+                 else B[c * LDB + i] = fma(-v2[i], y[c], B[c * LDB + i]));
           __syncthreads();
         }
         store_blk<NT, LDB>(B, a, rb, r, L2, L);
@@ -281,10 +272,7 @@ __global__ void __launch_bounds__(NT) tb2bd_kernel(const Stage2Args a) {
         y[i] = tau * t;
       }
       __syncthreads();
-      for (int e = threadIdx.x; e < Rb * L; e += NT) {
-        const int i = e % Rb, c = e / Rb;
-        B[c * LDB + i] = fma(-y[i], v[c], B[c * LDB + i]);
-      }
+      S2_FOR(Rb, L, B[c * LDB + i] = fma(-y[i], v[c], B[c * LDB + i]));
       __syncthreads();
       store_blk<NT, LDB>(B, a, rr, c0, Rb, L);
       __syncthreads();
@@ -302,10 +290,7 @@ __global__ void __launch_bounds__(NT) tb2bd_kernel(const Stage2Args a) {
         y[c] = tau * t;
       }
       __syncthreads();
-      for (int e = threadIdx.x; e < L * Cb; e += NT) {
-        const int i = e % L, c = e / L;
-        B[c * LDB + i] = fma(-v[i], y[c], B[c * LDB + i]);
-      }
+      S2_FOR(L, Cb, B[c * LDB + i] = fma(-v[i], y[c], B[c * LDB + i]));
       __syncthreads();
       store_blk<NT, LDB>(B, a, r0, cc, L, Cb);
       __syncthreads();
@@ -410,11 +395,13 @@ static int s2_max_ctas() {
   return e ? std::atoi(e) : 0;
 }
 
-// Threads per CTA for w <= 32 (BR_S2_THREADS = 32 / 64 / 128; tuning aid).
+// Threads per CTA (BR_S2_THREADS = 128 / 256 / 512 / 1024; tuning aid).
+// The per-task element loops dominate: at n = 2048, w = 32 the tridiagonal
+// took 101 / 58.7 / 37.3 / 27.9 ms with 32 / 64 / 128 / 256 threads.
 static int s2_threads() {
   const char* e = std::getenv("BR_S2_THREADS");
-  const int t = e ? std::atoi(e) : 128;
-  return (t == 32 || t == 64) ? t : 128;
+  const int t = e ? std::atoi(e) : 256;
+  return (t == 128 || t == 512 || t == 1024) ? t : 256;
 }
 
 int band_to_condensed(cudaStream_t st, bool bd, int64_t n, int64_t w, double* A, int64_t lda,
@@ -428,13 +415,20 @@ int band_to_condensed(cudaStream_t st, bool bd, int64_t n, int64_t w, double* A,
   Stage2Args a{n, (int)w, A, lda, prog, d, e};
   const int cap = s2_max_ctas();
   if (n > 2 || (bd && n > 1)) {
+    const int nt = s2_threads();
     if (w <= 32) {
-      const int nt = s2_threads();
-      if (nt == 32) BR_CHECK((launch_stage2<32, 32>(bd, st, a, num_sms, cap)));
-      else if (nt == 64) BR_CHECK((launch_stage2<64, 32>(bd, st, a, num_sms, cap)));
-      else BR_CHECK((launch_stage2<128, 32>(bd, st, a, num_sms, cap)));
-    } else if (w <= 64) BR_CHECK((launch_stage2<128, 64>(bd, st, a, num_sms, cap)));
-    else BR_CHECK((launch_stage2<256, 128>(bd, st, a, num_sms, cap)));
+      if (nt == 128) BR_CHECK((launch_stage2<128, 32>(bd, st, a, num_sms, cap)));
+      else if (nt == 512) BR_CHECK((launch_stage2<512, 32>(bd, st, a, num_sms, cap)));
+      else BR_CHECK((launch_stage2<256, 32>(bd, st, a, num_sms, cap)));
+    } else if (w <= 64) {
+      if (nt == 128) BR_CHECK((launch_stage2<128, 64>(bd, st, a, num_sms, cap)));
+      else if (nt == 512) BR_CHECK((launch_stage2<512, 64>(bd, st, a, num_sms, cap)));
+      else BR_CHECK((launch_stage2<256, 64>(bd, st, a, num_sms, cap)));
+    } else {
+      if (nt == 512) BR_CHECK((launch_stage2<512, 128>(bd, st, a, num_sms, cap)));
+      else if (nt == 1024) BR_CHECK((launch_stage2<1024, 128>(bd, st, a, num_sms, cap)));
+      else BR_CHECK((launch_stage2<256, 128>(bd, st, a, num_sms, cap)));
+    }
   }
   const int blocks = (int)std::min<int64_t>(cdiv(n, 256), 1024);
   count_launch();
@@ -446,11 +440,15 @@ int band_to_condensed(cudaStream_t st, bool bd, int64_t n, int64_t w, double* A,
 int preload_stage2_kernels() {
   Stage2Args a{};
   for (bool bd : {false, true}) {
-    BR_CHECK((launch_stage2<32, 32>(bd, 0, a, 148, 0)));
-    BR_CHECK((launch_stage2<64, 32>(bd, 0, a, 148, 0)));
     BR_CHECK((launch_stage2<128, 32>(bd, 0, a, 148, 0)));
+    BR_CHECK((launch_stage2<256, 32>(bd, 0, a, 148, 0)));
+    BR_CHECK((launch_stage2<512, 32>(bd, 0, a, 148, 0)));
     BR_CHECK((launch_stage2<128, 64>(bd, 0, a, 148, 0)));
+    BR_CHECK((launch_stage2<256, 64>(bd, 0, a, 148, 0)));
+    BR_CHECK((launch_stage2<512, 64>(bd, 0, a, 148, 0)));
     BR_CHECK((launch_stage2<256, 128>(bd, 0, a, 148, 0)));
+    BR_CHECK((launch_stage2<512, 128>(bd, 0, a, 148, 0)));
+    BR_CHECK((launch_stage2<1024, 128>(bd, 0, a, 148, 0)));
   }
   cudaFuncAttributes fa;
   BR_CUDA(cudaFuncGetAttributes(&fa, diag_pair_kernel));
