@@ -395,13 +395,15 @@ static int s2_max_ctas() {
   return e ? std::atoi(e) : 0;
 }
 
-// Threads per CTA (BR_S2_THREADS = 128 / 256 / 512 / 1024; tuning aid).
-// The per-task element loops dominate: at n = 2048, w = 32 the tridiagonal
-// took 101 / 58.7 / 37.3 / 27.9 ms with 32 / 64 / 128 / 256 threads.
+// Threads per CTA (BR_S2_THREADS = 128 / 256 / 512 / 1024 overrides; 0 =
+// per-width default). The per-task element loops dominate: tridiagonal
+// n = 2048, w = 32 with 128 / 256 / 512 / 1024 threads 32.4 / 24.9 / 24.0 /
+// 24.9 ms; n = 8192, w = 64 350 / 241 / 175 ms (128 / 256 / 512); w = 128
+// 666 / 460 / 431 ms (256 / 512 / 1024). Defaults: 512, 512, 1024.
 static int s2_threads() {
   const char* e = std::getenv("BR_S2_THREADS");
-  const int t = e ? std::atoi(e) : 256;
-  return (t == 128 || t == 512 || t == 1024) ? t : 256;
+  const int t = e ? std::atoi(e) : 0;
+  return (t == 128 || t == 256 || t == 512 || t == 1024) ? t : 0;
 }
 
 int band_to_condensed(cudaStream_t st, bool bd, int64_t n, int64_t w, double* A, int64_t lda,
@@ -418,16 +420,16 @@ int band_to_condensed(cudaStream_t st, bool bd, int64_t n, int64_t w, double* A,
     const int nt = s2_threads();
     if (w <= 32) {
       if (nt == 128) BR_CHECK((launch_stage2<128, 32>(bd, st, a, num_sms, cap)));
-      else if (nt == 512) BR_CHECK((launch_stage2<512, 32>(bd, st, a, num_sms, cap)));
-      else BR_CHECK((launch_stage2<256, 32>(bd, st, a, num_sms, cap)));
+      else if (nt == 256) BR_CHECK((launch_stage2<256, 32>(bd, st, a, num_sms, cap)));
+      else BR_CHECK((launch_stage2<512, 32>(bd, st, a, num_sms, cap)));
     } else if (w <= 64) {
       if (nt == 128) BR_CHECK((launch_stage2<128, 64>(bd, st, a, num_sms, cap)));
-      else if (nt == 512) BR_CHECK((launch_stage2<512, 64>(bd, st, a, num_sms, cap)));
-      else BR_CHECK((launch_stage2<256, 64>(bd, st, a, num_sms, cap)));
+      else if (nt == 256) BR_CHECK((launch_stage2<256, 64>(bd, st, a, num_sms, cap)));
+      else BR_CHECK((launch_stage2<512, 64>(bd, st, a, num_sms, cap)));
     } else {
-      if (nt == 512) BR_CHECK((launch_stage2<512, 128>(bd, st, a, num_sms, cap)));
-      else if (nt == 1024) BR_CHECK((launch_stage2<1024, 128>(bd, st, a, num_sms, cap)));
-      else BR_CHECK((launch_stage2<256, 128>(bd, st, a, num_sms, cap)));
+      if (nt == 256) BR_CHECK((launch_stage2<256, 128>(bd, st, a, num_sms, cap)));
+      else if (nt == 512) BR_CHECK((launch_stage2<512, 128>(bd, st, a, num_sms, cap)));
+      else BR_CHECK((launch_stage2<1024, 128>(bd, st, a, num_sms, cap)));
     }
   }
   const int blocks = (int)std::min<int64_t>(cdiv(n, 256), 1024);
