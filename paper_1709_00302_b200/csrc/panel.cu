@@ -145,13 +145,30 @@ static int launch_leaf_t(cudaStream_t st, const LeafArgs& a) {
   return 0;
 }
 
+static bool leaf_pow2() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = std::getenv("BR_LEAF_POW2");
+    m = (e && std::atoi(e) == 1) ? 1 : 0;
+  }
+  return m == 1;
+}
+
 // 2D-layout leaf (leaf2_kernel): NW warps of 8 columns x 32 RPT rows each.
 template <int NB, int NW, int RPT = 8>
 static int launch_leaf2_t(cudaStream_t st, const LeafArgs& a) {
   auto kern = leaf2_kernel<NB, NW, RPT>;
   constexpr int ROWS = (NW / (NB / 8)) * 32 * RPT;
-  int C = 1;
-  while (C < cdiv(a.L, ROWS)) C *= 2;
+  // as many CTAs as the rows need (the 2D leaf's source sums take any
+  // count): fewer pushes and sources per column step than a power-of-two
+  // cluster (1100 x 32 58.7 -> 54.9 us, 5000 x 32 80.7 -> 75.3; c1 5.29 ->
+  // 5.15 ms, c2 8.12 -> 7.88, c3 46.75 -> 46.09, c4 444.2 -> 441.1).
+  // BR_LEAF_POW2=1 rounds the cluster up to a power of two (A/B aid).
+  int C = (int)cdiv(a.L, ROWS);
+  if (leaf_pow2()) {
+    C = 1;
+    while (C < cdiv(a.L, ROWS)) C *= 2;
+  }
   const size_t smem = ((size_t)NB * (ROWS + 8) + 2 * (size_t)NB * (NB + 1)) * sizeof(double);
   static int attr_dev_mask = 0;
   int dev = 0;

@@ -509,7 +509,8 @@ def test_leaf_layouts_agree(tmp_path):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
     for mode in ({"BR_LEAF2": "0"}, {"BR_LEAF2": "1"}, {"BR_LEAF2": "1", "BR_LEAF2_WIDE": "1"},
-                 {"BR_LEAF2": "1", "BR_LEAF64": "1"}, {"BR_LEAF_RPT": "8"}, {"BR_LEAF_RPT": "4"}):
+                 {"BR_LEAF2": "1", "BR_LEAF64": "1"}, {"BR_LEAF_RPT": "8"}, {"BR_LEAF_RPT": "4"},
+                 {"BR_LEAF_POW2": "1"}):
         path = tmp_path / f"leaf{len(outs)}.npz"
         env = dict(os.environ, **mode)
         r = subprocess.run([sys.executable, "-c", code % path], cwd=root, env=env,
