@@ -65,7 +65,12 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
   // Ys column stride padded by 8 doubles: the W fragment loads
   // Ys[(k0 + tq) * YLD + r] of tq = 0,1 (and 2,3) then fill distinct banks
   constexpr int YLD = ROWS + 8;
-  double(*G)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(Ys + NB * YLD);
+  // Gram entries are written every column step: a static array (NB <= 32)
+  // keeps those stores shared-space (a pointer carved from the dynamic array
+  // was generic and cost a shared-window base read, S2R SR_CgaCtaId, per step)
+  __shared__ double Gst[NB <= 32 ? NB : 1][NB <= 32 ? NB + 1 : 1];
+  double(*G)[NB + 1] = (NB <= 32) ? reinterpret_cast<double(*)[NB + 1]>(&Gst[0][0])
+                                  : reinterpret_cast<double(*)[NB + 1]>(Ys + NB * YLD);
   double(*Ts)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(Ys + NB * YLD + NB * (NB + 1));
 
   const uint32_t rank = cluster_ctarank(), ncta = cluster_nctarank();
@@ -275,9 +280,10 @@ __global__ void __launch_bounds__(NW * 32, 1) leaf2_kernel(const LeafArgs a) {
       nrm2 = tn[0];
     }
     // ---- 4. scalars (identical in every warp and CTA) ----
-    const double* rowv = xch ? recvr[buf] : rowl[buf];
-    const double x0 = rowv[cg * 8];                      // owner slot 0 = column i
-    const double pic = rowv[wcg * 8 + sl];                // row i of this lane's slot
+    // (two direct shared loads: a pointer selected between the arrays would be
+    // generic and cost a shared-window base computation every step)
+    const double x0 = xch ? recvr[buf][cg * 8] : rowl[buf][cg * 8];  // owner slot 0 = column i
+    const double pic = xch ? recvr[buf][wcg * 8 + sl] : rowl[buf][wcg * 8 + sl];  // row i, this slot
     const int cs = wcg * 8 + (own ? ((ci + sl) & 7) : sl);  // its column
     double beta = 0.0, rb = 0.0, rinv = 0.0;
     if (nrm2 != 0.0) {
