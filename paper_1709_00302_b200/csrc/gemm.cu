@@ -94,7 +94,9 @@ static int big_cfg(int am, bool rank_update) {
   return rank_update ? rku : gen;
 }
 static int lower_cfg(int64_t j) {
-  // 64x64 tiles with BK=32 (3 CTAs/SM) for large trailing blocks, 128x128 for small ones
+  // 64x64 tiles with BK=32 (3 CTAs/SM) at every size: against 128x128 for
+  // j < 4096 (round 1's choice) the SYR2K class went c1 2.17 -> 1.69 ms,
+  // c3 18.1 -> 16.1 ms (whole step 46.1 -> 45.2), c5 1582 -> 1577 ms
   static int cfg = -2;
   if (cfg == -2) {
     cfg = -1;
@@ -102,7 +104,8 @@ static int lower_cfg(int64_t j) {
     if (cfg >= 0 && kTiles[cfg].bm != kTiles[cfg].bn) cfg = CFG_L;
   }
   if (cfg >= 0) return cfg;
-  return j >= 4096 ? CFG_J : CFG_L;
+  (void)j;
+  return CFG_J;
 }
 
 // Tile configuration of a general/symm GEMM of shape (M, N, K).
@@ -652,7 +655,7 @@ int syr2k_cyclic(cudaStream_t st, MatView L, MatView X3, MatView Y, CycCols m, d
   g.cyc_stride = m.stride;
   g.vecA = al16(X3.p, X3.ld) && al16(Y.p, Y.ld) && (m.r0 % 2 == 0);
   g.vecB = al16(Yo, nc) && al16(Xo, nc);
-  const int cfg = (j - m.r0) >= 4096 ? CFG_J : CFG_L;  // as lower_cfg; GF_CYC instantiations
+  const int cfg = CFG_J;  // as lower_cfg; GF_CYC instantiation
   dim3 grid((unsigned)cdiv(j - m.r0, kTiles[cfg].bm), (unsigned)cdiv(nc, kTiles[cfg].bn), 1);
   return launch_tile_cyc(cfg, A_N, B_T, EPI_LOWER, st, g, grid);
 }
