@@ -1,5 +1,6 @@
 // Shared device/host helpers for the B200 (sm_100a) band-reduction library.
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>

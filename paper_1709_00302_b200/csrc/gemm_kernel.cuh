@@ -427,12 +427,12 @@ template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, int AM, 
 static int launch(cudaStream_t st, const GemmArgs& g, dim3 grid) {
   constexpr int smem = smem_bytes<BM, BN, BK, STAGES, AM, BMD>();
   auto kern = dgemm_kernel<BM, BN, BK, WM, WN, STAGES, MINB, AM, BMD, EPI, FL>;
-  static int attr_dev_mask = 0;  // per-instantiation, per-device
+  static std::atomic<int> attr_dev_mask{0};  // per-instantiation, per-device
   int dev = 0;
   BR_CUDA(cudaGetDevice(&dev));
-  if (!(attr_dev_mask & (1 << dev))) {
+  if (!(attr_dev_mask.load() & (1 << dev))) {
     BR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr_dev_mask |= 1 << dev;
+    attr_dev_mask.fetch_or(1 << dev);
   }
   if (g_preload_only) return (int)launch_pdl(kern, grid, dim3(WM * WN * 32), smem, st, g);
   count_launch();

@@ -111,13 +111,13 @@ static int launch_leaf_t(cudaStream_t st, const LeafArgs& a) {
   int C = 1;
   while (C < cdiv(a.L, ROWS)) C *= 2;
   const size_t smem = (size_t)NB * ROWS * sizeof(double);
-  static int attr_dev_mask = 0;
+  static std::atomic<int> attr_dev_mask{0};
   int dev = 0;
   BR_CUDA(cudaGetDevice(&dev));
-  if (!(attr_dev_mask & (1 << dev))) {
+  if (!(attr_dev_mask.load() & (1 << dev))) {
     BR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     BR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_dev_mask |= (1 << dev);
+    attr_dev_mask.fetch_or(1 << dev);
   }
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[3];
@@ -170,13 +170,13 @@ static int launch_leaf2_t(cudaStream_t st, const LeafArgs& a) {
     while (C < cdiv(a.L, ROWS)) C *= 2;
   }
   const size_t smem = ((size_t)NB * (ROWS + 8) + 2 * (size_t)NB * (NB + 1)) * sizeof(double);
-  static int attr_dev_mask = 0;
+  static std::atomic<int> attr_dev_mask{0};
   int dev = 0;
   BR_CUDA(cudaGetDevice(&dev));
-  if (!(attr_dev_mask & (1 << dev))) {
+  if (!(attr_dev_mask.load() & (1 << dev))) {
     BR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     BR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_dev_mask |= (1 << dev);
+    attr_dev_mask.fetch_or(1 << dev);
   }
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[3];
@@ -490,13 +490,13 @@ int t_from_gram(cudaStream_t st, const double* G, int64_t ldg, const double* tau
   }
   const int nblk = (int)cdiv(b, TAB);
   const size_t smem = t_assemble_smem((int)b);
-  static int attr_dev_mask = 0;
+  static std::atomic<int> attr_dev_mask{0};
   int dev = 0;
   BR_CUDA(cudaGetDevice(&dev));
-  if (!(attr_dev_mask & (1 << dev))) {
+  if (!(attr_dev_mask.load() & (1 << dev))) {
     BR_CUDA(cudaFuncSetAttribute(t_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)t_assemble_smem(TAB_MAXB)));
-    attr_dev_mask |= 1 << dev;
+    attr_dev_mask.fetch_or(1 << dev);
   }
   count_launch();
   BR_CUDA(launch_pdl(t_assemble_kernel, dim3(nblk), dim3(256), smem, st, G, ldg, tau, (int)b, T,

@@ -138,12 +138,12 @@ template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB>
 static int launch_xchain(cudaStream_t st, XArgs x, int ctas_per_sm, int num_sms) {
   auto kern = xchain_kernel<BM, BN, BK, WM, WN, STAGES, MINB>;
   const int tile_smem = smem_bytes<BM, BN, BK, STAGES, A_SYM, B_N>();
-  static int attr_dev_mask = 0;
+  static std::atomic<int> attr_dev_mask{0};
   int dev = 0;
   BR_CUDA(cudaGetDevice(&dev));
-  if (!(attr_dev_mask & (1 << dev))) {
+  if (!(attr_dev_mask.load() & (1 << dev))) {
     BR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr_dev_mask |= 1 << dev;
+    attr_dev_mask.fetch_or(1 << dev);
   }
   int occ = 0;
   const int G0 = num_sms * ctas_per_sm;

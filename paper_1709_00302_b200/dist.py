@@ -270,11 +270,14 @@ def _chunks(rows, b, chunk_rows):
 
 
 def reduce_sym_band_dist(Aloc: CMat, lay: Layout, w: int, ops, comm, lookahead: int = 1,
-                         chunk_rows: int = CHUNK_ROWS):
+                         chunk_rows: int = CHUNK_ROWS, tau_out=None):
     """Distributed SEVP on the local block columns `Aloc` (n x ncols_local,
     lower triangle authoritative and ZERO above the diagonal - scatter_columns
     stores it so), in place. Returns the iteration count. Band entries of
-    owned columns are final afterwards (gather_band)."""
+    owned columns are final afterwards (gather_band). tau_out: optional
+    (flat n-vector, unused) receiving each owned panel's reflector scalars at
+    its leading column (zero elsewhere; the reference's per-panel tau, used
+    for its exact flop count)."""
     n, b, P, me = lay.n, lay.b, lay.world, lay.rank
     if w != b:
         raise ValueError("the distributed path is built for w == b (the sharded configs)")
@@ -307,6 +310,8 @@ def reduce_sym_band_dist(Aloc: CMat, lay: Layout, w: int, ops, comm, lookahead: 
                 ops.join(waiter_panel=False)
             else:
                 ops.qr_panel(block(t, k + w), Y, T, None, taub[par])
+            if tau_out is not None:
+                tau_out[0][k: k + b].copy_(taub[par].t[0, :b])
         prefetched = False
         comm.wait(comm.broadcast(pk[par][: j * b + b * b], owner))
         W = CMat.packed(wbuf, 0, j, b)
@@ -350,9 +355,11 @@ def reduce_sym_band_dist(Aloc: CMat, lay: Layout, w: int, ops, comm, lookahead: 
 
 
 def reduce_tri_band_dist(Aloc: CMat, lay: Layout, w: int, ops, comm, lookahead: int = 1,
-                         chunk_rows: int = CHUNK_ROWS):
+                         chunk_rows: int = CHUNK_ROWS, tau_out=None):
     """Distributed upper triangular-band reduction of a square n x n matrix
-    held as local block columns, in place. Returns the iteration count."""
+    held as local block columns, in place. Returns the iteration count.
+    tau_out: optional (QR taus, LQ taus) flat n-vectors: QR panels' scalars
+    on their owner (zero elsewhere), the LQ panels' on every rank."""
     n, b, P, me = lay.n, lay.b, lay.world, lay.rank
     m = n
     if w != b:
@@ -400,6 +407,8 @@ def reduce_tri_band_dist(Aloc: CMat, lay: Layout, w: int, ops, comm, lookahead: 
                 ops.join(waiter_panel=False)
             else:
                 ops.qr_panel(block(t, k), Y, T, None, tauu[par])
+            if tau_out is not None:
+                tau_out[0][k: k + b].copy_(tauu[par].t[0, :b])
         prefetched = False
         comm.wait(comm.broadcast(pk[par][: i * b + b * b], owner))
         ops.gemm(W, Y, T)  # same kernel on every rank -> identical W everywhere
@@ -431,6 +440,8 @@ def reduce_tri_band_dist(Aloc: CMat, lay: Layout, w: int, ops, comm, lookahead: 
                 R3[f::P, :, :b].copy_(parts[r][: cnt * b].view(cnt, b, b))
         Yvv, Wvv = Yv.view(0, jr, 0, b), Wv.view(0, jr, 0, b)
         ops.qr_panel(R, Yvv, Tv, Wvv, tauv, lq=True)
+        if tau_out is not None:
+            tau_out[1][k: k + b].copy_(tauv.t[0, :b])
         if lay.owner(t + 1) == me:  # L into block t+1's rows k..k+b
             ops.copy(block(t + 1, k, k + b), R.view(0, b, 0, b))
         # ---- right update, pipelined by row chunks: Z_c = D_c W_V (partial),

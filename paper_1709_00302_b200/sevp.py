@@ -23,6 +23,7 @@ import numpy as np
 
 from . import _dev, _lib
 from . import factors as _factors
+from . import multi as _multi
 from .flops import FLOPS, apply_correction, sevp_counted_flops, sevp_nominal_flops, tau_zero_correction  # noqa: F401
 
 
@@ -96,8 +97,12 @@ def _depth(cfg, groups, lookahead):
 
 
 def reduce_sym_band(A, cfg, groups=None, *, lookahead=None, device=None, stats=None,
-                    return_factors=False):
-    """Reduce symmetric A to a symmetric band matrix of bandwidth cfg.w."""
+                    return_factors=False, ngpus=None, devices=None):
+    """Reduce symmetric A to a symmetric band matrix of bandwidth cfg.w.
+
+    ngpus / devices (extension): run the 1D block-cyclic
+    multi-GPU driver over those devices from this one process (multi.py);
+    needs w == b and n a multiple of b, without accumulate_q / factors."""
     cfg.validate()
     A = np.array(A, dtype=np.float64, order="F")
     if A.ndim != 2 or A.shape[0] != A.shape[1]:
@@ -108,6 +113,9 @@ def reduce_sym_band(A, cfg, groups=None, *, lookahead=None, device=None, stats=N
     ks = _schedule(cfg.n, cfg.w, cfg.b)
     if not ks:  # n <= w + 1: the copy, unchanged (ref sevp.py:302-305); no arithmetic
         return SevpResult(band=A, q=None, flops={"total": 0}, iterations=0)
+    devs = _multi.resolve_devices(ngpus, devices)
+    if devs is not None:
+        return _reduce_multi(A, cfg, depth, devs, return_factors, stats)
     lib = _lib.load()
     h, _ = _dev.ctx(device)
     n = cfg.n
@@ -134,3 +142,23 @@ def reduce_sym_band(A, cfg, groups=None, *, lookahead=None, device=None, stats=N
         fac = _factors.BandFactors(left=_factors.ChainFactors(
             arrs["yl"], arrs["tl"], arrs["taul"], _factors.sevp_panels(n, cfg.w, cfg.b), n))
     return SevpResult(band=band, q=Q, flops=flops, iterations=int(st.iterations), factors=fac)
+
+
+def _reduce_multi(A, cfg, depth, devs, return_factors, stats):
+    """reduce_sym_band over several GPUs (block-cyclic driver, multi.py)."""
+    if cfg.accumulate_q or return_factors:
+        raise ValueError("accumulate_q / return_factors are single-GPU features "
+                         "(the block-cyclic driver does not keep Q or the factors)")
+    _multi.check_dist_shape(cfg.n, cfg.w, cfg.b, "reduce_sym_band")
+    n = cfg.n
+    band, its, (taul, _) = _multi.reduce_devices(A, "sevp", cfg.w, cfg.b, devs, depth)
+    variant = {SevpVariant.REFERENCE: "reference", SevpVariant.V1: "v1", SevpVariant.V2: "v2"}[cfg.variant]
+    flops, _ = sevp_counted_flops(n, cfg.w, cfg.b, variant, False, cfg.inner_b)
+    apply_correction(flops, tau_zero_correction(_factors.sevp_panels(n, cfg.w, cfg.b), taul,
+                                                cfg.inner_b))
+    for key, val in flops.items():
+        if key != "total":
+            FLOPS.add(key, val)
+    if stats is not None:
+        stats.update(iterations=its, devices=list(devs))
+    return SevpResult(band=band, q=None, flops=flops, iterations=int(its))

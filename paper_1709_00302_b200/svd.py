@@ -26,6 +26,7 @@ import numpy as np
 
 from . import _dev, _lib
 from . import factors as _factors
+from . import multi as _multi
 from .flops import (FLOPS, apply_correction, band_counted_flops, svd_nominal_flops,  # noqa: F401
                     tau_zero_correction, tri_counted_flops)
 from .sevp import V2Mapping
@@ -103,11 +104,14 @@ def _swap(fac):
 
 
 def reduce_tri_band(A, w, b, groups=None, range_log=None, inner_b=16, *, lookahead=None,
-                    device=None, stats=None, return_factors=False):
+                    device=None, stats=None, return_factors=False, ngpus=None, devices=None):
     """Reduce A to upper triangular-band form (band[i,j] = 0 for i > j or j > i + w).
 
     return_factors=True (extension) adds `factors`: the QR chain (left, U)
-    and the LQ chain (right, V) with A = U B V^T (see factors.py)."""
+    and the LQ chain (right, V) with A = U B V^T (see factors.py).
+    ngpus / devices (extension): the 1D block-cyclic multi-GPU
+    driver over those devices from this one process (multi.py); square A,
+    w == b, n a multiple of b, no factors."""
     if w < 1:
         raise ValueError("w >= 1")
     if not (1 <= b <= w):
@@ -119,6 +123,9 @@ def reduce_tri_band(A, w, b, groups=None, range_log=None, inner_b=16, *, lookahe
         raise ValueError("range_log instrumentation is a CPU-reference analysis feature; "
                          "not supported on the GPU path")
     depth = _depth(groups, lookahead)
+    devs = _multi.resolve_devices(ngpus, devices)
+    if devs is not None:
+        return _reduce_tri_multi(A, w, b, inner_b, depth, devs, return_factors, stats)
     lib = _lib.load()
     h, _ = _dev.ctx(device)
     m, n = A.shape
@@ -149,6 +156,29 @@ def reduce_tri_band(A, w, b, groups=None, range_log=None, inner_b=16, *, lookahe
                      factors=_chains(arrs if return_factors else None, (pl, pr), m, n))
 
 
+def _reduce_tri_multi(A, w, b, inner_b, depth, devs, return_factors, stats):
+    """reduce_tri_band over several GPUs (block-cyclic driver, multi.py)."""
+    m, n = A.shape
+    if m != n:
+        raise ValueError("reduce_tri_band on several GPUs needs a square matrix")
+    if return_factors:
+        raise ValueError("return_factors is a single-GPU feature (the block-cyclic driver "
+                         "does not keep the factors)")
+    _multi.check_dist_shape(n, w, b, "reduce_tri_band")
+    band, its, (taul, taur) = _multi.reduce_devices(A, "tri", w, b, devs, depth)
+    flops, _ = tri_counted_flops(m, n, w, b, inner_b)
+    pl, pr = _factors.tri_panels(m, n, w, b)
+    apply_correction(flops, tau_zero_correction(pl, taul, inner_b) +
+                     tau_zero_correction(pr, taur, inner_b))
+    for key, val in flops.items():
+        if key != "total":
+            FLOPS.add(key, val)
+    if stats is not None:
+        stats.update(iterations=its, devices=list(devs))
+    return SvdResult(band=band, flops=flops, form=SvdForm.TRIANGULAR_BAND, lower_bw=0, upper_bw=w,
+                     iterations=int(its))
+
+
 def _chains(arrs, panels, m, n):
     if arrs is None:
         return None
@@ -159,10 +189,14 @@ def _chains(arrs, panels, m, n):
 
 
 def reduce_band_svd(A, cfg, groups=None, range_log=None, *, lookahead=None, device=None,
-                    stats=None, return_factors=False):
+                    stats=None, return_factors=False, ngpus=None, devices=None):
     """Dispatch on cfg.form (ref svd.py:515-589); m < n reduces A^T and swaps
-    the bandwidth tags (ref svd.py:530-550); m <= w + 1 returns A unchanged."""
+    the bandwidth tags (ref svd.py:530-550); m <= w + 1 returns A unchanged.
+    ngpus / devices: the triangular-band form only (multi.py)."""
     cfg.validate()
+    multi = _multi.resolve_devices(ngpus, devices) is not None
+    if multi and cfg.form != SvdForm.TRIANGULAR_BAND:
+        raise ValueError("the band form has no multi-GPU driver; use form=TRIANGULAR_BAND")
     A = np.array(A, dtype=np.float64, order="F")
     if A.ndim != 2:
         raise ValueError("reduce_band_svd needs a 2-D matrix")
@@ -175,14 +209,14 @@ def reduce_band_svd(A, cfg, groups=None, range_log=None, *, lookahead=None, devi
                              variant=cfg.variant, v2_mapping=cfg.v2_mapping, inner_b=cfg.inner_b)
             inner = reduce_band_svd(np.asfortranarray(A.T), tcfg, groups, range_log,
                                     lookahead=lookahead, device=device, stats=stats,
-                                    return_factors=return_factors)
+                                    return_factors=return_factors, ngpus=ngpus, devices=devices)
         return SvdResult(band=np.asfortranarray(inner.band.T), flops=inner.flops, form=cfg.form,
                          lower_bw=inner.upper_bw, upper_bw=inner.lower_bw,
                          iterations=inner.iterations, factors=_swap(inner.factors))
     if cfg.form == SvdForm.TRIANGULAR_BAND:
         return reduce_tri_band(A, cfg.w, cfg.b, groups, range_log, cfg.inner_b,
                                lookahead=lookahead, device=device, stats=stats,
-                               return_factors=return_factors)
+                               return_factors=return_factors, ngpus=ngpus, devices=devices)
     if range_log is not None:
         if cfg.variant != SvdVariant.REFERENCE:
             raise ValueError("range logging is defined for the reference schedule")
