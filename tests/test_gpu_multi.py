@@ -64,7 +64,13 @@ def test_zero_column_flops_match_native():
     native = br.reduce_sym_band(A, cfg)
     res = br.reduce_sym_band(A, cfg, devices=[0])
     assert res.flops == native.flops
-    assert np.linalg.norm(res.band - native.band) <= 1e-12 * np.linalg.norm(A)
+    # columns that are zero up to rounding noise make the later reflectors (and
+    # so the band entries) depend on that noise: the bands are compared through
+    # their spectra, which every valid reduction shares with A
+    ev = np.linalg.eigvalsh(A)
+    for band in (res.band, native.band):
+        assert br.band_check(band, b, b) == 0.0
+        assert np.max(np.abs(np.linalg.eigvalsh(band) - ev)) <= 1e-12 * np.max(np.abs(ev))
 
 
 def test_native_path_unchanged_after_multi_call():
