@@ -155,9 +155,9 @@ static bool leaf_pow2() {
 }
 
 // 2D-layout leaf (leaf2_kernel): NW warps of 8 columns x 32 RPT rows each.
-template <int NB, int NW, int RPT = 8>
+template <int NB, int NW, int RPT = 8, bool PAIR = false>
 static int launch_leaf2_t(cudaStream_t st, const LeafArgs& a) {
-  auto kern = leaf2_kernel<NB, NW, RPT>;
+  auto kern = leaf2_kernel<NB, NW, RPT, PAIR>;
   constexpr int ROWS = (NW / (NB / 8)) * 32 * RPT;
   // as many CTAs as the rows need (the 2D leaf's source sums take any
   // count): fewer pushes and sources per column step than a power-of-two
@@ -181,7 +181,7 @@ static int launch_leaf2_t(cudaStream_t st, const LeafArgs& a) {
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[3];
   cfg.gridDim = dim3(C);
-  cfg.blockDim = dim3(NW * 32);
+  cfg.blockDim = dim3(NW * 32 + ((PAIR && NW <= 4) ? 32 : 0));  // + the T warp
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -235,6 +235,18 @@ static int leaf_rpt() {
   return r;
 }
 
+// Pair steps (two columns per cluster exchange, leaf2_kernel<..., PAIR = true>)
+// for every leaf that has an exchange; BR_LEAF_PAIR=0: one column per
+// exchange everywhere (A/B aid).
+static bool leaf_pair() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = std::getenv("BR_LEAF_PAIR");
+    m = (e && std::atoi(e) == 0) ? 0 : 1;
+  }
+  return m == 1;
+}
+
 // Launch the 2D-layout leaf when it covers (nb, L) (sets *done).
 static int launch_leaf2(cudaStream_t st, const LeafArgs& a, bool* done) {
   const int mode = leaf2_mode();
@@ -242,6 +254,24 @@ static int launch_leaf2(cudaStream_t st, const LeafArgs& a, bool* done) {
   if (mode == 0 || a.nleaves != 1) return *done = false, 0;
   const int64_t L = a.L;
   const bool wide = mode == 2;
+  if (leaf_pair() && mode == 1 && leaf_rpt() == 44 && a.nb > 1) {
+    if (L <= 256) {  // one CTA, no exchange: single steps, T on the T warp
+      if (a.nb > 16 && a.nb <= 32) return launch_leaf2_t<32, 4, 8, true>(st, a);
+      if (a.nb > 8 && a.nb <= 16) return launch_leaf2_t<16, 2, 8, true>(st, a);
+    }
+    if (L > 256 && L <= (int64_t)LEAF_MAXC * 128) {
+      if (a.nb > 16 && a.nb <= 32) return launch_leaf2_t<32, 4, 4, true>(st, a);
+      if (a.nb > 8 && a.nb <= 16) return launch_leaf2_t<16, 2, 4, true>(st, a);
+    }
+    if (a.nb > 16 && a.nb <= 32 && L > 256) {
+      if (L <= (int64_t)LEAF_MAXC * 256) return launch_leaf2_t<32, 4, 8, true>(st, a);
+      if (L <= (int64_t)LEAF_MAXC * 512) return launch_leaf2_t<32, 8, 8, true>(st, a);
+    }
+    if (a.nb <= 16 && L > 256 && !(a.nb <= 8 && L > (int64_t)LEAF_MAXC * 1024)) {
+      if (L <= (int64_t)LEAF_MAXC * 512) return launch_leaf2_t<16, 4, 8, true>(st, a);
+      if (L <= (int64_t)LEAF_MAXC * 1024) return launch_leaf2_t<16, 8, 8, true>(st, a);
+    }
+  }
   if (leaf_rpt() == 44 && !wide && L > 256 && L <= (int64_t)LEAF_MAXC * 128) {
     if (a.nb > 16 && a.nb <= 32) return launch_leaf2_t<32, 4, 4>(st, a);
     if (a.nb > 8 && a.nb <= 16) return launch_leaf2_t<16, 2, 4>(st, a);
@@ -827,6 +857,13 @@ int preload_panel_kernels() {
   BR_CHECK((launch_leaf2_t<32, 16, 4>(0, a)));
   BR_CHECK((launch_leaf2_t<16, 4, 4>(0, a)));
   BR_CHECK((launch_leaf2_t<16, 8, 4>(0, a)));
+  BR_CHECK((launch_leaf2_t<32, 4, 4, true>(0, a)));
+  BR_CHECK((launch_leaf2_t<16, 2, 4, true>(0, a)));
+  BR_CHECK((launch_leaf2_t<16, 2, 8, true>(0, a)));
+  BR_CHECK((launch_leaf2_t<32, 4, 8, true>(0, a)));
+  BR_CHECK((launch_leaf2_t<32, 8, 8, true>(0, a)));
+  BR_CHECK((launch_leaf2_t<16, 4, 8, true>(0, a)));
+  BR_CHECK((launch_leaf2_t<16, 8, 8, true>(0, a)));
   cudaFuncAttributes fa;
   BR_CUDA(cudaFuncGetAttributes(&fa, t_assemble_kernel));
   BR_CUDA(cudaFuncGetAttributes(&fa, house_gen_kernel));
