@@ -309,6 +309,7 @@ int timed_reduction(Workspace& ws, br_stats* stats, double nominal, Workspace::G
       graphs_enabled(nominal) && ws.timing == 0 && ws.main != nullptr && ws.band_out == nullptr &&
       ws.band_in == nullptr;
   const bool same = graphable && key == ws.gkey;
+  ws.no_partition = graphable;  // green-context streams stay out of captured programs
   int rc = 0;
   int64_t iters = 0;
   float ms = 0.f;
@@ -361,6 +362,7 @@ int timed_reduction(Workspace& ws, br_stats* stats, double nominal, Workspace::G
   if (!rc) rc = cu(cudaEventSynchronize(e1));
   if (!rc) rc = cu(cudaStreamSynchronize(ws.panel));
   if (!rc && ws.gpanel) rc = cu(cudaStreamSynchronize(ws.gpanel));
+  if (!rc && ws.gupd) rc = cu(cudaStreamSynchronize(ws.gupd));
   if (!rc) rc = cu(cudaGetLastError());
   if (!rc) rc = cu(cudaEventElapsedTime(&ms, e0, e1));
   if (!rc && ws.timing) rc = ws_collect_timing(ws);
@@ -479,6 +481,44 @@ static int drv_sym(const char* name, F* f) {
   *f = (F)p;
   return 0;
 }
+// Stream on the complement of an nsm-SM partition (see Workspace::gupd).
+static int green_update_stream(int device, int nsm, int prio, cudaStream_t* upd, int* got_sms) {
+  PFN_getDevRes getres;
+  PFN_split split;
+  PFN_genDesc gen;
+  PFN_gcCreate create;
+  PFN_gcStream mkstream;
+  BR_CHECK(drv_sym("cuDeviceGetDevResource", &getres));
+  BR_CHECK(drv_sym("cuDevSmResourceSplitByCount", &split));
+  BR_CHECK(drv_sym("cuDevResourceGenerateDesc", &gen));
+  BR_CHECK(drv_sym("cuGreenCtxCreate", &create));
+  BR_CHECK(drv_sym("cuGreenCtxStreamCreate", &mkstream));
+  CUdevResource sm, part, rest;
+  unsigned n = 1;
+  if (getres((CUdevice)device, &sm, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS ||
+      split(&part, &n, &sm, &rest, CU_DEV_SM_RESOURCE_SPLIT_MAX_POTENTIAL_CLUSTER_SIZE, (unsigned)nsm) !=
+          CUDA_SUCCESS ||
+      n != 1 || rest.sm.smCount == 0) {
+    set_error("green context: SM split of %d failed", nsm);
+    return 1;
+  }
+  CUdevResourceDesc desc;
+  CUgreenCtx g;
+  if (gen(&desc, &rest, 1) != CUDA_SUCCESS ||
+      create(&g, desc, (CUdevice)device, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) {
+    set_error("green context creation failed");
+    return 1;
+  }
+  CUstream s1;
+  if (mkstream(&s1, g, CU_STREAM_NON_BLOCKING, prio) != CUDA_SUCCESS) {
+    set_error("green context stream creation failed");
+    return 1;
+  }
+  *upd = (cudaStream_t)s1;
+  *got_sms = (int)rest.sm.smCount;
+  return 0;
+}
+
 static int green_panel_streams(int device, int nsm, int prio, cudaStream_t* panel, cudaStream_t* aux,
                                int* got_sms) {
   PFN_getDevRes getres;
@@ -556,6 +596,29 @@ int br_create(int device, br_handle_t* out) {
     h->ws.green_sms = got;
     if (const char* r = std::getenv("BR_GREEN_ROWS")) h->ws.green_rows = std::atoll(r);
   }
+  {
+    // SMs kept free of overlapped update CTAs (Workspace::gupd): 16 = one leaf
+    // cluster; BR_UPD_SMS=0 disables the partition, BR_UPD_ROWS moves the
+    // trailing-rows threshold. Measured (tools/exp_upd.sh): c4 441.5 -> 433.8 ms,
+    // c3 44.4 -> 42.0 ms, c5 1572 -> 1568 ms; 8 SMs do nothing, 24-48 lose more
+    // update throughput than the panels gain. A driver without green contexts
+    // just runs without the partition.
+    const char* g = std::getenv("BR_UPD_SMS");
+    const int nres = g ? std::atoi(g) : 16;
+    if (nres > 0) {
+      cudaStream_t gu = nullptr;
+      int got = 0;
+      if (green_update_stream(device, nres, lo, &gu, &got) == 0) {
+        h->ws.gupd = gu;
+        h->ws.upd_sms = got;
+        h->ws.upd_rows = 10240;
+        if (const char* r = std::getenv("BR_UPD_ROWS")) h->ws.upd_rows = std::atoll(r);
+      } else {
+        cudaGetLastError();
+        set_error("%s", "");
+      }
+    }
+  }
   BR_CUDA(cudaStreamCreateWithFlags(&h->ws.copy, cudaStreamNonBlocking));
   BR_CUDA(cudaStreamCreateWithFlags(&h->ws.copy_in, cudaStreamNonBlocking));
   // [0, 128): persistent-panel handshakes; [128, 130): xchain grid barrier
@@ -608,6 +671,7 @@ int br_destroy(br_handle_t h) {
   for (auto e : ws.events) cudaEventDestroy(e);
   for (auto e : ws.tevents) cudaEventDestroy(e);
   if (ws.gexec) cudaGraphExecDestroy(ws.gexec);
+  if (ws.gupd) cudaStreamDestroy(ws.gupd);
   if (ws.own_main) cudaStreamDestroy(ws.own_main);
   if (ws.own_panel) cudaStreamDestroy(ws.own_panel);
   delete h;
@@ -627,6 +691,7 @@ int br_sync(br_handle_t h) {
   BR_CUDA(cudaStreamSynchronize(h->ws.main));
   BR_CUDA(cudaStreamSynchronize(h->ws.panel));
   if (h->ws.gpanel) BR_CUDA(cudaStreamSynchronize(h->ws.gpanel));
+  if (h->ws.gupd) BR_CUDA(cudaStreamSynchronize(h->ws.gupd));
   return 0;
 }
 

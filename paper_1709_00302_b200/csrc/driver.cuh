@@ -42,6 +42,19 @@ struct Workspace {
     if (confined(rows)) r.num_sms = green_sms;
     return r;
   }
+  // SM-partitioned update stream (green context over all but BR_UPD_SMS SMs):
+  // where the panel chain bounds an iteration (trailing rows <= upd_rows) the
+  // overlapped rest of the trailing update runs there, so the SMs left out
+  // never hold a long-running update CTA and the high-priority panel kernels
+  // (16-CTA leaf clusters, small GEMMs) start on them at once instead of
+  // waiting for update tiles to drain. Results do not depend on the stream.
+  cudaStream_t gupd = nullptr;
+  int upd_sms = 0;
+  int64_t upd_rows = 0;
+  cudaStream_t ustream(int64_t rows, bool overlap) const {
+    return (gupd && overlap && rows <= upd_rows && !no_partition) ? gupd : main;
+  }
+  bool no_partition = false;  // set while a graphable (small) reduction runs or is captured
   cudaStream_t main = nullptr, panel = nullptr;
   cudaStream_t own_main = nullptr, own_panel = nullptr;
   Scratch sk_main, sk_panel;  // split-K partials, one per stream

@@ -205,11 +205,28 @@ int sevp_reduce(Workspace& ws, int64_t n, int64_t w, int64_t b, int lookahead, d
       BR_CHECK(gemm(ws.main, ws.sk_main, X2, X1.T(), W, 0.5, 0.0));
       return gemm(ws.main, ws.sk_main, X3, Y, X2, 1.0, 1.0, &X1);
     };
-    auto trail = [&](int64_t c0, int64_t c1, const char* tag) -> int {
+    // `overlap`: this piece runs beside the next panel's factorization; where the
+    // panel chain bounds the iteration it goes to the SM-partitioned stream
+    // (Workspace::gupd), ordered after / before the main stream by events
+    auto trail = [&](int64_t c0, int64_t c1, const char* tag, bool overlap = false) -> int {
       if (c0 >= c1) return 0;
       MatView X3(X3b, jmax, j, bp);
-      TimeScope ts(ws, ws.main, TC_SYR2K, syr2k_flops(j, bp, c0, c1), tag, k);
-      return syr2k_lower(ws.main, A2, X3, Y, c0, c1);
+      cudaStream_t us = ws.ustream(j, overlap);
+      if (us != ws.main) {
+        cudaEvent_t ev = ws_event(ws);
+        BR_CUDA(cudaEventRecord(ev, ws.main));
+        BR_CUDA(cudaStreamWaitEvent(us, ev, 0));
+      }
+      {
+        TimeScope ts(ws, us, TC_SYR2K, syr2k_flops(j, bp, c0, c1), tag, k);
+        BR_CHECK(syr2k_lower(us, A2, X3, Y, c0, c1));
+      }
+      if (us != ws.main) {
+        cudaEvent_t ev = ws_event(ws);
+        BR_CUDA(cudaEventRecord(ev, us));
+        BR_CUDA(cudaStreamWaitEvent(ws.main, ev, 0));
+      }
+      return 0;
     };
     // Q[:, k+w:n] := Q[:, k+w:n] (I + W Y^T) (ref sevp.py:138-144)
     auto accq = [&]() -> int {
@@ -246,7 +263,7 @@ int sevp_reduce(Workspace& ws, int64_t n, int64_t w, int64_t b, int lookahead, d
       BR_CHECK(xprods());
       BR_CHECK(trail(0, split, "trail-lead"));
       BR_CHECK(launch_next_panel());
-      BR_CHECK(trail(split, j, "trail-rest"));
+      BR_CHECK(trail(split, j, "trail-rest", true));
       BR_CHECK(accq());
     } else {
       BR_CHECK(mid(k + bp, k + w, "mid"));
@@ -366,6 +383,21 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
     BR_CUDA(cudaStreamWaitEvent(ws.main, ev, 0));
     return 0;
   };
+  // the overlapped rest of an update on the SM-partitioned stream (Workspace::gupd)
+  auto upd_begin = [&](cudaStream_t us) -> int {
+    if (us == ws.main) return 0;
+    cudaEvent_t ev = ws_event(ws);
+    BR_CUDA(cudaEventRecord(ev, ws.main));
+    BR_CUDA(cudaStreamWaitEvent(us, ev, 0));
+    return 0;
+  };
+  auto upd_end = [&](cudaStream_t us) -> int {
+    if (us == ws.main) return 0;
+    cudaEvent_t ev = ws_event(ws);
+    BR_CUDA(cudaEventRecord(ev, us));
+    BR_CUDA(cudaStreamWaitEvent(ws.main, ev, 0));
+    return 0;
+  };
 
   BR_CHECK(band_in_wait(ws, bi, its[0].bp));  // the first panel's columns
   BR_CHECK(qr(ws.main, ws.sk_main, its[0].k, its[0].bp, 0));
@@ -475,9 +507,14 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
                           1.0));
           }
           BR_CHECK(issue_lq());
-          TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, ncE, bp), "left", k);
-          BR_CHECK(gemm(ws.main, ws.sk_main, E.sub(bq, 0, i - bq, ncE), Yuv.sub(bq, 0, i - bq, bp), Z,
-                        1.0, 1.0));
+          cudaStream_t us = ws.ustream(i, lookahead != 0);
+          BR_CHECK(upd_begin(us));
+          {
+            TimeScope ts(ws, us, TC_GEMM, gemm_flops(i - bq, ncE, bp), "left", k);
+            BR_CHECK(gemm(us, ws.sk_main, E.sub(bq, 0, i - bq, ncE), Yuv.sub(bq, 0, i - bq, bp), Z, 1.0,
+                          1.0));
+          }
+          BR_CHECK(upd_end(us));
         }
         const int64_t splitc = has_next ? std::max<int64_t>(0, bp + bpn - w) : 0;
         if (la && splitc == 0) BR_CHECK(next_qr_on_panel());  // next panel is left-only
@@ -533,9 +570,14 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
             }
             BR_CHECK(next_qr_on_panel());
             if (sc < jr) {
-              TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, jr - sc, bq), "right", k);
-              BR_CHECK(gemm(ws.main, ws.sk_main, D.sub(0, sc, i - bq, jr - sc), Zr,
-                            Yvv.sub(sc, 0, jr - sc, bq).T(), 1.0, 1.0, nullptr, 0, kps));
+              cudaStream_t us = ws.ustream(i, true);
+              BR_CHECK(upd_begin(us));
+              {
+                TimeScope ts(ws, us, TC_GEMM, gemm_flops(i - bq, jr - sc, bq), "right", k);
+                BR_CHECK(gemm(us, ws.sk_main, D.sub(0, sc, i - bq, jr - sc), Zr,
+                              Yvv.sub(sc, 0, jr - sc, bq).T(), 1.0, 1.0, nullptr, 0, kps));
+              }
+              BR_CHECK(upd_end(us));
             }
           } else {
             TimeScope ts(ws, ws.main, TC_GEMM, gemm_flops(i - bq, jr, bq), "right", k);
