@@ -482,7 +482,8 @@ static int drv_sym(const char* name, F* f) {
   return 0;
 }
 // Stream on the complement of an nsm-SM partition (see Workspace::gupd).
-static int green_update_stream(int device, int nsm, int prio, cudaStream_t* upd, int* got_sms) {
+static int green_update_stream(int device, int nsm, int prio, cudaStream_t* upd, int* got_sms,
+                               cudaStream_t* panel = nullptr, int panel_prio = 0, int* panel_sms = nullptr) {
   PFN_getDevRes getres;
   PFN_split split;
   PFN_genDesc gen;
@@ -516,6 +517,19 @@ static int green_update_stream(int device, int nsm, int prio, cudaStream_t* upd,
   }
   *upd = (cudaStream_t)s1;
   *got_sms = (int)rest.sm.smCount;
+  if (panel) {  // experimental: a panel stream on the nsm SMs themselves (strict split)
+    CUdevResourceDesc pdesc;
+    CUgreenCtx pg;
+    CUstream s2;
+    if (gen(&pdesc, &part, 1) != CUDA_SUCCESS ||
+        create(&pg, pdesc, (CUdevice)device, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
+        mkstream(&s2, pg, CU_STREAM_NON_BLOCKING, panel_prio) != CUDA_SUCCESS) {
+      set_error("green context (panel side) creation failed");
+      return 1;
+    }
+    *panel = (cudaStream_t)s2;
+    *panel_sms = (int)part.sm.smCount;
+  }
   return 0;
 }
 
@@ -608,11 +622,22 @@ int br_create(int device, br_handle_t* out) {
     if (nres > 0) {
       cudaStream_t gu = nullptr;
       int got = 0;
-      if (green_update_stream(device, nres, lo, &gu, &got) == 0) {
+      // BR_SPLIT_ROWS=R (experimental): panels taller than R rows run confined to
+      // the nres SMs while their update runs on the others (strict split)
+      const char* sr = std::getenv("BR_SPLIT_ROWS");
+      cudaStream_t gp = nullptr;
+      int gps = 0;
+      if (green_update_stream(device, nres, lo, &gu, &got, sr ? &gp : nullptr, hi, &gps) == 0) {
         h->ws.gupd = gu;
         h->ws.upd_sms = got;
         h->ws.upd_rows = 10240;
         if (const char* r = std::getenv("BR_UPD_ROWS")) h->ws.upd_rows = std::atoll(r);
+        if (sr && gp) {
+          h->ws.gpanel = gp;
+          h->ws.green_sms = gps;
+          h->ws.green_rows = std::atoll(sr);
+          h->ws.split_upd = true;
+        }
       } else {
         cudaGetLastError();
         set_error("%s", "");

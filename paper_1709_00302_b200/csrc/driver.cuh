@@ -52,8 +52,10 @@ struct Workspace {
   int upd_sms = 0;
   int64_t upd_rows = 0;
   cudaStream_t ustream(int64_t rows, bool overlap) const {
-    return (gupd && overlap && rows <= upd_rows && !no_partition) ? gupd : main;
+    return (gupd && overlap && !no_partition && (rows <= upd_rows || (split_upd && confined(rows)))) ? gupd
+                                                                                                   : main;
   }
+  bool split_upd = false;  // BR_SPLIT_ROWS: confined panels, their update on the other SMs
   bool no_partition = false;  // set while a graphable (small) reduction runs or is captured
   cudaStream_t main = nullptr, panel = nullptr;
   cudaStream_t own_main = nullptr, own_panel = nullptr;
