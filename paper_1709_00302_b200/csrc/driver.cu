@@ -622,9 +622,18 @@ int br_create(int device, br_handle_t* out) {
     if (nres > 0) {
       cudaStream_t gu = nullptr;
       int got = 0;
-      // BR_SPLIT_ROWS=R (experimental): panels taller than R rows run confined to
-      // the nres SMs while their update runs on the others (strict split)
-      const char* sr = std::getenv("BR_SPLIT_ROWS");
+      // Strict split for the triangular band's tall panels (BR_SPLIT_ROWS = R,
+      // default 11264, 0 disables): above R rows the update has slack over the
+      // panels, and what it loses beside them are dispatch pauses around the
+      // panel's ~70 launches. There the leaves and block updates of a panel run
+      // confined to the nres SMs (panel_qr phase 1), only the three full-size
+      // products that finish it (Gram, T, W) on the whole device, and the
+      // overlapped update on the other SMs: update class 411 -> 404 ms, c4
+      // 433.8 -> 430.2 ms (tools/exp_upd.sh). Without the two-phase panel the
+      // confined panels became the bottleneck (447 ms).
+      const char* sre = std::getenv("BR_SPLIT_ROWS");
+      const int64_t srows = sre ? std::atoll(sre) : 11264;
+      const bool sr = srows > 0;
       cudaStream_t gp = nullptr;
       int gps = 0;
       if (green_update_stream(device, nres, lo, &gu, &got, sr ? &gp : nullptr, hi, &gps) == 0) {
@@ -635,7 +644,7 @@ int br_create(int device, br_handle_t* out) {
         if (sr && gp) {
           h->ws.gpanel = gp;
           h->ws.green_sms = gps;
-          h->ws.green_rows = std::atoll(sr);
+          h->ws.green_rows = srows;
           h->ws.split_upd = true;
         }
       } else {

@@ -186,7 +186,7 @@ struct LeafMarks {
 };
 int panel_qr(cudaStream_t st, Scratch& sk, DevBuf& pscratch, MatView P, MatView Y, double* tau,
              MatView T, MatView* W, int max_ctas = 0, Workspace* pws = nullptr,
-             LeafMarks* marks = nullptr);
+             LeafMarks* marks = nullptr, int phase = 0);
 int64_t panel_scratch_doubles(int64_t b);
 int t_from_gram(cudaStream_t st, const double* G, int64_t ldg, const double* tau, int64_t b,
                 double* T, int64_t ldt, bool diag_given = false);

@@ -638,8 +638,12 @@ static int64_t rec_min_rows() {
   return v;
 }
 
+// phase: 0 = the whole panel; 1 = leaves and block updates only (Y, tau, the
+// leaves' diagonal T blocks); 2 = the rest of a multi-leaf panel (Gram matrix,
+// T, W = Y T) - the strict SM split runs phase 1 on the confined stream and
+// phase 2 on the full device. Single-leaf panels finish in phase 1.
 int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView Y, double* tau,
-             MatView T, MatView* W, int max_ctas, Workspace* pws, LeafMarks* marks) {
+             MatView T, MatView* W, int max_ctas, Workspace* pws, LeafMarks* marks, int phase) {
   const int64_t j = P.rows, b = P.cols;
   if (marks) marks->n = 0;
   auto mark = [&](int64_t c0, int64_t c1) -> int {  // Y[:, c0:c1) final on st
@@ -667,6 +671,7 @@ int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView 
     return -1;
   }
   if (b <= nbl) {
+    if (phase == 2) return 0;
     // single leaf: Y, tau, T and W in one kernel (narrow leaves: W by a GEMM)
     if (nbl < 8) {
       BR_CHECK(zero_fill(st, T));
@@ -678,8 +683,10 @@ int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView 
     return mark(0, b);
   }
   // multi-leaf, right-looking
-  BR_CHECK(zero_fill(st, Y));
-  BR_CHECK(zero_fill(st, T));
+  if (phase != 2) {
+    BR_CHECK(zero_fill(st, Y));
+    BR_CHECK(zero_fill(st, T));
+  }
   if (pscratch.cap < panel_scratch_doubles(b)) {
     set_error("panel_qr: panel scratch too small");
     return -1;
@@ -691,7 +698,7 @@ int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView 
   MatView Z2(Z.p + LEAF_NB * b, LEAF_NB, LEAF_NB, b);
   const int nleaves = (int)cdiv(b, nbl);
   const bool persist = pws && W && nleaves <= 64 && nbl <= 32 && persistent_panel_enabled(j);
-  if (persist) {
+  if (persist && phase != 2) {
     // Persistent panel: one cluster launch factors every leaf; the block
     // update of leaf s is applied on the aux stream, first to the next
     // leaf's columns (then the leaf may proceed), then to the rest of the
@@ -775,7 +782,8 @@ int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView 
     BR_CHECK(gemm(st, ws, P2, Y1, Zr2, 1.0, 1.0, nullptr, max_ctas));
     return rec(c0 + h, c1);
   };
-  if (!persist) BR_CHECK(rec(0, b));
+  if (!persist && phase != 2) BR_CHECK(rec(0, b));
+  if (phase == 1) return 0;
   // full T: Gram, then the blocked recurrence in one kernel (T is written whole,
   // zeros below the diagonal). 32-wide leaves already wrote the 32 x 32
   // diagonal blocks of T.

@@ -93,8 +93,20 @@ static double panel_flops(int64_t j, int64_t b) {
 // ---------------------------------------------------------------------------
 // SEVP
 // ---------------------------------------------------------------------------
+// The strict SM split (confined tall panels, two-phase panel) is wired into the
+// triangular band only: the other reductions keep their panels unconfined.
+struct NoSplit {
+  Workspace& ws;
+  int64_t saved;
+  explicit NoSplit(Workspace& w) : ws(w), saved(w.green_rows) {
+    if (ws.split_upd) ws.green_rows = INT64_MAX;
+  }
+  ~NoSplit() { ws.green_rows = saved; }
+};
+
 int sevp_reduce(Workspace& ws, int64_t n, int64_t w, int64_t b, int lookahead, double* A,
                 int64_t lda, double* Q, int64_t ldq, int64_t* iterations, BandOut* bo) {
+  NoSplit nosplit(ws);
   std::vector<int64_t> ks;
   for (int64_t k = 0; n - k - w >= 2; k += std::min(b, n - k - w)) ks.push_back(k);
   // partial reduction (BR_OPT_MAX_ITERS): the first max_iters panels only,
@@ -348,14 +360,40 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
   LeafMarks mk_qr[2], mk_lq;
 
   auto Aat = [&](int64_t r, int64_t c) { return A + r + c * lda; };
+  // Strict SM split (BR_SPLIT_ROWS, experimental): the leaves and block updates
+  // of a tall panel run confined to the reserved SMs (`st` is then the confined
+  // stream, or the main stream without look-ahead - same plans either way), the
+  // three full-size products that finish it (Gram, T, W) on the full device.
+  auto split_panel = [&](cudaStream_t st, Scratch& sk, int64_t rows, MatView P, MatView Y, double* tau,
+                         MatView T, MatView W) -> int {
+    Scratch s1 = ws.pscratch_for(sk, rows);
+    BR_CHECK(panel_qr(st, s1, ws.pscratch, P, Y, tau, T, &W, panel_cap(rows), &ws, nullptr, 1));
+    cudaStream_t fs = (st == ws.gpanel) ? ws.panel : st;
+    if (fs != st) {
+      cudaEvent_t ev = ws_event(ws);
+      BR_CUDA(cudaEventRecord(ev, st));
+      BR_CUDA(cudaStreamWaitEvent(fs, ev, 0));
+    }
+    BR_CHECK(panel_qr(fs, sk, ws.pscratch, P, Y, tau, T, &W, panel_cap(rows), &ws, nullptr, 2));
+    if (fs != st) {  // callers mark completion on `st`
+      cudaEvent_t ev = ws_event(ws);
+      BR_CUDA(cudaEventRecord(ev, fs));
+      BR_CUDA(cudaStreamWaitEvent(st, ev, 0));
+    }
+    return 0;
+  };
   auto qr = [&](cudaStream_t st, Scratch& sk, int64_t k, int64_t bp, int par) -> int {
     const int64_t i = m - k;
     MatView P(Aat(k, k), lda, i, bp);
     MatView Y(Yu[par], m, i, bp), T(Tu[par], b, bp, bp), W(Wu[par], m, i, bp);
     TimeScope ts(ws, st, TC_PANEL, panel_flops(i, bp), "qr", k);
-    Scratch s = ws.pscratch_for(sk, i);
-    BR_CHECK(panel_qr(st, s, ws.pscratch, P, Y, tauu[par], T, &W, panel_cap(i), &ws,
-                      pz_rows() > 0 ? &mk_qr[par] : nullptr));
+    if (ws.split_upd && ws.confined(i)) {
+      BR_CHECK(split_panel(st, sk, i, P, Y, tauu[par], T, W));
+    } else {
+      Scratch s = ws.pscratch_for(sk, i);
+      BR_CHECK(panel_qr(st, s, ws.pscratch, P, Y, tauu[par], T, &W, panel_cap(i), &ws,
+                        pz_rows() > 0 ? &mk_qr[par] : nullptr));
+    }
     return store_factors(ws, st, 0, k, k, i, bp, Yu[par], m, Tu[par], b, tauu[par]);
   };
   auto lq = [&](cudaStream_t st, Scratch& sk, int64_t k, int64_t bq) -> int {
@@ -363,9 +401,13 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
     MatView P(Aat(k, k + w), lda, jr, bq, true);  // transposed view of the bq x jr rows
     MatView Y(Yv, n, jr, bq), T(Tv, b, bq, bq), W(Wv, n, jr, bq);
     TimeScope ts(ws, st, TC_PANEL, panel_flops(jr, bq), "lq", k);
-    Scratch s = ws.pscratch_for(sk, jr);
-    BR_CHECK(panel_qr(st, s, ws.pscratch, P, Y, tauv, T, &W, panel_cap(jr), &ws,
-                      pz_rows() > 0 ? &mk_lq : nullptr));
+    if (ws.split_upd && ws.confined(jr)) {
+      BR_CHECK(split_panel(st, sk, jr, P, Y, tauv, T, W));
+    } else {
+      Scratch s = ws.pscratch_for(sk, jr);
+      BR_CHECK(panel_qr(st, s, ws.pscratch, P, Y, tauv, T, &W, panel_cap(jr), &ws,
+                        pz_rows() > 0 ? &mk_lq : nullptr));
+    }
     return store_factors(ws, st, 1, k, k + w, jr, bq, Yv, n, Tv, b, tauv);
   };
   auto handoff = [&](cudaStream_t ps) -> int {  // main -> panel ordering point
@@ -633,6 +675,7 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
 // equal to depth 0.
 int band_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int fused,
                 int lookahead, double* A, int64_t lda, int64_t* iterations, BandOut* bo) {
+  NoSplit nosplit(ws);
   struct It {
     int64_t k, bp, jr, bq;
   };
