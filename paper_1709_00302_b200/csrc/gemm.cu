@@ -87,7 +87,10 @@ static int big_cfg(int am, bool rank_update) {
   static int gen = -1, sym = -1, rku = -1;
   if (gen < 0) {
     gen = env_cfg("BR_GEMM_BIG", CFG_G);
-    sym = env_cfg("BR_GEMM_SYMM", CFG_K);
+    // SYMM: 64x128 tiles with BK = 16, 3 stages (G) against BK = 32, 2 stages (K,
+    // round 1's choice): SYMM class c3 13.9 -> 13.2 ms, c5 711 -> 703 ms
+    // (tools/exp_symm.sh; whole step c3 42.2 -> 41.4 ms, c5 1566 -> 1558 ms)
+    sym = env_cfg("BR_GEMM_SYMM", CFG_G);
     rku = env_cfg("BR_GEMM_RANKB", CFG_J);
   }
   if (am == A_SYM) return sym;
