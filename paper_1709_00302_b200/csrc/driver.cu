@@ -618,7 +618,14 @@ int br_create(int device, br_handle_t* out) {
     // update throughput than the panels gain. A driver without green contexts
     // just runs without the partition.
     const char* g = std::getenv("BR_UPD_SMS");
-    const int nres = g ? std::atoi(g) : 16;
+    // Nsight Compute cannot prepare kernels launched on green-context streams
+    // ("Failed to prepare kernel for profiling"): under its injection the
+    // partition stays off unless BR_UPD_SMS asks for it, so `ncu python
+    // bench.py` and the launch lists in profiles/ work (they then show the
+    // two-stream program without the partition)
+    const bool profiled = std::getenv("NV_NSIGHT_INJECTION_PORT_BASE") != nullptr ||
+                          std::getenv("NV_COMPUTE_PROFILER_PERFWORKS_DIR") != nullptr;
+    const int nres = g ? std::atoi(g) : (profiled ? 0 : 16);
     if (nres > 0) {
       cudaStream_t gu = nullptr;
       int got = 0;

@@ -10,9 +10,9 @@ from collections import defaultdict
 
 
 def family(name: str) -> str:
-    m = re.search(r"dgemm_kernel<(\d+), (\d+), (\d+), (\d+), (\d+), (\d+), (\d+), (\d+), (\d+), (\d+)>", name)
+    m = re.search(r"dgemm_kernel<(\d+), (\d+), (\d+), (\d+), (\d+), (\d+), (\d+), (\d+), (\d+), (\d+)(?:, \d+)*>", name)
     if m:
-        bm, bn, bk, wm, wn, st, minb, am, bmd, epi = m.groups()
+        bm, bn, bk, wm, wn, st, minb, am, bmd, epi = m.groups()[:10]
         amn = {"0": "N", "1": "T", "2": "SYM"}[am]
         bmn = {"0": "N", "1": "T"}[bmd]
         epn = {"0": "gen", "1": "splitK", "2": "lower(SYR2K)"}[epi]
@@ -20,7 +20,7 @@ def family(name: str) -> str:
     m = re.search(r"leaf_reg_kernel<(\d+), (\d+), (\d+)>", name)
     if m:
         return f"panel leaf (1D) NB={m.group(1)} R={m.group(2)} LT={m.group(3)}"
-    m = re.search(r"leaf2_kernel<(\d+), (\d+)>", name)
+    m = re.search(r"leaf2_kernel<(\d+), (\d+)", name)
     if m:
         return f"panel leaf (2D) NB={m.group(1)} warps={m.group(2)}"
     for key in ("splitk_reduce", "t_assemble", "t_diag", "finalize_sym", "mask_band",
