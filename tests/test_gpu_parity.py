@@ -120,6 +120,42 @@ def test_qr_panel_wide_vs_oracle(br, j, b, seed):
         assert np.linalg.norm(Qe.T @ Qe - np.eye(j)) <= 1e-12 * np.sqrt(j)
 
 
+def _structured_panels(j, b):
+    """Panels that reach the pair step's special cases: exact zero columns and
+    zero tails (tau = 0 / 2 rules), an already triangular panel, graded column
+    norms, and neighbouring columns that nearly cancel (the norm-downdating
+    safeguard's single-step fallback)."""
+    rng = np.random.default_rng(j + b)
+    P = rng.standard_normal((j, b)); P[:, 5] = 0.0; P[:, 6] = 0.0
+    yield "zero columns", P, 1e-12
+    P = rng.standard_normal((j, b)); P[8:, 7] = 0.0; P[9:, 8] = 0.0
+    yield "zero tails", P, 1e-12
+    yield "triangular", np.triu(rng.standard_normal((j, b))), 1e-12
+    yield "graded", rng.standard_normal((j, b)) * np.logspace(0, -10, b)[None, :], 1e-12
+    P = rng.standard_normal((j, b))
+    for c in range(1, b, 2):
+        P[:, c] = P[:, c - 1] + 1e-3 * rng.standard_normal(j)
+    yield "near-dependent pairs", P, 1e-11  # conditioning ~1e3 amplifies both implementations
+
+
+@pytest.mark.parametrize("j,b", [(300, 32), (2016, 32), (1000, 16), (5000, 32), (9000, 24), (16000, 16)])
+def test_qr_panel_pair_steps_structured(br, j, b):
+    """Pair-step leaves (two columns per exchange, every launch shape) on
+    structured panels against the oracle, signs of R included."""
+    for name, P0, tol in _structured_panels(j, b):
+        Pg, Po = P0.copy(order="F"), P0.copy(order="F")
+        f = br.qr_panel(Pg)
+        Y, T, W, R, tau = O.qr_panel(Po)
+        assert np.array_equal(np.sign(np.diag(f.r_or_l)), np.sign(np.diag(R))), name
+        assert rel(f.r_or_l, R, np.linalg.norm(P0)) <= tol / 10, name
+        assert rel(f.y, Y, np.linalg.norm(Y)) <= tol, name
+        assert rel(f.t, T, np.linalg.norm(T)) <= tol, name
+        assert rel(f.w, W, np.linalg.norm(W)) <= tol, name
+        assert rel(f.tau, tau, np.linalg.norm(tau)) <= tol / 10, name
+        if name == "zero columns":
+            assert f.tau[5] == 0.0 and f.tau[6] == 0.0
+
+
 def test_lq_panel_wide_vs_oracle(br):
     P0 = rand(256, 5000, 7)
     Pg, Po = P0.copy(order="F"), P0.copy(order="F")
@@ -556,10 +592,17 @@ def test_pipelined_z_matches(tmp_path):
 @pytest.mark.parametrize("env", [{"BR_LEAF_W": "0"},
                                  {"BR_PANEL_CAP": "16", "BR_PANEL_CAP_ROWS": "0"},
                                  {"BR_PERSIST_ROWS": "100000"},
-                                 {"BR_LEAF2": "0"}])
+                                 {"BR_LEAF2": "0"},
+                                 {"BR_LEAF_PAIR": "0"},
+                                 {"BR_GRAPHS": "0"},
+                                 {"BR_GRAPHS": "0", "BR_UPD_SMS": "0"},
+                                 {"BR_GRAPHS": "0", "BR_SPLIT_ROWS": "400"}])
 def test_tuning_modes_agree(tmp_path, env):
     """The measured-and-kept tuning modes (T^T inside the split-K reduction,
-    split-K shaped by a panel CTA cap, persistent panels, the 1D leaf) reduce to the same
+    split-K shaped by a panel CTA cap, persistent panels, the 1D leaf, leaves
+    without pair steps; with graphs off the SM-partitioned update stream runs
+    at this size too, with and without the partition, and with the strict
+    split's two-phase confined panels) reduce to the same
     bands as the default path, to rounding, with depth 1 == depth 0 bitwise."""
     import subprocess
     import sys
