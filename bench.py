@@ -409,7 +409,9 @@ def run_ours(args, rank, world, local_rank):
             "data": "synthetic",
             "config": same_config(args.config, la, world),
             "clocks": clocks.summary(),
-            "e2e": {"value": e2e_val, "unit": "GFLOP/s", "h2d_bytes_per_step": n * n * 8,
+            "e2e": {"value": e2e_val, "unit": "GFLOP/s",
+                    # SEVP: the host entry point copies the lower triangle only
+                    "h2d_bytes_per_step": int(lib.br_sym_stage_bytes(n)) if kind == "sevp" else n * n * 8,
                     "d2h_bytes_per_step": n * n * 8, "steps": e2e_steps,
                     "path": "br_reduce_*_host (C ABI), pinned host in/out"},
             "gpu_launches": int(launches),

@@ -221,6 +221,12 @@ int br_reduce_sym_band_host(br_handle_t h, int64_t n, int64_t w, int64_t b, int 
 int br_reduce_tri_band_host(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b,
                             int lookahead, const double* A, int64_t lda, double* band,
                             int64_t ldb, const br_factors* factors, br_stats* stats);
+/* Bytes br_reduce_sym_band_host copies to the device for an n x n input with
+ * n > w + 1: the reduction reads the lower triangle only (as the reference
+ * does, sevp.py:287-324 / kernels.py:312-341), so the stage-in copies the
+ * lower triangle by column blocks and the upper triangle of A is never
+ * touched. */
+int64_t br_sym_stage_bytes(int64_t n);
 
 /* Equal-bandwidth band form of the SVD (replaces the band branch of
  * reduce_band_svd, ref pkg/src/bandred/svd.py:515-589, task bodies

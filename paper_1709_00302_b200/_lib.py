@@ -76,6 +76,7 @@ SIGNATURES = {
                                      C.POINTER(BrFactors), C.POINTER(BrStats)]),
     "br_reduce_tri_band": (C.c_int, [C.c_void_p, i64, i64, i64, i64, C.c_int, dptr, i64,
                                      C.POINTER(BrFactors), C.POINTER(BrStats)]),
+    "br_sym_stage_bytes": (C.c_int64, [i64]),
     "br_reduce_sym_band_host": (C.c_int, [C.c_void_p, i64, i64, i64, C.c_int, dptr, i64, dptr, i64,
                                           dptr, i64, C.POINTER(BrFactors), C.POINTER(BrStats)]),
     "br_reduce_tri_band_host": (C.c_int, [C.c_void_p, i64, i64, i64, i64, C.c_int, dptr, i64, dptr,

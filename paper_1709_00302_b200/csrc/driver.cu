@@ -1301,6 +1301,32 @@ static int host_stage_in(Workspace& ws, int64_t m, int64_t n, const double* A, i
   return 0;
 }
 
+// Bytes the symmetric stage-in copies for an n x n input (br_sym_stage_bytes in
+// the header): column blocks of the lower triangle, from each block's first
+// row down. The reduction reads the lower triangle only (ref sevp.py reads
+// A's lower part; the upper triangle of the device copy is first written by
+// the finalize pass), so half of the input never crosses PCIe.
+static int64_t sym_stage_block(int64_t n) { return std::max<int64_t>(256, (n / 32 + 31) / 32 * 32); }
+static int host_stage_in_lower(Workspace& ws, int64_t n, const double* A, int64_t lda, DevBuf& dev,
+                               int64_t& ldd) {
+  ldd = (n + 31) / 32 * 32;
+  BR_CHECK(devbuf_reserve(dev, ldd * n));
+  const int64_t blk = sym_stage_block(n);
+  for (int64_t c0 = 0; c0 < n; c0 += blk) {
+    const int64_t nc = std::min(blk, n - c0);
+    BR_CUDA(cudaMemcpy2DAsync(dev.p + c0 + c0 * ldd, ldd * sizeof(double), A + c0 + c0 * lda,
+                              lda * sizeof(double), (n - c0) * sizeof(double), nc,
+                              cudaMemcpyHostToDevice, ws.main));
+  }
+  return 0;
+}
+extern "C" int64_t br_sym_stage_bytes(int64_t n) {
+  int64_t bytes = 0;
+  const int64_t blk = sym_stage_block(n);
+  for (int64_t c0 = 0; c0 < n; c0 += blk) bytes += (n - c0) * std::min(blk, n - c0) * (int64_t)sizeof(double);
+  return bytes;
+}
+
 int br_reduce_sym_band_host(br_handle_t h, int64_t n, int64_t w, int64_t b, int lookahead,
                             const double* A, int64_t lda, double* band, int64_t ldb, double* Q,
                             int64_t ldq, const br_factors* factors, br_stats* stats) {
@@ -1319,7 +1345,9 @@ int br_reduce_sym_band_host(br_handle_t h, int64_t n, int64_t w, int64_t b, int 
   DevBuf& dA = ws.stageA;
   DevBuf& dQ = ws.stageQ;
   int64_t ldd = 0;
-  BR_CHECK(host_stage_in(ws, n, n, A, lda, dA, ldd));
+  // the unchanged-input case (n <= w + 1) and partial runs hand the raw matrix back
+  if (n <= w + 1 || ws.max_iters > 0) BR_CHECK(host_stage_in(ws, n, n, A, lda, dA, ldd));
+  else BR_CHECK(host_stage_in_lower(ws, n, A, lda, dA, ldd));
   double* qd = nullptr;
   if (Q) {
     BR_CHECK(devbuf_reserve(dQ, ldd * n));
