@@ -156,6 +156,25 @@ def test_qr_panel_pair_steps_structured(br, j, b):
             assert f.tau[5] == 0.0 and f.tau[6] == 0.0
 
 
+@pytest.mark.parametrize("j,b", [(256, 32), (2016, 32), (4000, 32), (8000, 32), (3000, 16), (16000, 16)])
+def test_qr_panel_repeatable_bitwise(br, j, b):
+    """The leaf's exchange protocol (double-buffered shared / cluster buffers,
+    the T warp's progress hand-off) has no window for a race: 12 runs of the
+    same panel are bitwise identical in R, Y, T, W and tau (compute-sanitizer
+    is closed on this GPU pool, so repeatability is the race check)."""
+    P0 = rand(j, b, 77)
+    ref = None
+    for _ in range(12):
+        Pg = P0.copy(order="F")
+        f = br.qr_panel(Pg)
+        got = (f.r_or_l.copy(), f.y.copy(), f.t.copy(), f.w.copy(), f.tau.copy())
+        if ref is None:
+            ref = got
+        else:
+            for x, y in zip(ref, got):
+                assert np.array_equal(x, y)
+
+
 def test_lq_panel_wide_vs_oracle(br):
     P0 = rand(256, 5000, 7)
     Pg, Po = P0.copy(order="F"), P0.copy(order="F")
