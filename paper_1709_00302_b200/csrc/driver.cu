@@ -482,8 +482,10 @@ static int drv_sym(const char* name, F* f) {
   return 0;
 }
 // Stream on the complement of an nsm-SM partition (see Workspace::gupd).
+typedef CUresult (*PFN_gcDestroy)(CUgreenCtx);
 static int green_update_stream(int device, int nsm, int prio, cudaStream_t* upd, int* got_sms,
-                               cudaStream_t* panel = nullptr, int panel_prio = 0, int* panel_sms = nullptr) {
+                               cudaStream_t* panel, int panel_prio, int* panel_sms, void** ctx_upd,
+                               void** ctx_panel) {
   PFN_getDevRes getres;
   PFN_split split;
   PFN_genDesc gen;
@@ -517,6 +519,7 @@ static int green_update_stream(int device, int nsm, int prio, cudaStream_t* upd,
   }
   *upd = (cudaStream_t)s1;
   *got_sms = (int)rest.sm.smCount;
+  *ctx_upd = (void*)g;
   if (panel) {  // experimental: a panel stream on the nsm SMs themselves (strict split)
     CUdevResourceDesc pdesc;
     CUgreenCtx pg;
@@ -529,6 +532,7 @@ static int green_update_stream(int device, int nsm, int prio, cudaStream_t* upd,
     }
     *panel = (cudaStream_t)s2;
     *panel_sms = (int)part.sm.smCount;
+    *ctx_panel = (void*)pg;
   }
   return 0;
 }
@@ -643,7 +647,8 @@ int br_create(int device, br_handle_t* out) {
       const bool sr = srows > 0;
       cudaStream_t gp = nullptr;
       int gps = 0;
-      if (green_update_stream(device, nres, lo, &gu, &got, sr ? &gp : nullptr, hi, &gps) == 0) {
+      if (green_update_stream(device, nres, lo, &gu, &got, sr ? &gp : nullptr, hi, &gps, &h->ws.gctx_upd,
+                              &h->ws.gctx_panel) == 0) {
         h->ws.gupd = gu;
         h->ws.upd_sms = got;
         h->ws.upd_rows = 10240;
@@ -713,6 +718,14 @@ int br_destroy(br_handle_t h) {
   for (auto e : ws.tevents) cudaEventDestroy(e);
   if (ws.gexec) cudaGraphExecDestroy(ws.gexec);
   if (ws.gupd) cudaStreamDestroy(ws.gupd);
+  if (ws.split_upd && ws.gpanel) cudaStreamDestroy(ws.gpanel);
+  {
+    PFN_gcDestroy gdestroy = nullptr;
+    if ((ws.gctx_upd || ws.gctx_panel) && drv_sym("cuGreenCtxDestroy", &gdestroy) == 0) {
+      if (ws.gctx_upd) gdestroy((CUgreenCtx)ws.gctx_upd);
+      if (ws.gctx_panel) gdestroy((CUgreenCtx)ws.gctx_panel);
+    }
+  }
   if (ws.own_main) cudaStreamDestroy(ws.own_main);
   if (ws.own_panel) cudaStreamDestroy(ws.own_panel);
   delete h;

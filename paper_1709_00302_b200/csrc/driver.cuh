@@ -49,6 +49,7 @@ struct Workspace {
   // (16-CTA leaf clusters, small GEMMs) start on them at once instead of
   // waiting for update tiles to drain. Results do not depend on the stream.
   cudaStream_t gupd = nullptr;
+  void *gctx_upd = nullptr, *gctx_panel = nullptr;  // the partition's green contexts (br_destroy)
   int upd_sms = 0;
   int64_t upd_rows = 0;
   cudaStream_t ustream(int64_t rows, bool overlap) const {
