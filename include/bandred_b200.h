@@ -210,7 +210,7 @@ int br_reduce_tri_band(br_handle_t h, int64_t m, int64_t n, int64_t w, int64_t b
                        double* A, int64_t lda, const br_factors* factors, br_stats* stats);
 /* Host-buffer variants: copy A (host, lda) to the device, reduce, copy the
  * band back to `band` (host, ldb). Host buffers may be pageable or pinned.
- * Pinned buffers of 64 MiB and more are streamed: finished band column
+ * Pinned buffers of 16 MiB and more are streamed: finished band column
  * blocks are copied out while the reduction runs, and (triangular band) the
  * input is copied in by column chunks while iteration 0's panel and left
  * update start on the chunks already there. Results are bitwise those of

@@ -1235,7 +1235,15 @@ static bool setup_band_out(Workspace& ws, BandOut& bo, double* band, int64_t ldb
   const bool pinned = cudaPointerGetAttributes(&pa, band) == cudaSuccess &&
                       pa.type == cudaMemoryTypeHost;
   cudaGetLastError();
-  if (!pinned || m * n * (int64_t)sizeof(double) < ((int64_t)64 << 20)) return false;
+  // streamed output from BR_STREAM_MIN_MB MiB (default 16; 64 until late in
+  // round 2): at c1 / c2's 32 MiB the overlapped copy-out is worth more end to
+  // end than the graph replay it displaces (e2e c1 1964 -> 2059 GFLOP/s, c2
+  // 2676 -> 2789)
+  static const int64_t min_mb = [] {
+    const char* e = std::getenv("BR_STREAM_MIN_MB");
+    return e ? (int64_t)std::atoll(e) : (int64_t)16;
+  }();
+  if (!pinned || m * n * (int64_t)sizeof(double) < (min_mb << 20)) return false;
   bo.st = ws.copy;
   bo.host = band;
   bo.ldh = ldb;
@@ -1410,7 +1418,11 @@ int br_reduce_tri_band_host(br_handle_t h, int64_t m, int64_t n, int64_t w, int6
                          pa.type == cudaMemoryTypeHost && stream_in_enabled();
   cudaGetLastError();
   BandIn bi;
-  const bool stream_in = pinned_in && m * n * (int64_t)sizeof(double) >= ((int64_t)64 << 20);
+  static const int64_t in_min_mb = [] {  // BR_STREAM_IN_MIN_MB (default 64)
+    const char* e = std::getenv("BR_STREAM_IN_MIN_MB");
+    return e ? (int64_t)std::atoll(e) : (int64_t)64;
+  }();
+  const bool stream_in = pinned_in && m * n * (int64_t)sizeof(double) >= (in_min_mb << 20);
   if (stream_in) {
     ldd = (m + 31) / 32 * 32;
     BR_CHECK(devbuf_reserve(dA, ldd * n));
