@@ -634,7 +634,7 @@ int br_create(int device, br_handle_t* out) {
       cudaStream_t gu = nullptr;
       int got = 0;
       // Strict split for the triangular band's tall panels (BR_SPLIT_ROWS = R,
-      // default 11264, 0 disables): above R rows the update has slack over the
+      // default 10240, 0 disables): above R rows the update has slack over the
       // panels, and what it loses beside them are dispatch pauses around the
       // panel's ~70 launches. There the leaves and block updates of a panel run
       // confined to the nres SMs (panel_qr phase 1), only the three full-size
@@ -643,7 +643,7 @@ int br_create(int device, br_handle_t* out) {
       // 433.8 -> 430.2 ms (tools/exp_upd.sh). Without the two-phase panel the
       // confined panels became the bottleneck (447 ms).
       const char* sre = std::getenv("BR_SPLIT_ROWS");
-      const int64_t srows = sre ? std::atoll(sre) : 11264;
+      const int64_t srows = sre ? std::atoll(sre) : 10240;
       const bool sr = srows > 0;
       cudaStream_t gp = nullptr;
       int gps = 0;

@@ -768,7 +768,12 @@ int panel_qr(cudaStream_t st, Scratch& ws, DevBuf& pscratch, MatView P, MatView 
     // reads the leaves' diagonal blocks at multiples of 32
     const int64_t al = std::max<int64_t>(nbl, TAB);
     const int64_t h = std::max<int64_t>(al, cdiv(w / 2, al) * al);
-    if (w <= rec_width() || h >= w || j < rec_min_rows()) return right_looking(c0, c1);
+    // confined panels (phase 1 of the strict SM split) split once at 128 columns:
+    // on 16 SMs one K = 128 update of the right half beats the leaf-by-leaf
+    // updates it replaces (c4 panel class 215 -> 201 ms, tools/exp_env.sh)
+    const int64_t rw = (phase == 1) ? std::min<int64_t>(rec_width(), 128) : rec_width();
+    const int64_t rmin = (phase == 1) ? 0 : rec_min_rows();
+    if (w <= rw || h >= w || j < rmin) return right_looking(c0, c1);
     BR_CHECK(rec(c0, c0 + h));
     // T1 of the left half from its Gram matrix (leaves wrote the diagonal blocks)
     MatView Y1 = Y.sub(c0, c0, j - c0, h), T1 = T.sub(c0, c0, h, h);
