@@ -508,7 +508,10 @@ int tri_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int lo
         cudaEvent_t ev_lq = nullptr;
         auto issue_lq = [&]() -> int {  // LQ on the panel stream once its rows are updated
           if (!lookahead) return 0;
-          cudaStream_t ps = ws.pstream(jr);
+          // streamed input: the whole left update has been issued chunk by chunk
+          // before this point, so this LQ overlaps nothing - it runs its (same)
+          // two-phase plan on the whole device instead of the confined stream
+          cudaStream_t ps = chunked ? ws.panel : ws.pstream(jr);
           BR_CHECK(handoff(ps));
           BR_CHECK(lq(ps, ws.sk_panel, k, bq));
           ev_lq = mark_panel(ps);
