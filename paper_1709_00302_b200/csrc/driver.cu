@@ -653,6 +653,13 @@ int br_create(int device, br_handle_t* out) {
         h->ws.upd_sms = got;
         h->ws.upd_rows = 10240;
         if (const char* r = std::getenv("BR_UPD_ROWS")) h->ws.upd_rows = std::atoll(r);
+        if (sr && gp && !panel_clusters_fit(gp)) {  // this board's partition cannot hold a leaf cluster
+          cudaStreamDestroy(gp);
+          gp = nullptr;
+        }
+        if (std::getenv("BR_DEBUG_PARTITION"))
+          fprintf(stderr, "bandred: update partition %d SMs, panel partition %d SMs, strict split %s\n", got,
+                  gps, (sr && gp) ? "on" : "off");
         if (sr && gp) {
           h->ws.gpanel = gp;
           h->ws.green_sms = gps;

@@ -189,6 +189,7 @@ int panel_qr(cudaStream_t st, Scratch& sk, DevBuf& pscratch, MatView P, MatView 
              MatView T, MatView* W, int max_ctas = 0, Workspace* pws = nullptr,
              LeafMarks* marks = nullptr, int phase = 0);
 int64_t panel_scratch_doubles(int64_t b);
+bool panel_clusters_fit(cudaStream_t st);  // every tall-panel leaf cluster can be placed on st's SMs
 int t_from_gram(cudaStream_t st, const double* G, int64_t ldg, const double* tau, int64_t b,
                 double* T, int64_t ldt, bool diag_given = false);
 int house_gen_dev(cudaStream_t st, int64_t L, const double* x, double* v, double* tau_beta);

@@ -374,6 +374,49 @@ static int launch_leaf(cudaStream_t st, MatView P, MatView Y, double* tau, doubl
 
 }  // namespace br
 
+// Can `st` (a stream of the 16-SM green context) place the leaf clusters a
+// confined panel launches? The partition is asked for with the
+// max-potential-cluster-size split, but boards differ in their GPC layout: the
+// strict split is only enabled when every tall-panel leaf shape fits.
+namespace br {
+template <class K>
+static bool cluster_fits(K kern, int threads, size_t smem, cudaStream_t st) {
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  cfg.gridDim = dim3(LEAF_MAXC);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = LEAF_MAXC;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  const bool ok = cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n >= 1;
+  cudaGetLastError();
+  return ok;
+}
+template <int NB, int NW, int RPT, bool PAIR>
+static bool leaf2_fits(cudaStream_t st) {
+  constexpr int ROWS = (NW / (NB / 8)) * 32 * RPT;
+  const size_t smem = ((size_t)NB * (ROWS + 8) + 2 * (size_t)NB * (NB + 1)) * sizeof(double);
+  return cluster_fits(leaf2_kernel<NB, NW, RPT, PAIR>, NW * 32 + ((PAIR && NW <= 4) ? 32 : 0), smem, st);
+}
+bool panel_clusters_fit(cudaStream_t st) {
+  return leaf2_fits<16, 8, 8, true>(st) && leaf2_fits<32, 8, 8, true>(st) && leaf2_fits<16, 4, 8, true>(st) &&
+         leaf2_fits<8, 8, 8, false>(st) &&
+         cluster_fits(leaf_reg_kernel<4, 16, 256>, 256, (size_t)4 * 256 * 16 * sizeof(double), st) &&
+         cluster_fits(leaf_reg_kernel<2, 32, 256>, 256, (size_t)2 * 256 * 32 * sizeof(double), st);
+}
+}  // namespace br
+
 // Print and reset the leaf phase counters (collected when BR_LEAF_PROF is set;
 // development aid, not part of include/bandred_b200.h).
 extern "C" int br_leaf_prof_dump() {
