@@ -833,6 +833,15 @@ int band_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int f
       BR_CHECK(panels(ps, ws.sk_panel, tn, par ^ 1));
       ev_panels = ws_event(ws);
       BR_CUDA(cudaEventRecord(ev_panels, ps));
+      // the updates issued after this point overlap the panels: below the
+      // threshold they go to the SM-partitioned stream (Workspace::gupd)
+      cudaStream_t us = ws.ustream(i, true);
+      if (us != ws.main) {
+        cudaEvent_t e2 = ws_event(ws);
+        BR_CUDA(cudaEventRecord(e2, ws.main));
+        BR_CUDA(cudaStreamWaitEvent(us, e2, 0));
+        st = us;
+      }
       return 0;
     };
 
@@ -901,6 +910,12 @@ int band_reduce(Workspace& ws, int64_t m, int64_t n, int64_t w, int64_t b, int f
         BR_CHECK(ur(0, c1r, 0, jr));
         BR_CHECK(dsim(0, i, 0, jr));
       }
+    }
+    if (st != ws.main) {  // join the partitioned update stream
+      cudaEvent_t e2 = ws_event(ws);
+      BR_CUDA(cudaEventRecord(e2, st));
+      BR_CUDA(cudaStreamWaitEvent(ws.main, e2, 0));
+      st = ws.main;
     }
     if (has_next && !issued) BR_CHECK(panels(ws.main, ws.sk_main, tn, par ^ 1));
     BR_CHECK(band_out_flush(ws, bo, std::min(n, t.k + t.bp)));  // columns [0, k + bp) are final
